@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the HP-GWAS hot path on B200 (GLS solves / s), driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--m M] [--impl ours|reference]
+
+A step is one whole job over the rank's synthetic workload:
+  gls_create  (potrf of M + inverse, X~_L, y~, S_TL, b_T -- Alg. 5 lines 1,2,4,5,6; on rank 0,
+               then one NCCL broadcast of the shared state to the other ranks)
+  gls_solve_block over the rank's m SNPs resident in HBM (Alg. 5 line 3 + lines 7-11, fused).
+value = SNPs solved by all ranks / max-over-ranks device time (weak scaling: each rank owns a
+config-sized SNP range).  e2e = the same through the C ABI with HOST buffers (M, X_L, y and the
+rank's X_R in pinned host memory, b back to host) -- the double-buffered H2D stream of Alg. 8.
+
+--impl reference times the CPU oracle (oracle/, the only other place bench.py runs it) on a
+bounded sample of the same workload and prints the same JSON line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import gen  # noqa: E402
+
+METRIC = "GLS solves (SNPs)/sec at n=10^4, p=4; FP64 tensor-pipe % of peak, 1/2/4/8 B200"
+UNIT = "SNPs/s"
+# FP64 tensor (DMMA.8x8x4) peak measured on this pool's B200 by tools/probe (profiles/r01_probe.txt):
+# 37.10 TFLOP/s burst, 36.86 TFLOP/s sustained over 4 s.  MEASURED_PEAKS.json carries no FP64 figure.
+FP64_DMMA_PEAK_SUSTAINED = 36.86
+FP64_DMMA_PEAK_BURST = 37.10
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--m", type=int, default=0, help="SNPs per rank (default: the config's m)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=gen.DEFAULT_SEED)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                  "--format=csv,noheader,nounits", "-lms", "200"],
+                                 stdout=subprocess.PIPE, text=True)
+        except Exception:
+            return
+        while not self._stop.is_set():
+            line = p.stdout.readline()
+            if not line:
+                break
+            self.rows.append([x.strip() for x in line.split(",")])
+        p.terminate()
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 3 + k and r[3 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_sample(P, cfg, seed, nsnp, L=None):
+    """Time the CPU oracle (as it stands) on `nsnp` seeded SNPs of the workload."""
+    import oracle
+    t_chol = None
+    if L is None:
+        t0 = time.perf_counter()
+        L = oracle.cholesky(P.M)
+        t_chol = time.perf_counter() - t0
+    rng = np.random.default_rng(seed)
+    sel = np.sort(rng.choice(cfg.m, nsnp, replace=False))
+    XRs = np.concatenate([gen.make_XR(seed, cfg.n, int(i) * cfg.pR, cfg.pR) for i in sel])
+    t0 = time.perf_counter()
+    oracle.gls_sequence(L, P.XL, P.y, XRs, cfg.pR, sel=sel, xr_is_selected=True)
+    t_snp = time.perf_counter() - t0
+    return L, t_chol, t_snp
+
+
+def cpu_threads():
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = gen.CONFIGS[args.config]
+    m = args.m or cfg.m
+    P = gen.config_problem(cfg, seed=args.seed)
+    nsnp = 64 if cfg.n >= 5000 else 512
+    L, t_chol, _ = oracle_sample(P, cfg, args.seed, 8)
+    times = []
+    for s in range(args.warmup + args.steps):
+        _, _, t_snp = oracle_sample(P, cfg, args.seed + s, nsnp, L=L)
+        if s >= args.warmup:
+            times.append(t_snp)
+    rate = nsnp / statistics.median(times)
+    value = m / (t_chol + m / rate)
+    sample = ("oracle Cholesky of the full n=%d M (%.2f s, once) + %d seeded SNPs per step (Alg. 4 "
+              "per-problem steps); value = m / (t_chol + m / rate)" % (cfg.n, t_chol, nsnp))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "config%d" % args.config, "n": cfg.n, "pL": cfg.pL, "pR": cfg.pR,
+                       "m_per_rank": m},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1210_7325_b200 as pkg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pkg.load()
+
+    cfg = gen.CONFIGS[args.config]
+    n, pL, pR, p = cfg.n, cfg.pL, cfg.pR, cfg.p
+    m = args.m or cfg.m
+    col0 = rank * m * pR  # this rank's SNP range [rank*m, (rank+1)*m)
+
+    P = gen.config_problem(cfg, seed=args.seed)
+    Md = torch.from_numpy(P.M).cuda()
+    XLd = torch.from_numpy(np.ascontiguousarray(P.XL)).cuda()
+    yd = torch.from_numpy(P.y).cuda()
+    Xd = torch.empty((m * pR, n), dtype=torch.float64, device="cuda")
+    chunk = 65536
+    for c in range(0, m * pR, chunk):
+        k = min(chunk, m * pR - c)
+        pkg.gen_xr_device(args.seed, n, col0 + c, k, Xd[c:c + k])
+    b = torch.empty((m, p), dtype=torch.float64, device="cuda")
+    st = torch.empty(m, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    # a real (non-legacy) stream: the library's kernels are enqueued on it via gls_set_stream,
+    # so CUDA events recorded on it bracket exactly the fused kernel
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+
+    def make_ctx(Mx, XLx, yx):
+        if rank == 0:
+            ctx = pkg.Context(n, pL, pR, Mx, XLx, yx)
+        else:
+            ctx = pkg.Context(n, pL, pR, adopt=True)
+        if world > 1:
+            for t in ctx.shared_tensors():
+                dist.broadcast(t, src=0)
+            torch.cuda.synchronize()
+            if rank != 0:
+                ctx.commit_shared()
+        return ctx
+
+    kern_ms = []
+    create_ms = []
+    launches = [0]
+
+    def step(timed: bool):
+        tc = time.perf_counter()
+        ctx = make_ctx(Md, XLd, yd)
+        if timed:
+            create_ms.append(1e3 * (time.perf_counter() - tc))
+        ctx.set_stream(stream.cuda_stream)
+        k0 = torch.cuda.Event(enable_timing=True)
+        k1 = torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
+        ctx.solve_block(Xd, m, b, st, async_=True)
+        k1.record(stream)
+        ctx.sync()
+        if timed:
+            launches[0] += ctx.kernel_launches
+            k1.synchronize()
+            kern_ms.append(k0.elapsed_time(k1))
+        ctx.close()
+
+    for _ in range(args.warmup):
+        step(False)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = e0.elapsed_time(e1)
+    t = torch.tensor([total_ms, statistics.mean(kern_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kern_avg_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    value = world * m / (ms_per_step / 1e3)
+
+    # parity spot check of this run's output against the planted structure is in tests/; here only
+    # a sanity count of RankDeficient rows (seeded data has none).
+    n_bad = int(st.sum().item())
+
+    # ---- roofline of the dominant kernel (fused_trsm_gls), algorithmic n^2 flops per column
+    flops_per_launch = float(n) * n * m * pR
+    achieved_tf = flops_per_launch / (kern_avg_ms / 1e3) / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get("config%d" % args.config)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_DMMA_PEAK_SUSTAINED,
+                "unit": "TFLOP/s", "frac": achieved_tf / FP64_DMMA_PEAK_SUSTAINED, "traffic": traffic,
+                "kernel": "fused_trsm_gls_kernel", "kernel_ms": kern_avg_ms,
+                "create_ms": statistics.mean(create_ms),
+                "flops_per_launch": flops_per_launch,
+                "peak_source": "FP64 DMMA.8x8x4 microbenchmark on this pool's B200, 4 s sustained "
+                               "(profiles/r01_probe.txt); MEASURED_PEAKS.json has no FP64 entry"}
+
+    # ---- e2e: same job through the C ABI with host buffers (rank's X_R pinned in host memory)
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.empty((m * pR, n), dtype=torch.float64, pin_memory=True)
+        for c in range(0, m * pR, chunk):
+            k = min(chunk, m * pR - c)
+            Xh[c:c + k].copy_(Xd[c:c + k], non_blocking=False)
+        Mh = torch.from_numpy(P.M).pin_memory()
+        XLh = torch.from_numpy(np.ascontiguousarray(P.XL)).pin_memory()
+        yh = torch.from_numpy(P.y).pin_memory()
+        bh = torch.empty((m, p), dtype=torch.float64, pin_memory=True)
+        sh = torch.empty(m, dtype=torch.int32, pin_memory=True)
+        ref_b = b.cpu()
+
+        def e2e_step():
+            ctx = make_ctx(Mh, XLh, yh)
+            ctx.solve_block(Xh, m, bh, sh)
+            ctx.close()
+
+        for _ in range(1):
+            e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        dt = torch.tensor([(time.perf_counter() - t0) / args.steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        same = bool(torch.equal(bh, ref_b))
+        e2e = {"value": world * m / float(dt[0]), "unit": UNIT,
+               "h2d_bytes_per_step": int((n * n + n * (pL + 1) + m * pR * n) * 8),
+               "d2h_bytes_per_step": int(m * p * 8 + m * 4),
+               "bitwise_equal_to_device_run": same}
+        del Xh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nsnp = 64 if n >= 5000 else 512
+        L, t_chol, t_snp = oracle_sample(P, cfg, args.seed, nsnp)
+        rate = nsnp / t_snp
+        cpu = {"value": m / (t_chol + m / rate), "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+               "sample": "oracle Cholesky of the full n=%d M (%.2f s) + %d seeded SNPs of the workload "
+                         "(%.2f s); value = m / (t_chol + m / rate)" % (n, t_chol, nsnp, t_snp)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "config%d: n=%d pL=%d pR=%d, %d SNPs per GPU in HBM (rank r owns "
+                                       "SNPs [r*m, (r+1)*m))" % (args.config, n, pL, pR, m),
+                           "n": n, "pL": pL, "pR": pR, "m_per_rank": m, "seed": args.seed,
+                           "step": "gls_create (+NCCL broadcast) + gls_solve_block over all rank SNPs",
+                           "l2": "inputs larger than L2 (X_R %.1f GB per rank)" % (m * pR * n * 8 / 1e9)},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches[0],
+                "clocks": clk, "rank_deficient_rows": n_bad}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

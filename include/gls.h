@@ -1,0 +1,124 @@
+/*
+ * gls.h -- C ABI of libgls.so: the B200 hot path of HP-GWAS / OOC-HP-GWAS
+ * (Fabregat, Aulchenko, Bientinesi; arXiv 1210.7325).
+ *
+ * The library solves the sequence of generalized least-squares problems
+ *
+ *     b_i := (X_i^T M^{-1} X_i)^{-1} X_i^T M^{-1} y,      1 <= i <= m          (Eq. (1))
+ *
+ * with X_i = (X_L | X_Ri): X_L (n x pL) shared by all problems, X_Ri (n x pR) per problem
+ * (PAPER.md:53-54).  M is n x n SPD, X_i full rank, n > p = pL + pR, 1 <= p <= 20
+ * (PAPER.md:44-51).
+ *
+ *   gls_create       -- Alg. 5 lines 1, 2, 4, 5, 6: potrf of M, the shared
+ *                       transforms X~_L = L^{-1} X_L, y~ = L^{-1} y, S_TL = X~_L^T X~_L,
+ *                       b_T = X~_L^T y~.  Done once, on the GPU.
+ *   gls_solve_block  -- Alg. 5 line 3 + lines 7-11 on one block of problems (PAPER.md:314,
+ *                       318-322; Alg. 8 lines 9-14): the blocked triangular
+ *                       solve of the block's X_R columns fused with the per-problem assembly of
+ *                       S_i, b_i (Fig. 1) and the p x p SPD solve.  The whitened
+ *                       X~_R is never written to memory.  A host-resident X_R block is streamed
+ *                       to the device with double buffering (Alg. 8).
+ *
+ * All matrices are column-major FP64: element (r, c) of an n x k matrix is at r + c*n (leading
+ * dimension = n, no padding).  Problem i of a block uses columns [i*pR, (i+1)*pR) of X_R.
+ * Result record i is b_out[i*p .. i*p+p-1]: the pL coefficients of X_L first, then the pR
+ * coefficients of X_Ri, following the column order of X_i = (X_L | X_Ri) (reading A3).
+ *
+ * Pointers may be host or CUDA device pointers (detected with cudaPointerGetAttributes; host
+ * memory may be pinned or pageable -- pinned is required for copy/compute overlap).
+ *
+ * Errors are return codes; nothing is thrown across the ABI.  One context belongs to one CUDA
+ * device (the device current at gls_create) and must be used by one host thread at a time.
+ */
+#ifndef GLS_H_
+#define GLS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gls_ctx gls_ctx; /* opaque */
+
+enum {
+  GLS_OK = 0,
+  GLS_ERR_ARG = 1,     /* NULL pointer where one is required, bad flag value                 */
+  GLS_ERR_DIM = 2,     /* dimensions violate n > p, pL >= 0, pR >= 1, p <= 20, m_blk >= 1     */
+  GLS_ERR_NOT_SPD = 3, /* M is not SPD: a Cholesky pivot d_j <= 2^-52 * max_k M_kk (reading A5)*/
+  GLS_ERR_CUDA = 4,    /* a CUDA runtime/driver call failed; see gls_last_error               */
+  GLS_ERR_OOM = 5,     /* device or pinned-host allocation failed                             */
+  GLS_ERR_STATE = 6    /* context is in a failed state or not yet committed (adopt mode)      */
+};
+
+/* gls_create -- factor M and prepare the shared state (Alg. 5 lines 1,2,4,5,6).
+ *   n, pL, pR : dimensions; GLS_ERR_DIM unless n > pL+pR, pL >= 0, pR >= 1, pL+pR <= 20.
+ *   M         : n x n, column-major; only the lower triangle (r >= c) is read.
+ *   X_L       : n x pL column-major; may be NULL iff pL == 0.
+ *   y         : n observations.
+ *   out       : receives the context.
+ * Ownership: M, X_L, y are copied; the caller may free them on return.  The context owns all
+ * device memory it allocates (about 1.6*n^2*8 bytes transiently, 0.5*n^2*8 bytes resident).
+ * On GLS_ERR_NOT_SPD (and on any CUDA failure after the dims were validated) *out is set to a
+ * context in the failed state: only gls_failed_pivot, gls_last_error and gls_destroy are valid
+ * on it.  On GLS_ERR_ARG / GLS_ERR_DIM *out is set to NULL. */
+int gls_create(int64_t n, int32_t pL, int32_t pR, const double* M, const double* X_L,
+               const double* y, gls_ctx** out);
+
+/* gls_solve_block -- solve m_blk consecutive problems (Alg. 5 line 3 and lines 7-11; Alg. 8 l.9-14).
+ *   X_R   : n x (m_blk*pR) column-major, NOT modified (reading A9: the in-place X_R := L^{-1} X_R of
+ *           the paper is never materialised).  Device pointer: read in place.  Host pointer:
+ *           streamed through two device staging buffers (Alg. 8 double buffering).
+ *   m_blk : number of problems in the block, >= 1.
+ *   b_out : m_blk x p, record i at b_out + i*p (host or device).  A RankDeficient problem
+ *           (a pivot of its p x p Cholesky <= 1e-10 * S_jj, reading A4) gets a quiet-NaN record;
+ *           the other problems are unaffected.
+ * Synchronous: returns after b_out is written. */
+int gls_solve_block(gls_ctx* ctx, const double* X_R, int64_t m_blk, double* b_out);
+
+/* gls_solve_block_ex -- as gls_solve_block, plus
+ *   status_out : NULL, or m_blk int32 (host or device): 0 = OK, 1 = RankDeficient.
+ *   async      : 0 = return after b_out/status_out are written; 1 = return after enqueueing
+ *                on the context stream (device X_R) or after the last host chunk is enqueued
+ *                (host X_R); X_R, b_out and status_out stay borrowed until gls_sync. */
+int gls_solve_block_ex(gls_ctx* ctx, const double* X_R, int64_t m_blk, double* b_out,
+                       int32_t* status_out, int async);
+
+/* gls_sync -- wait until every enqueued solve of this context has completed. */
+int gls_sync(gls_ctx* ctx);
+
+/* gls_set_stream -- run the compute kernels on `stream` (a cudaStream_t of the context's device,
+ * e.g. torch.cuda.current_stream().cuda_stream); NULL restores the context's own stream. */
+int gls_set_stream(gls_ctx* ctx, void* stream);
+
+/* gls_set_block_cols -- columns per host->device chunk for host-resident X_R (the paper's block
+ * size); rounded to whole problems.  Default: 64 * (number of SMs) columns. */
+int gls_set_block_cols(gls_ctx* ctx, int64_t cols);
+
+/* gls_destroy -- free everything (NULL is a no-op).  Waits for outstanding work first. */
+void gls_destroy(gls_ctx* ctx);
+
+/* Diagnostics. */
+int64_t gls_failed_pivot(const gls_ctx* ctx);  /* 0-based failing pivot of M after NOT_SPD, else -1 */
+const char* gls_last_error(const gls_ctx* ctx); /* owned by ctx; "" when no error                  */
+const char* gls_error_string(int code);         /* static text for any return code                 */
+
+/* Multi-GPU replicate-then-shard.  The root rank calls
+ * gls_create; every other rank calls gls_create_adopt (allocates the shared state, computes
+ * nothing), receives the root's buffers listed by gls_shared_view (e.g. an NCCL broadcast over
+ * NVLink), then calls gls_commit_shared.  Afterwards all ranks are bitwise identical.
+ *   gls_shared_view: ptrs[k] (device pointers, owned by ctx), bytes[k]; *count = number of
+ *   buffers (<= 8).  Valid on a committed context (root) and on an adopt-mode context. */
+int gls_create_adopt(int64_t n, int32_t pL, int32_t pR, gls_ctx** out);
+int gls_shared_view(gls_ctx* ctx, void** ptrs, int64_t* bytes, int32_t* count);
+int gls_commit_shared(gls_ctx* ctx);
+
+/* Number of kernel launches this context issued so far (evidence counter for bench.py). */
+int64_t gls_kernel_launches(const gls_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GLS_H_ */

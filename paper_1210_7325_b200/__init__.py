@@ -1,0 +1,6 @@
+"""B200-native hot path of HP-GWAS / OOC-HP-GWAS (arXiv 1210.7325).
+
+`gls` is the ctypes binding of libgls.so (C ABI in include/gls.h); `build` compiles the
+in-tree CUDA libraries for sm_100a.  See DESIGN.md.
+"""
+from .gls import Context, GLSError, gen_xr_device, load  # noqa: F401

@@ -1,0 +1,140 @@
+// chol_inv.cu -- once-per-context factorisation: M = L L^T (potrf, Alg. 5 line 1)
+// and the explicit lower-triangular inverse T = L^{-1} that the hot kernel applies blockwise
+// (DESIGN.md "Design A: the blocked solve as a product with T").
+//
+// Recursive, all contractions on the FP64 tensor pipe through dgemm():
+//   chol_inv([[A11, .], [A21, A22]]):
+//     (L11, T11) = chol_inv(A11)
+//     L21  = A21 T11^T                 (= A21 L11^{-T}, the panel solve)
+//     A22 -= L21 L21^T                 (trailing SYRK, lower tiles only)
+//     (L22, T22) = chol_inv(A22)
+//     T21  = -T22 (L21 T11)            ([[L11,0],[L21,L22]]^{-1} = [[T11,0],[-T22 L21 T11, T22]])
+// Leaves (n <= 64) factor and invert one diagonal block inside one CTA.
+// NotSPD (reading A5): a pivot d_j <= 2^-52 * max_k M_kk records min(j) in st->fail.
+#include <climits>
+
+#include "gls_internal.cuh"
+
+namespace gls {
+namespace {
+
+constexpr int LEAF = 64;
+constexpr int LLD = LEAF + 1;
+
+__global__ void maxdiag_kernel(int64_t n, const double* A, int64_t ld, CholStatus* st) {
+  __shared__ double red[256];
+  double m = 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) m = fmax(m, A[k + k * ld]);
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    st->tol = ldexp(1.0, -52) * red[0];
+    st->fail = ULLONG_MAX;
+  }
+}
+
+// One CTA: Cholesky of the nb x nb diagonal block at A (lower read), then its inverse.
+// Writes L into A's lower triangle and T = L^{-1} (with explicit zeros above the diagonal).
+__global__ void __launch_bounds__(256) chol_inv_leaf(int nb, double* A, double* T, int64_t ld,
+                                                     int64_t goff, CholStatus* st) {
+  extern __shared__ double leaf_smem[];
+  double* L = leaf_smem;
+  double* Ti = leaf_smem + LEAF * LLD;
+  __shared__ int failed;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+    const int i = idx % nb, j = idx / nb;
+    L[i * LLD + j] = (i >= j) ? A[i + (int64_t)j * ld] : 0.0;
+  }
+  if (tid == 0) failed = 0;
+  __syncthreads();
+  const double tol = st->tol;
+  for (int j = 0; j < nb; ++j) {
+    if (tid == 0) {
+      const double d = L[j * LLD + j];
+      if (!(d > tol) || failed) {
+        if (!failed) atomicMin(&st->fail, (unsigned long long)(goff + j));
+        failed = 1;
+        L[j * LLD + j] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: poisons the rest
+      } else {
+        L[j * LLD + j] = sqrt(d);
+      }
+    }
+    __syncthreads();
+    const double ljj = L[j * LLD + j];
+    for (int i = j + 1 + tid; i < nb; i += blockDim.x) L[i * LLD + j] /= ljj;
+    __syncthreads();
+    const int r = nb - j - 1;
+    for (int idx = tid; idx < r * r; idx += blockDim.x) {
+      const int i = j + 1 + idx / r, k = j + 1 + idx % r;
+      if (k <= i) L[i * LLD + k] -= L[i * LLD + j] * L[k * LLD + j];
+    }
+    __syncthreads();
+  }
+  // T = L^{-1}: column j solves L t = e_j by forward substitution (rows j..nb-1).
+  for (int j = tid; j < nb; j += blockDim.x) {
+    for (int i = 0; i < j; ++i) Ti[i * LLD + j] = 0.0;
+    for (int i = j; i < nb; ++i) {
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int k = j; k < i; ++k) s -= L[i * LLD + k] * Ti[k * LLD + j];
+      Ti[i * LLD + j] = s / L[i * LLD + i];
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+    const int i = idx % nb, j = idx / nb;
+    if (i >= j) A[i + (int64_t)j * ld] = L[i * LLD + j];
+    T[i + (int64_t)j * ld] = Ti[i * LLD + j];
+  }
+}
+
+void chol_inv_rec(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, int64_t goff,
+                  CholStatus* st, int64_t* lc) {
+  if (n <= LEAF) {
+    constexpr int kLeafSmem = 2 * LEAF * LLD * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
+      attr = true;
+    }
+    chol_inv_leaf<<<1, 256, kLeafSmem, s>>>((int)n, A, T, ld, goff, st);
+    if (lc) ++*lc;
+    return;
+  }
+  const int64_t nblk = (n + LEAF - 1) / LEAF;
+  const int64_t h1 = LEAF * ((nblk + 1) / 2), h2 = n - h1;
+  double* A11 = A;
+  double* A21 = A + h1;
+  double* A22 = A + h1 + h1 * ld;
+  double* T11 = T;
+  double* T21 = T + h1;
+  double* T22 = T + h1 + h1 * ld;
+  chol_inv_rec(s, h1, A11, T11, ld, goff, st, lc);
+  // L21 = A21 T11^T  -> stored in T21's (still unused) place
+  dgemm(s, h2, h1, h1, 1.0, A21, ld, 'N', T11, ld, 'T', 0.0, T21, ld, GEMM_KMAX_COL, lc);
+  // A22 -= L21 L21^T (lower)
+  dgemm(s, h2, h2, h1, -1.0, T21, ld, 'N', T21, ld, 'T', 1.0, A22, ld, GEMM_LOWER_C, lc);
+  chol_inv_rec(s, h2, A22, T22, ld, goff + h1, st, lc);
+  // Y = L21 T11 -> A21's place;  T21 = -T22 Y
+  dgemm(s, h2, h1, h1, 1.0, T21, ld, 'N', T11, ld, 'N', 0.0, A21, ld, GEMM_KMIN_COL, lc);
+  dgemm(s, h2, h1, h2, -1.0, T22, ld, 'N', A21, ld, 'N', 0.0, T21, ld, GEMM_KMAX_ROW, lc);
+}
+
+}  // namespace
+
+void chol_prepare(cudaStream_t s, int64_t n, const double* A, int64_t ld, CholStatus* st,
+                  int64_t* lc) {
+  maxdiag_kernel<<<1, 256, 0, s>>>(n, A, ld, st);
+  if (lc) ++*lc;
+}
+
+void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholStatus* st,
+              int64_t* lc) {
+  chol_inv_rec(s, n, A, T, ld, 0, st, lc);
+}
+
+}  // namespace gls

@@ -1,0 +1,471 @@
+// gls_api.cu -- the C ABI (include/gls.h) and the host runtime around the kernels:
+// context lifetime, pointer-kind dispatch, the once-per-context setup (Alg. 5 lines 1,2,4,5,6;
+// PAPER.md:311-317) and the double-buffered host->device stream of X_R blocks
+// (Alg. 8 ooc-hp-gwas; workspaces fig:workspaces PAPER.md:633-653).
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/gls.h"
+#include "gls_internal.cuh"
+
+using namespace gls;
+
+namespace {
+enum CtxState { ST_OK = 0, ST_FAILED = 1, ST_ADOPT = 2 };
+}
+
+struct gls_ctx {
+  int device = 0;
+  int64_t n = 0;
+  int pL = 0, pR = 0, p = 0, NW = 1;
+  int64_t NB = 0;
+  int state = ST_FAILED;
+  int64_t failed_pivot = -1;
+  std::string err;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr, stream = nullptr, h2d = nullptr, d2h = nullptr;
+  // shared state (replicated across GPUs)
+  double* Tpk = nullptr;
+  size_t Tpk_bytes = 0;
+  double* Wpk = nullptr;
+  size_t Wpk_bytes = 0;
+  double* G = nullptr;
+  size_t G_bytes = 0;
+  // host-streaming workspaces (two, swapping roles -- fig:workspaces)
+  int64_t block_cols = 0;
+  int64_t stage_cols = 0, ld_stage = 0;
+  double* stage[2] = {nullptr, nullptr};
+  double* bstage[2] = {nullptr, nullptr};
+  int32_t* sstage[2] = {nullptr, nullptr};
+  int64_t bstage_groups = 0;
+  cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+  uint64_t seq = 0;
+  // device scratch for host outputs of device-resident X_R
+  double* bscratch = nullptr;
+  int32_t* sscratch = nullptr;
+  int64_t scratch_groups = 0;
+  int64_t launches = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int fail_cuda(gls_ctx* c, cudaError_t e, const char* what) {
+  if (c) {
+    c->err = std::string(what) + ": " + cudaGetErrorString(e);
+  }
+  cudaGetLastError();
+  return e == cudaErrorMemoryAllocation ? GLS_ERR_OOM : GLS_ERR_CUDA;
+}
+
+#define CK(ctx, call)                                          \
+  do {                                                         \
+    cudaError_t e_ = (call);                                   \
+    if (e_ != cudaSuccess) return fail_cuda((ctx), e_, #call); \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int check_dims(int64_t n, int32_t pL, int32_t pR) {
+  if (pL < 0 || pR < 1) return GLS_ERR_DIM;
+  const int64_t p = (int64_t)pL + pR;
+  if (p > 20 || n <= p || n > (int64_t)INT32_MAX / 2) return GLS_ERR_DIM;
+  return GLS_OK;
+}
+
+int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
+  c->n = n;
+  c->pL = pL;
+  c->pR = pR;
+  c->p = pL + pR;
+  c->NW = (pL + 1 + 7) / 8;
+  c->NB = (n + kNB - 1) / kNB;
+  CK(c, cudaGetDevice(&c->device));
+  CK(c, cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  CK(c, cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+  CK(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+  CK(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+  c->stream = c->own_stream;
+  for (int k = 0; k < 2; ++k) {
+    CK(c, cudaEventCreateWithFlags(&c->ev_h2d[k], cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_comp[k], cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_d2h[k], cudaEventDisableTiming));
+  }
+  const PanelGeom pg = panel_geom(pR);
+  c->block_cols = (int64_t)c->num_sms * pg.cpp;  // one wave of panels per chunk
+  c->Tpk_bytes = (size_t)tpk_total_tiles(c->NB) * kTileDoubles * sizeof(double);
+  c->Wpk_bytes = (size_t)c->NB * wpk_rb_doubles(c->NW) * sizeof(double);
+  c->G_bytes = (size_t)(pL + 1) * (pL + 1) * sizeof(double);
+  CK(c, cudaMalloc(&c->Tpk, c->Tpk_bytes));
+  CK(c, cudaMalloc(&c->Wpk, c->Wpk_bytes));
+  CK(c, cudaMalloc(&c->G, c->G_bytes));
+  return GLS_OK;
+}
+
+void free_staging(gls_ctx* c) {
+  for (int k = 0; k < 2; ++k) {
+    if (c->stage[k]) cudaFree(c->stage[k]);
+    if (c->bstage[k]) cudaFree(c->bstage[k]);
+    if (c->sstage[k]) cudaFree(c->sstage[k]);
+    c->stage[k] = c->bstage[k] = nullptr;
+    c->sstage[k] = nullptr;
+  }
+  c->stage_cols = 0;
+  c->bstage_groups = 0;
+}
+
+// Setup: Alg. 5 lines 1 (potrf), 2 + 4 (X~_L, y~), 5 (S_TL), 6 (b_T).
+int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
+  const int64_t n = c->n;
+  const int pL = c->pL;
+  cudaStream_t s = c->stream;
+  double *A = nullptr, *T = nullptr, *B = nullptr, *W = nullptr;
+  CholStatus* st = nullptr;
+  CholStatus hst;
+  int rc = GLS_OK;
+  auto cleanup = [&]() {
+    if (A) cudaFree(A);
+    if (T) cudaFree(T);
+    if (B) cudaFree(B);
+    if (W) cudaFree(W);
+    if (st) cudaFree(st);
+  };
+#define CKS(call)                              \
+  do {                                         \
+    cudaError_t e_ = (call);                   \
+    if (e_ != cudaSuccess) {                   \
+      rc = fail_cuda(c, e_, #call);            \
+      cudaStreamSynchronize(s);                \
+      cleanup();                               \
+      return rc;                               \
+    }                                          \
+  } while (0)
+  const size_t nn = (size_t)n * (size_t)n * sizeof(double);
+  CKS(cudaMalloc(&A, nn));
+  CKS(cudaMalloc(&T, nn));
+  CKS(cudaMalloc(&B, (size_t)n * (pL + 1) * sizeof(double)));
+  CKS(cudaMalloc(&W, (size_t)n * (pL + 1) * sizeof(double)));
+  CKS(cudaMalloc(&st, sizeof(CholStatus)));
+  CKS(cudaMemcpyAsync(A, M, nn, cudaMemcpyDefault, s));
+  CKS(cudaMemsetAsync(T, 0, nn, s));
+  chol_prepare(s, n, A, n, st, &c->launches);
+  chol_inv(s, n, A, T, n, st, &c->launches);
+  CKS(cudaGetLastError());
+  CKS(cudaMemcpyAsync(&hst, st, sizeof hst, cudaMemcpyDeviceToHost, s));
+  CKS(cudaStreamSynchronize(s));
+  if (hst.fail != ULLONG_MAX) {
+    c->failed_pivot = (int64_t)hst.fail;
+    char buf[128];
+    snprintf(buf, sizeof buf, "M is not SPD: Cholesky pivot %lld <= 2^-52 * max diag",
+             (long long)hst.fail);
+    c->err = buf;
+    cleanup();
+    return GLS_ERR_NOT_SPD;
+  }
+  // B = [X_L | y];  W = T B = [X~_L | y~];  G = W^T W  (S_TL and b_T)
+  if (pL > 0) CKS(cudaMemcpyAsync(B, X_L, (size_t)n * pL * sizeof(double), cudaMemcpyDefault, s));
+  CKS(cudaMemcpyAsync(B + (size_t)n * pL, y, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
+  dgemm(s, n, pL + 1, n, 1.0, T, n, 'N', B, n, 'N', 0.0, W, n, GEMM_KMAX_ROW, &c->launches);
+  dgemm(s, pL + 1, pL + 1, n, 1.0, W, n, 'T', W, n, 'N', 0.0, c->G, pL + 1, 0, &c->launches);
+  pack_T(s, T, n, n, c->NB, c->Tpk, &c->launches);
+  pack_W(s, W, n, n, pL + 1, c->NB, c->NW, c->Wpk, &c->launches);
+  CKS(cudaGetLastError());
+  CKS(cudaStreamSynchronize(s));
+  cleanup();
+#undef CKS
+  return GLS_OK;
+}
+
+int ensure_scratch(gls_ctx* c, int64_t groups) {
+  if (groups <= c->scratch_groups) return GLS_OK;
+  if (c->bscratch) cudaFree(c->bscratch);
+  if (c->sscratch) cudaFree(c->sscratch);
+  c->bscratch = nullptr;
+  c->sscratch = nullptr;
+  c->scratch_groups = 0;
+  CK(c, cudaMalloc(&c->bscratch, (size_t)groups * c->p * sizeof(double)));
+  CK(c, cudaMalloc(&c->sscratch, (size_t)groups * sizeof(int32_t)));
+  c->scratch_groups = groups;
+  return GLS_OK;
+}
+
+int ensure_staging(gls_ctx* c, int64_t chunk_groups) {
+  const int64_t cols = chunk_groups * c->pR;
+  const int64_t ld = c->n + (c->n & 1);
+  if (c->stage_cols >= cols && c->ld_stage == ld && c->bstage_groups >= chunk_groups) return GLS_OK;
+  CK(c, cudaDeviceSynchronize());
+  free_staging(c);
+  for (int k = 0; k < 2; ++k) {
+    CK(c, cudaMalloc(&c->stage[k], (size_t)ld * cols * sizeof(double)));
+    CK(c, cudaMalloc(&c->bstage[k], (size_t)chunk_groups * c->p * sizeof(double)));
+    CK(c, cudaMalloc(&c->sstage[k], (size_t)chunk_groups * sizeof(int32_t)));
+  }
+  c->stage_cols = cols;
+  c->ld_stage = ld;
+  c->bstage_groups = chunk_groups;
+  return GLS_OK;
+}
+
+int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt) {
+  SolveArgs a;
+  a.X = X;
+  a.ldx = ldx;
+  a.n = c->n;
+  a.NB = c->NB;
+  a.pL = c->pL;
+  a.pR = c->pR;
+  a.m_blk = groups;
+  a.Tpk = c->Tpk;
+  a.Wpk = c->Wpk;
+  a.G = c->G;
+  a.b_out = b;
+  a.status_out = stt;
+  std::string msg;
+  cudaError_t e = launch_fused_trsm_gls(c->stream, a, c->num_sms, &msg, &c->launches);
+  if (e != cudaSuccess) {
+    c->err = msg;
+    cudaGetLastError();
+    return GLS_ERR_CUDA;
+  }
+  return GLS_OK;
+}
+
+// Alg. 8 with host DRAM -> HBM in place of disk -> RAM: chunk j+1 is copied
+// into workspace (j+1)%2 on the h2d stream while chunk j is computed from workspace j%2; b of
+// chunk j is copied back on the d2h stream.  Event waits reproduce the algorithm's two waits:
+// "wait(current X_blk)" (compute waits ev_h2d) and "wait(previous b_blk)" (workspace reuse waits
+// ev_comp / ev_d2h of the chunk that used it two iterations ago).
+int solve_streamed(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out, bool b_dev,
+                   int32_t* status_out, bool s_dev) {
+  const int pR = c->pR, p = c->p;
+  const int64_t n = c->n;
+  int64_t chunk_groups = c->block_cols / pR;
+  if (chunk_groups < 1) chunk_groups = 1;
+  if (chunk_groups > m_blk) chunk_groups = m_blk;
+  int rc = ensure_staging(c, chunk_groups);
+  if (rc) return rc;
+  const int64_t ld = c->ld_stage;
+  for (int64_t g0 = 0; g0 < m_blk; g0 += chunk_groups) {
+    const int64_t gc = (m_blk - g0 < chunk_groups) ? m_blk - g0 : chunk_groups;
+    const int buf = (int)(c->seq++ & 1);
+    const double* src = X_R + (size_t)g0 * pR * n;
+    CK(c, cudaStreamWaitEvent(c->h2d, c->ev_comp[buf], 0));
+    if (ld == n)
+      CK(c, cudaMemcpyAsync(c->stage[buf], src, (size_t)n * gc * pR * sizeof(double), cudaMemcpyDefault,
+                            c->h2d));
+    else
+      CK(c, cudaMemcpy2DAsync(c->stage[buf], ld * sizeof(double), src, n * sizeof(double),
+                              n * sizeof(double), gc * pR, cudaMemcpyDefault, c->h2d));
+    CK(c, cudaEventRecord(c->ev_h2d[buf], c->h2d));
+    CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d[buf], 0));
+    CK(c, cudaStreamWaitEvent(c->stream, c->ev_d2h[buf], 0));
+    double* bdst = b_dev ? b_out + (size_t)g0 * p : c->bstage[buf];
+    int32_t* sdst = status_out ? (s_dev ? status_out + g0 : c->sstage[buf]) : nullptr;
+    rc = run_kernel(c, c->stage[buf], ld, gc, bdst, sdst);
+    if (rc) return rc;
+    CK(c, cudaEventRecord(c->ev_comp[buf], c->stream));
+    if (!b_dev || (status_out && !s_dev)) {
+      CK(c, cudaStreamWaitEvent(c->d2h, c->ev_comp[buf], 0));
+      if (!b_dev)
+        CK(c, cudaMemcpyAsync(b_out + (size_t)g0 * p, c->bstage[buf], (size_t)gc * p * sizeof(double),
+                              cudaMemcpyDeviceToHost, c->d2h));
+      if (status_out && !s_dev)
+        CK(c, cudaMemcpyAsync(status_out + g0, c->sstage[buf], (size_t)gc * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, c->d2h));
+      CK(c, cudaEventRecord(c->ev_d2h[buf], c->d2h));
+    }
+  }
+  return GLS_OK;
+}
+
+int sync_all(gls_ctx* c) {
+  CK(c, cudaStreamSynchronize(c->h2d));
+  CK(c, cudaStreamSynchronize(c->stream));
+  CK(c, cudaStreamSynchronize(c->d2h));
+  return GLS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gls_error_string(int code) {
+  switch (code) {
+    case GLS_OK: return "GLS_OK: success";
+    case GLS_ERR_ARG: return "GLS_ERR_ARG: invalid argument (NULL pointer or bad flag)";
+    case GLS_ERR_DIM: return "GLS_ERR_DIM: dimensions must satisfy n > pL+pR, pL >= 0, pR >= 1, pL+pR <= 20, m_blk >= 1";
+    case GLS_ERR_NOT_SPD: return "GLS_ERR_NOT_SPD: M is not symmetric positive definite";
+    case GLS_ERR_CUDA: return "GLS_ERR_CUDA: CUDA error (see gls_last_error)";
+    case GLS_ERR_OOM: return "GLS_ERR_OOM: out of device or pinned memory";
+    case GLS_ERR_STATE: return "GLS_ERR_STATE: context failed or not committed";
+    default: return "unknown gls error code";
+  }
+}
+
+int gls_create(int64_t n, int32_t pL, int32_t pR, const double* M, const double* X_L,
+               const double* y, gls_ctx** out) {
+  if (!out) return GLS_ERR_ARG;
+  *out = nullptr;
+  if (!M || !y || (pL > 0 && !X_L)) return GLS_ERR_ARG;
+  int rc = check_dims(n, pL, pR);
+  if (rc) return rc;
+  gls_ctx* c = new gls_ctx();
+  *out = c;
+  rc = ctx_init(c, n, pL, pR);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  rc = ctx_setup(c, M, X_L, y);
+  if (rc) return rc;
+  c->state = ST_OK;
+  return GLS_OK;
+}
+
+int gls_create_adopt(int64_t n, int32_t pL, int32_t pR, gls_ctx** out) {
+  if (!out) return GLS_ERR_ARG;
+  *out = nullptr;
+  int rc = check_dims(n, pL, pR);
+  if (rc) return rc;
+  gls_ctx* c = new gls_ctx();
+  *out = c;
+  rc = ctx_init(c, n, pL, pR);
+  if (rc) return rc;
+  c->state = ST_ADOPT;
+  return GLS_OK;
+}
+
+int gls_shared_view(gls_ctx* c, void** ptrs, int64_t* bytes, int32_t* count) {
+  if (!c || !ptrs || !bytes || !count) return GLS_ERR_ARG;
+  if (c->state == ST_FAILED) return GLS_ERR_STATE;
+  ptrs[0] = c->Tpk;
+  bytes[0] = (int64_t)c->Tpk_bytes;
+  ptrs[1] = c->Wpk;
+  bytes[1] = (int64_t)c->Wpk_bytes;
+  ptrs[2] = c->G;
+  bytes[2] = (int64_t)c->G_bytes;
+  *count = 3;
+  return GLS_OK;
+}
+
+int gls_commit_shared(gls_ctx* c) {
+  if (!c) return GLS_ERR_ARG;
+  if (c->state == ST_FAILED) return GLS_ERR_STATE;
+  DeviceGuard g(c->device);
+  CK(c, cudaDeviceSynchronize());
+  c->state = ST_OK;
+  return GLS_OK;
+}
+
+int gls_solve_block_ex(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out,
+                       int32_t* status_out, int async) {
+  if (!c) return GLS_ERR_ARG;
+  if (c->state != ST_OK) return GLS_ERR_STATE;
+  if (!X_R || !b_out || (async != 0 && async != 1)) return GLS_ERR_ARG;
+  if (m_blk < 1) return GLS_ERR_DIM;
+  DeviceGuard g(c->device);
+  c->err.clear();
+  const bool x_dev = is_device_ptr(X_R);
+  const bool b_dev = is_device_ptr(b_out);
+  const bool s_dev = status_out ? is_device_ptr(status_out) : false;
+  int rc;
+  const bool direct = x_dev && (c->n % 2 == 0) && (((uintptr_t)X_R & 15) == 0);
+  if (direct) {
+    double* bdst = b_out;
+    int32_t* sdst = status_out;
+    if (!b_dev || (status_out && !s_dev)) {
+      rc = ensure_scratch(c, m_blk);
+      if (rc) return rc;
+      if (!b_dev) bdst = c->bscratch;
+      if (status_out && !s_dev) sdst = c->sscratch;
+    }
+    rc = run_kernel(c, X_R, c->n, m_blk, bdst, sdst);
+    if (rc) return rc;
+    if (!b_dev)
+      CK(c, cudaMemcpyAsync(b_out, bdst, (size_t)m_blk * c->p * sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream));
+    if (status_out && !s_dev)
+      CK(c, cudaMemcpyAsync(status_out, sdst, (size_t)m_blk * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                            c->stream));
+  } else {
+    rc = solve_streamed(c, X_R, m_blk, b_out, b_dev, status_out, s_dev);
+    if (rc) return rc;
+  }
+  if (!async) return sync_all(c);
+  return GLS_OK;
+}
+
+int gls_solve_block(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out) {
+  return gls_solve_block_ex(c, X_R, m_blk, b_out, nullptr, 0);
+}
+
+int gls_sync(gls_ctx* c) {
+  if (!c) return GLS_ERR_ARG;
+  DeviceGuard g(c->device);
+  return sync_all(c);
+}
+
+int gls_set_stream(gls_ctx* c, void* stream) {
+  if (!c) return GLS_ERR_ARG;
+  c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+  return GLS_OK;
+}
+
+int gls_set_block_cols(gls_ctx* c, int64_t cols) {
+  if (!c) return GLS_ERR_ARG;
+  if (cols < 1) return GLS_ERR_DIM;
+  c->block_cols = cols;
+  return GLS_OK;
+}
+
+void gls_destroy(gls_ctx* c) {
+  if (!c) return;
+  DeviceGuard g(c->device);
+  if (c->h2d) cudaStreamSynchronize(c->h2d);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->d2h) cudaStreamSynchronize(c->d2h);
+  free_staging(c);
+  if (c->bscratch) cudaFree(c->bscratch);
+  if (c->sscratch) cudaFree(c->sscratch);
+  if (c->Tpk) cudaFree(c->Tpk);
+  if (c->Wpk) cudaFree(c->Wpk);
+  if (c->G) cudaFree(c->G);
+  for (int k = 0; k < 2; ++k) {
+    if (c->ev_h2d[k]) cudaEventDestroy(c->ev_h2d[k]);
+    if (c->ev_comp[k]) cudaEventDestroy(c->ev_comp[k]);
+    if (c->ev_d2h[k]) cudaEventDestroy(c->ev_d2h[k]);
+  }
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
+  cudaGetLastError();
+  delete c;
+}
+
+int64_t gls_failed_pivot(const gls_ctx* c) { return c ? c->failed_pivot : -1; }
+
+const char* gls_last_error(const gls_ctx* c) { return c ? c->err.c_str() : ""; }
+
+int64_t gls_kernel_launches(const gls_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// gls_internal.cuh -- internal declarations shared by the libgls.so translation units.
+// Nothing here is visible through the C ABI (include/gls.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace gls {
+
+// ---------------------------------------------------------------- hot-kernel tiling constants
+// Row block of T / z handled per epilogue ("nb" in DESIGN.md), K extent per pipeline stage.
+constexpr int kNB = 128;         // z rows per row block (4 warp slices x 32)
+constexpr int kKT = 16;          // K per stage (one 128-byte TMA swizzle span of doubles)
+constexpr int kKTPerRB = kNB / kKT;
+constexpr int kTileDoubles = kNB * kKT;  // packed T tile: 2048 doubles = 16 KiB
+constexpr int kMaxPanelCols = 64;        // 2 warps x 32 columns
+
+// Packed-T tile index of (row block i, K tile kt): row block i holds K tiles 0..8(i+1)-1.
+__host__ __device__ inline int64_t tpk_tile_offset(int64_t i) { return 4 * i * (i + 1); }
+inline int64_t tpk_total_tiles(int64_t NB) { return 4 * NB * (NB + 1); }
+// Packed W per row block: 4 slices x NW x 4 subtiles x 32 lanes x 2 doubles.
+inline int64_t wpk_rb_doubles(int NW) { return 1024 * (int64_t)NW; }
+
+// Hot-kernel geometry for a given pR: groups never straddle a warp.
+struct PanelGeom {
+  int gw;   // problems (groups) per warp
+  int cpw;  // columns per warp = gw * pR (<= 32)
+  int cpp;  // columns per panel = 2 * cpw
+  int gpp;  // groups per panel = 2 * gw
+  bool full_gram;  // groups straddle 8-column MMA tiles (pR does not divide 8)
+};
+inline PanelGeom panel_geom(int pR) {
+  PanelGeom g;
+  g.gw = 32 / pR;
+  g.cpw = g.gw * pR;
+  g.cpp = 2 * g.cpw;
+  g.gpp = 2 * g.gw;
+  g.full_gram = (8 % pR) != 0;
+  return g;
+}
+
+// ---------------------------------------------------------------- generic FP64 DMMA GEMM
+enum GemmFlags : int {
+  GEMM_KMAX_ROW = 1,   // op(A) lower triangular: k < r0 + BM
+  GEMM_KMAX_COL = 2,   // op(B) upper triangular: k < c0 + BN
+  GEMM_KMIN_COL = 4,   // op(B) lower triangular: k >= c0
+  GEMM_LOWER_C = 8,    // only tiles intersecting the lower triangle of C
+};
+// C[M x N] = alpha * op(A) * op(B) + beta * C, column-major.  op = 'N' or 'T'.
+void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+           int64_t lda, char opA, const double* B, int64_t ldb, char opB, double beta, double* C,
+           int64_t ldc, int flags, int64_t* launch_counter);
+
+// ---------------------------------------------------------------- setup: Cholesky + inverse
+// In place: on return T (n x n, lower, ld) holds L^{-1} of M = L L^T; A (M on entry) is destroyed.
+// T must be zero-initialised.  tol_fail: device {double tol; unsigned long long fail_pivot}.
+struct CholStatus {
+  double tol;
+  unsigned long long fail;  // ULLONG_MAX when no pivot failed
+};
+void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholStatus* st,
+              int64_t* launch_counter);
+void chol_prepare(cudaStream_t s, int64_t n, const double* A, int64_t ld, CholStatus* st,
+                  int64_t* launch_counter);
+
+// ---------------------------------------------------------------- packing + hot kernel
+void pack_T(cudaStream_t s, const double* T, int64_t ld, int64_t n, int64_t NB, double* Tpk,
+            int64_t* launch_counter);
+void pack_W(cudaStream_t s, const double* W, int64_t ld, int64_t n, int ncolsW, int64_t NB, int NW,
+            double* Wpk, int64_t* launch_counter);
+
+struct SolveArgs {
+  const double* X;      // X_R block, column-major, leading dimension ldx (device)
+  int64_t ldx;          // >= n, even
+  int64_t n;
+  int64_t NB;
+  int pL, pR;
+  int64_t m_blk;
+  const double* Tpk;
+  const double* Wpk;
+  const double* G;      // (pL+1) x (pL+1): S_TL = G[0:pL,0:pL], b_T = G[0:pL, pL]
+  double* b_out;        // device
+  int32_t* status_out;  // device or nullptr
+};
+// Returns cudaSuccess or the launch error; msg receives a description on failure.
+cudaError_t launch_fused_trsm_gls(cudaStream_t s, const SolveArgs& a, int num_sms, std::string* msg,
+                                  int64_t* launch_counter);
+
+}  // namespace gls

@@ -1,0 +1,207 @@
+"""Thin ctypes binding of libgls.so (include/gls.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels.  There is no CPU fallback:
+if libgls.so is missing or no CUDA device is present, calls raise GLSError.
+
+Array arguments may be torch tensors (CPU, pinned CPU or CUDA; float64 / int32, contiguous)
+or numpy arrays (host).  Column-major n x k matrices are passed as contiguous arrays of
+shape (k, n): row j of the array is column j of the matrix.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import build as _build
+
+GLS_OK = 0
+GLS_ERR_ARG = 1
+GLS_ERR_DIM = 2
+GLS_ERR_NOT_SPD = 3
+GLS_ERR_CUDA = 4
+GLS_ERR_OOM = 5
+GLS_ERR_STATE = 6
+
+ABI_SYMBOLS = (
+    "gls_create", "gls_solve_block", "gls_solve_block_ex", "gls_sync", "gls_set_stream",
+    "gls_set_block_cols", "gls_destroy", "gls_failed_pivot", "gls_last_error",
+    "gls_error_string", "gls_create_adopt", "gls_shared_view", "gls_commit_shared",
+    "gls_kernel_launches",
+)
+
+
+class GLSError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+_lib = None
+_gen = None
+
+
+def load(build_if_missing: bool = True):
+    """Load libgls.so (building it in-tree with nvcc if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.lib_path("libgls.so")
+    if not os.path.exists(path) and build_if_missing:
+        _build.build()
+    if not os.path.exists(path):
+        raise GLSError(GLS_ERR_CUDA, "libgls.so not built (python -m paper_1210_7325_b200.build)")
+    L = ctypes.CDLL(path)
+    vp, i64, i32, dp = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+    L.gls_create.argtypes = [i64, i32, i32, dp, dp, dp, ctypes.POINTER(vp)]
+    L.gls_create.restype = ctypes.c_int
+    L.gls_create_adopt.argtypes = [i64, i32, i32, ctypes.POINTER(vp)]
+    L.gls_create_adopt.restype = ctypes.c_int
+    L.gls_solve_block.argtypes = [vp, dp, i64, dp]
+    L.gls_solve_block.restype = ctypes.c_int
+    L.gls_solve_block_ex.argtypes = [vp, dp, i64, dp, dp, ctypes.c_int]
+    L.gls_solve_block_ex.restype = ctypes.c_int
+    L.gls_sync.argtypes = [vp]
+    L.gls_sync.restype = ctypes.c_int
+    L.gls_set_stream.argtypes = [vp, vp]
+    L.gls_set_stream.restype = ctypes.c_int
+    L.gls_set_block_cols.argtypes = [vp, i64]
+    L.gls_set_block_cols.restype = ctypes.c_int
+    L.gls_destroy.argtypes = [vp]
+    L.gls_destroy.restype = None
+    L.gls_failed_pivot.argtypes = [vp]
+    L.gls_failed_pivot.restype = i64
+    L.gls_last_error.argtypes = [vp]
+    L.gls_last_error.restype = ctypes.c_char_p
+    L.gls_error_string.argtypes = [ctypes.c_int]
+    L.gls_error_string.restype = ctypes.c_char_p
+    L.gls_shared_view.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(i64), ctypes.POINTER(i32)]
+    L.gls_shared_view.restype = ctypes.c_int
+    L.gls_commit_shared.argtypes = [vp]
+    L.gls_commit_shared.restype = ctypes.c_int
+    L.gls_kernel_launches.argtypes = [vp]
+    L.gls_kernel_launches.restype = i64
+    _lib = L
+    return L
+
+
+def load_gen():
+    """libglsgen_dev.so: device genotype generator (test / bench input only)."""
+    global _gen
+    if _gen is None:
+        path = _build.lib_path("libglsgen_dev.so")
+        if not os.path.exists(path):
+            _build.build()
+        G = ctypes.CDLL(path)
+        G.glsgen_dev_xr.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64,
+                                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        G.glsgen_dev_xr.restype = ctypes.c_int
+        _gen = G
+    return _gen
+
+
+def _ptr(a, dtype: str = "float64"):
+    """Raw pointer of a torch tensor / numpy array (must be contiguous, right dtype); None -> NULL."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):  # torch
+        assert a.is_contiguous(), "tensor must be contiguous"
+        assert str(a.dtype).endswith(dtype), "expected %s, got %s" % (dtype, a.dtype)
+        return a.data_ptr()
+    import numpy as np
+    assert isinstance(a, np.ndarray) and a.flags.c_contiguous and a.dtype == np.dtype(dtype)
+    return a.ctypes.data
+
+
+def error_string(code: int) -> str:
+    return load().gls_error_string(code).decode()
+
+
+class Context:
+    """gls_ctx wrapper.  Context(n, pL, pR, M, X_L, y) runs gls_create on the current device."""
+
+    def __init__(self, n: int, pL: int, pR: int, M=None, X_L=None, y=None, adopt: bool = False):
+        L = load()
+        self._lib = L
+        self.n, self.pL, self.pR, self.p = n, pL, pR, pL + pR
+        h = ctypes.c_void_p()
+        if adopt:
+            rc = L.gls_create_adopt(n, pL, pR, ctypes.byref(h))
+        else:
+            rc = L.gls_create(n, pL, pR, _ptr(M), _ptr(X_L) if pL > 0 else None, _ptr(y), ctypes.byref(h))
+        self._h = h
+        self.failed_pivot = -1
+        if rc != GLS_OK:
+            msg = error_string(rc)
+            if h.value:
+                self.failed_pivot = L.gls_failed_pivot(h)
+                msg += " -- " + L.gls_last_error(h).decode()
+                L.gls_destroy(h)
+                self._h = ctypes.c_void_p()
+            raise GLSError(rc, msg)
+
+    # -- helpers
+    def _check(self, rc: int):
+        if rc != GLS_OK:
+            raise GLSError(rc, error_string(rc) + " -- " + self._lib.gls_last_error(self._h).decode())
+
+    def solve_block(self, X_R, m_blk: int, b_out, status_out=None, async_: bool = False):
+        self._check(self._lib.gls_solve_block_ex(self._h, _ptr(X_R), m_blk, _ptr(b_out),
+                                                 _ptr(status_out, "int32"), 1 if async_ else 0))
+
+    def sync(self):
+        self._check(self._lib.gls_sync(self._h))
+
+    def set_stream(self, stream_handle: int | None):
+        self._check(self._lib.gls_set_stream(self._h, stream_handle))
+
+    def set_block_cols(self, cols: int):
+        self._check(self._lib.gls_set_block_cols(self._h, cols))
+
+    def shared_view(self):
+        ptrs = (ctypes.c_void_p * 8)()
+        nbytes = (ctypes.c_int64 * 8)()
+        cnt = ctypes.c_int32()
+        self._check(self._lib.gls_shared_view(self._h, ptrs, nbytes, ctypes.byref(cnt)))
+        return [(ptrs[k], nbytes[k]) for k in range(cnt.value)]
+
+    def shared_tensors(self):
+        """The shared-state buffers as zero-copy torch uint8 CUDA tensors (for dist.broadcast)."""
+        import torch
+
+        class _Raw:
+            def __init__(self, ptr, nbytes):
+                self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                                 "data": (ptr, False), "version": 2, "strides": None}
+
+        return [torch.as_tensor(_Raw(p, nb), device="cuda") for p, nb in self.shared_view()]
+
+    def commit_shared(self):
+        self._check(self._lib.gls_commit_shared(self._h))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self._lib.gls_kernel_launches(self._h))
+
+    def close(self):
+        if self._h and self._h.value:
+            self._lib.gls_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def gen_xr_device(seed: int, n: int, col0: int, ncols: int, X, ld: int | None = None, stream: int = 0):
+    """Fill a CUDA float64 tensor X (shape (ncols, ld)) with genotype columns [col0, col0+ncols)."""
+    rc = load_gen().glsgen_dev_xr(seed, n, col0, ncols, X.data_ptr(), ld or n, stream)
+    if rc != 0:
+        raise GLSError(GLS_ERR_CUDA, "glsgen_dev_xr failed with cudaError %d" % rc)

@@ -1,0 +1,67 @@
+"""CPU-side checks of the boundary: libgls.so loads and exports every symbol include/gls.h
+declares; argument/dimension validation runs without touching the GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "gls.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gls_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1210_7325_b200 import gls
+    return gls.load()
+
+
+def test_header_declares_boundary():
+    syms = header_symbols()
+    for s in ("gls_create", "gls_solve_block", "gls_destroy"):
+        assert s in syms
+
+
+def test_library_exports_every_header_symbol(lib):
+    from paper_1210_7325_b200 import gls
+    syms = header_symbols()
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert sorted(gls.ABI_SYMBOLS) == syms
+
+
+def test_error_strings(lib):
+    for code in range(7):
+        s = lib.gls_error_string(code).decode()
+        assert s.startswith("GLS_")
+    assert b"unknown" in lib.gls_error_string(99)
+
+
+@pytest.mark.parametrize("n,pL,pR,code", [(10, 3, 0, 2), (4, 3, 1, 2), (100, -1, 1, 2),
+                                           (100, 17, 4, 2), (100, 0, 21, 2), (21, 19, 1, 0)])
+def test_dims_validated_before_device_work(lib, n, pL, pR, code):
+    """GLS_ERR_DIM unless n > p, pL >= 0, pR >= 1, p <= 20."""
+    h = ctypes.c_void_p(123)
+    if code == 0:
+        # valid dims but NULL M -> GLS_ERR_ARG, *out NULL, no CUDA call
+        assert lib.gls_create(n, pL, pR, None, None, None, ctypes.byref(h)) == 1
+        assert h.value is None
+        return
+    buf = (ctypes.c_double * 4)()
+    rc = lib.gls_create(n, pL, pR, buf, buf, buf, ctypes.byref(h))
+    assert rc == code and h.value is None
+    assert lib.gls_create_adopt(n, pL, pR, ctypes.byref(h)) == code
+
+
+def test_null_handles(lib):
+    assert lib.gls_solve_block(None, None, 1, None) == 1
+    assert lib.gls_sync(None) == 1
+    assert lib.gls_failed_pivot(None) == -1
+    assert lib.gls_last_error(None) == b""
+    lib.gls_destroy(None)
+    assert lib.gls_create(10, 1, 1, None, None, None, None) == 1

@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, on the same seeded inputs.
+
+Every input comes from gen/ (CPU) or its independent device twin (libglsgen_dev.so, checked
+bit-exact here first); every expected value comes from oracle/.  Tolerance: the north-star
+1e-9 per b_i entry, guarded as in DESIGN.md reading A10 (tests/_util.py).
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+from _util import assert_parity, guarded_rel_err, normwise_err
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+SEED = gen.DEFAULT_SEED
+
+
+@pytest.fixture(scope="module")
+def glsmod():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1210_7325_b200 as pkg
+    pkg.load()
+    return pkg
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run_gpu(pkg, P, XR_dev, m, pR, host_out=False, status=True):
+    p = P.pL + pR
+    ctx = pkg.Context(P.n, P.pL, pR, dev(P.M), dev(P.XL) if P.pL else None, dev(P.y))
+    try:
+        if host_out:
+            b = np.empty((m, p))
+            st = np.empty(m, dtype=np.int32)
+        else:
+            b = torch.empty((m, p), dtype=torch.float64, device="cuda")
+            st = torch.empty(m, dtype=torch.int32, device="cuda")
+        ctx.solve_block(XR_dev, m, b, st if status else None)
+        launches = ctx.kernel_launches
+    finally:
+        ctx.close()
+    if not host_out:
+        b, st = b.cpu().numpy(), st.cpu().numpy()
+    return b, st, launches
+
+
+def test_device_generator_matches_cpu(glsmod):
+    for n, col0, ncols in [(500, 0, 37), (1501, 12345, 9), (10_000, 999_990, 3)]:
+        X = torch.empty((ncols, n), dtype=torch.float64, device="cuda")
+        glsmod.gen_xr_device(SEED, n, col0, ncols, X)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(X.cpu().numpy(), gen.make_XR(SEED, n, col0, ncols))
+
+
+def test_config0_all_snps(glsmod):
+    """Config 0 (n=500, pL=3, pR=1, m=2000): every SNP against the oracle."""
+    cfg = gen.CONFIGS[0]
+    P = gen.config_problem(cfg)
+    XR = gen.make_XR(SEED, cfg.n, 0, cfg.cols)
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, cfg.pR)
+    Xd = torch.empty((cfg.cols, cfg.n), dtype=torch.float64, device="cuda")
+    glsmod.gen_xr_device(SEED, cfg.n, 0, cfg.cols, Xd)
+    b, st, launches = run_gpu(glsmod, P, Xd, cfg.m, cfg.pR)
+    assert launches > 0
+    err = assert_parity(b, st, b_or, st_or, label="config0")
+    assert normwise_err(b, b_or) <= 1e-12
+    print("config0 guarded err %.3e" % err)
+
+
+@pytest.mark.parametrize("n,pL,pR,m,sex", [
+    (37, 3, 1, 70, True),       # n < 128: one row block, ragged rows; odd n -> staged path
+    (130, 0, 1, 65, False),     # pL = 0: pure X_R regression
+    (256, 1, 2, 200, False),    # exact multiple of 128
+    (300, 7, 1, 129, True),     # pL + 1 = 8: one full W tile
+    (300, 8, 1, 100, True),     # pL + 1 = 9: two W tiles
+    (420, 16, 4, 50, False),    # config-3 shape (p = 20), 2 W tiles... 17 columns -> 3 tiles
+    (333, 2, 3, 77, True),      # pR = 3: groups straddle 8-column MMA tiles (full Gram)
+    (200, 0, 20, 9, False),     # pR = 20, p = 20
+    (515, 4, 5, 41, True),      # pR = 5
+    (640, 3, 8, 33, True),      # pR = 8
+    (771, 19, 1, 40, False),    # p = 20 with pL = 19 (3 W tiles)
+])
+def test_ragged_shapes(glsmod, n, pL, pR, m, sex):
+    P = gen.make_problem(n, pL, pR, with_sex=sex, seed=SEED + n)
+    XR = gen.make_XR(SEED + n, n, 0, m * pR)
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, pR)
+    b, st, _ = run_gpu(glsmod, P, dev(XR), m, pR)
+    assert_parity(b, st, b_or, st_or, label="n=%d pL=%d pR=%d" % (n, pL, pR))
+
+
+def test_host_stream_equals_device_bitwise(glsmod):
+    """Host-resident X_R (Alg. 8 double-buffered stream) gives the same bits as device X_R,
+    for several block sizes (block-partition independence)."""
+    n, pL, pR, m = 512, 3, 1, 1000
+    P = gen.make_problem(n, pL, pR, seed=3)
+    XR = gen.make_XR(3, n, 0, m)
+    ctx = glsmod.Context(n, pL, pR, dev(P.M), dev(P.XL), dev(P.y))
+    try:
+        bd = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+        ctx.solve_block(dev(XR), m, bd)
+        ref = bd.cpu().numpy()
+        XRh = torch.from_numpy(XR).pin_memory()
+        for cols in (64, 100, 333, 10_000):
+            ctx.set_block_cols(cols)
+            bh = np.empty((m, 4))
+            sth = np.empty(m, dtype=np.int32)
+            ctx.solve_block(XRh, m, bh, sth)
+            np.testing.assert_array_equal(bh, ref)
+            assert np.all(sth == 0)
+        # pageable numpy input, host output
+        bh = np.empty((m, 4))
+        ctx.solve_block(XR, m, bh)
+        np.testing.assert_array_equal(bh, ref)
+        # split into sub-blocks through the device path
+        for cut in (1, 63, 64, 65, 500):
+            b1 = torch.empty((cut, 4), dtype=torch.float64, device="cuda")
+            b2 = torch.empty((m - cut, 4), dtype=torch.float64, device="cuda")
+            Xd = dev(XR)
+            ctx.solve_block(Xd[:cut], cut, b1)
+            ctx.solve_block(Xd[cut:], m - cut, b2)
+            np.testing.assert_array_equal(torch.cat([b1, b2]).cpu().numpy(), ref)
+    finally:
+        ctx.close()
+
+
+def test_not_spd_pivot_matches_oracle(glsmod):
+    n = 300
+    P = gen.make_problem(n, 3, 1, seed=4)
+    M = P.M.copy()
+    M[200, 200] = -1.0  # first 200 pivots fine, pivot 200 negative
+    with pytest.raises(oracle.NotSPD) as ei:
+        oracle.cholesky(M)
+    with pytest.raises(glsmod.GLSError) as eg:
+        glsmod.Context(n, 3, 1, dev(M), dev(P.XL), dev(P.y))
+    assert eg.value.code == 3
+    ctx_pivot = None
+    # failed pivot is reported through the ABI
+    import ctypes
+    L = glsmod.load()
+    h = ctypes.c_void_p()
+    Md, XLd, yd = dev(M), dev(P.XL), dev(P.y)  # keep the tensors alive across the raw calls
+    rc = L.gls_create(n, 3, 1, Md.data_ptr(), XLd.data_ptr(), yd.data_ptr(), ctypes.byref(h))
+    assert rc == 3 and h.value
+    ctx_pivot = L.gls_failed_pivot(h)
+    assert L.gls_solve_block(h, yd.data_ptr(), 1, yd.data_ptr()) == 6  # GLS_ERR_STATE
+    L.gls_destroy(h)
+    assert ctx_pivot == ei.value.pivot == 200
+
+
+def test_rank_deficient_isolation(glsmod):
+    n, m = 400, 130
+    P = gen.make_problem(n, 3, 1, with_sex=True, seed=5)
+    XR = gen.make_XR(5, n, 0, m)
+    XR[7] = 0.0
+    XR[64] = 2.0 * P.XL[2]
+    XR[129] = 0.0
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, 1)
+    assert list(np.nonzero(st_or)[0]) == [7, 64, 129]
+    b, st, _ = run_gpu(glsmod, P, dev(XR), m, 1)
+    assert_parity(b, st, b_or, st_or, label="rank-deficient")
+
+
+def test_scaling_invariance_bitwise(glsmod):
+    """b(4M) == b(M) bit for bit on the GPU (all arithmetic scales by exact powers of 2)."""
+    n, m = 384, 300
+    P = gen.make_problem(n, 3, 1, seed=6)
+    Xd = dev(gen.make_XR(6, n, 0, m))
+    b1, _, _ = run_gpu(glsmod, P, Xd, m, 1)
+    P4 = gen.Problem(P.n, P.pL, P.pR, 4.0 * P.M, P.XL, P.y, P.beta_L)
+    b4, _, _ = run_gpu(glsmod, P4, Xd, m, 1)
+    np.testing.assert_array_equal(b1, b4)
+
+
+def test_planted_beta_config1_all_snps(glsmod):
+    """Full config 1 size (n=1500, m=220833), noise-free y = X_L beta: b_i = (beta, 0) for all i."""
+    cfg = gen.CONFIGS[1]
+    P = gen.config_problem(cfg, noise=0.0)
+    Xd = torch.empty((cfg.cols, cfg.n), dtype=torch.float64, device="cuda")
+    glsmod.gen_xr_device(SEED, cfg.n, 0, cfg.cols, Xd)
+    b, st, _ = run_gpu(glsmod, P, Xd, cfg.m, cfg.pR)
+    assert np.all(st == 0)
+    ref = np.concatenate([P.beta_L, [0.0]])
+    err = np.max(np.abs(b - ref)) / np.max(np.abs(P.beta_L))
+    assert err <= 1e-10, err
+
+
+def test_config1_sampled_parity(glsmod):
+    """Config 1 at full size in the bench launch configuration; oracle on a seeded sample
+    plus every panel/wave edge in the first and last waves."""
+    cfg = gen.CONFIGS[1]
+    P = gen.config_problem(cfg)
+    Xd = torch.empty((cfg.cols, cfg.n), dtype=torch.float64, device="cuda")
+    glsmod.gen_xr_device(SEED, cfg.n, 0, cfg.cols, Xd)
+    b, st, _ = run_gpu(glsmod, P, Xd, cfg.m, cfg.pR)
+    rng = np.random.default_rng(11)
+    edges = [0, 1, 63, 64, 65, 148 * 64 - 1, 148 * 64, cfg.m - 65, cfg.m - 2, cfg.m - 1]
+    sel = np.unique(np.concatenate([rng.choice(cfg.m, 1500, replace=False), edges]))
+    XRs = np.concatenate([gen.make_XR(SEED, cfg.n, int(i), 1) for i in sel])
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XRs, 1, sel=sel, xr_is_selected=True)
+    err = assert_parity(b[sel], st[sel], b_or, st_or, label="config1 sample")
+    print("config1 sampled guarded err %.3e normwise %.3e" % (err, normwise_err(b[sel], b_or)))
+
+
+def test_adopt_shared_state_bitwise(glsmod):
+    """Replicate-then-shard: an adopt-mode context fed the root's shared buffers (what the NCCL
+    broadcast delivers) solves bit-identically."""
+    n, m = 300, 200
+    P = gen.make_problem(n, 3, 1, seed=8)
+    Xd = dev(gen.make_XR(8, n, 0, m))
+    root = glsmod.Context(n, 3, 1, dev(P.M), dev(P.XL), dev(P.y))
+    other = glsmod.Context(n, 3, 1, adopt=True)
+    try:
+        with pytest.raises(glsmod.GLSError):
+            other.solve_block(Xd, m, torch.empty((m, 4), dtype=torch.float64, device="cuda"))
+        for src, dst in zip(root.shared_tensors(), other.shared_tensors()):
+            assert src.numel() == dst.numel()
+            dst.copy_(src)
+        torch.cuda.synchronize()
+        other.commit_shared()
+        b1 = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+        b2 = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+        root.solve_block(Xd, m, b1)
+        other.solve_block(Xd, m, b2)
+        assert torch.equal(b1, b2)
+    finally:
+        root.close()
+        other.close()
