@@ -93,6 +93,8 @@ struct KParams {
   int64_t m_blk;
   int64_t num_panels;
   int NB;
+  int pad;  // n_pad - n: virtual rows [0, pad) are zero padding at the TOP
+  int kt0;  // first K tile that is not all padding = pad / 16
   int pL, pR, p;
   int gw, cpw, cpp, gpp;
 };
@@ -103,13 +105,12 @@ struct KCfg {
   static constexpr int STAGES = (NW == 1 && !FULL) ? 6 : 5;
   static constexpr int kWBytes = 1024 * NW * 8;  // packed W per row block
   static constexpr int kRedDoubles = (4 * NW + NG) * 64;
-  static constexpr size_t off_X = 0;
-  static constexpr size_t off_T = off_X + (size_t)STAGES * kXStageBytes;
-  static constexpr size_t off_W = off_T + (size_t)STAGES * kTStageBytes;
-  static constexpr size_t off_R = off_W + 2 * (size_t)kWBytes;
-  static constexpr size_t off_B = off_R + 2 * (size_t)kRedDoubles * 8;
-  static constexpr size_t bytes = off_B + 2 * STAGES * 8 + 1024;  // + alignment slack
-  static_assert(STAGES < kKTPerRB, "W double-buffer reuse argument needs STAGES < nb/16");
+  static constexpr uint32_t off_X = 0;
+  static constexpr uint32_t off_T = off_X + STAGES * kXStageBytes;
+  static constexpr uint32_t off_W = off_T + STAGES * kTStageBytes;
+  static constexpr uint32_t off_R = off_W + 2 * kWBytes;
+  static constexpr uint32_t off_B = off_R + 2 * kRedDoubles * 8;
+  static constexpr uint32_t bytes = off_B + (2 * STAGES + 2) * 8 + 1024;  // + alignment slack
 };
 
 // Pair index of Gram tile (t, t2), t <= t2 < 4, for FULL mode.
@@ -117,18 +118,52 @@ __host__ __device__ constexpr int gram_pair(int t, int t2) {
   return t * 4 - (t * (t - 1)) / 2 + (t2 - t);  // rows: t=0 -> 0..3, t=1 -> 4..6, t=2 -> 7..8, t=3 -> 9
 }
 
-template <int NW, bool FULL>
+__device__ __forceinline__ void lds128(uint32_t addr, double& x, double& y) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(addr));
+}
+
+// One stage's operand fragments for one P half (K rows 4kk+2P, 4kk+2P+1 of the 16-row tile).
+struct Frag {
+  double a[4][2];  // X^T: 4 column tiles t
+  double b[4][2];  // T^T: 4 z-row subtiles s
+};
+
+template <bool ALIGNED>
+__device__ __forceinline__ void load_frag(Frag& f, uint32_t xs, uint32_t ts, const uint32_t (&xoff)[4][2],
+                                          uint32_t toff0, int P) {
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const uint32_t o = ALIGNED ? xoff[0][P] + t * 1024 : xoff[t][P];
+    lds128(xs + o, f.a[t][0], f.a[t][1]);
+  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s) lds128(ts + toff0 + s * 1024 + P * 512, f.b[s][0], f.b[s][1]);
+}
+
+__device__ __forceinline__ void mma_frag(double (&acc)[4][4][2], const Frag& f) {
+#pragma unroll
+  for (int e = 0; e < 2; ++e)
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) dmma(acc[t][s], f.a[t][e], f.b[s][e]);
+}
+
+template <int NW, bool FULL, bool ALIGNED>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_trsm_gls_kernel(const __grid_constant__ CUtensorMap xmap, const KParams kp) {
   using C = KCfg<NW, FULL>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sX = smem + C::off_X;
-  uint8_t* sT = smem + C::off_T;
+  // 1024-byte alignment for the 128B-swizzled TMA destination, in the shared window
+  const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (sbase - smem_u32(smem_raw));
+  const uint32_t sX = sbase + C::off_X;
+  const uint32_t sT = sbase + C::off_T;
   double* sW = (double*)(smem + C::off_W);
   double* sR = (double*)(smem + C::off_R);
   uint64_t* full = (uint64_t*)(smem + C::off_B);
   uint64_t* empty = full + C::STAGES;
+  uint64_t* wempty = empty + C::STAGES;  // W double buffer: consumers release after the epilogue
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -136,34 +171,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
+    mbar_init(&wempty[0], kConsumerWarps);
+    mbar_init(&wempty[1], kConsumerWarps);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
   const int NB = kp.NB;
+  const int kt0 = kp.kt0;
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------------------ TMA producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
       int st = 0;
       uint32_t ph = 0;
-      uint32_t rbc = 0;  // running row-block counter (W buffer parity)
+      uint32_t rbc = 0;  // running row-block counter (W buffer = rbc & 1, its use = rbc >> 1)
       const uint32_t xbytes = (uint32_t)(kKT * kp.cpp * 8);
       for (int64_t panel = blockIdx.x; panel < kp.num_panels; panel += gridDim.x) {
         const int col0 = (int)(panel * kp.cpp);
         for (int i = 0; i < NB; ++i, ++rbc) {
           const double* Trb = kp.Tpk + tpk_tile_offset(i) * kTileDoubles;
           const int nkt = (i + 1) * kKTPerRB;
-          for (int kt = 0; kt < nkt; ++kt) {
+          for (int kt = kt0; kt < nkt; ++kt) {
             mbar_wait(&empty[st], ph ^ 1);
-            const uint32_t bytes = kTStageBytes + xbytes + (kt == 0 ? C::kWBytes : 0);
+            const bool first = (kt == kt0);
+            if (first) mbar_wait(&wempty[rbc & 1], ((rbc >> 1) & 1) ^ 1);
+            const uint32_t bytes = kTStageBytes + xbytes + (first ? C::kWBytes : 0);
             mbar_arrive_expect_tx(&full[st], bytes);
-            bulk_g2s(sT + (size_t)st * kTStageBytes, Trb + (size_t)kt * kTileDoubles, kTStageBytes,
-                     &full[st]);
-            tma_2d_g2s(sX + (size_t)st * kXStageBytes, &xmap, kt * kKT, col0, &full[st]);
-            if (kt == 0)
-              bulk_g2s(sW + (size_t)(rbc & 1) * (C::kWBytes / 8),
-                       kp.Wpk + (size_t)i * (C::kWBytes / 8), C::kWBytes, &full[st]);
+            bulk_g2s(smem + C::off_T + (size_t)st * kTStageBytes, Trb + (size_t)kt * kTileDoubles,
+                     kTStageBytes, &full[st]);
+            // virtual row kt*16 is real row kt*16 - pad; negative rows are zero-filled by TMA
+            tma_2d_g2s(smem + C::off_X + (size_t)st * kXStageBytes, &xmap, kt * kKT - kp.pad, col0,
+                       &full[st]);
+            if (first)
+              bulk_g2s(sW + (size_t)(rbc & 1) * (C::kWBytes / 8), kp.Wpk + (size_t)i * (C::kWBytes / 8),
+                       C::kWBytes, &full[st]);
             if (++st == C::STAGES) {
               st = 0;
               ph ^= 1;
@@ -191,12 +233,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int P = 0; P < 2; ++P) xoff[t][P] = row * 128 + (((2 * kk + P) ^ (row & 7)) << 4);
   }
-  // T^T fragment addresses in the packed tile: [subtile g = ns*4+s][P][lane][2]
-  uint32_t toff[4][2];
-#pragma unroll
-  for (int s = 0; s < 4; ++s)
-#pragma unroll
-    for (int P = 0; P < 2; ++P) toff[s][P] = ((((ns * 4 + s) * 2 + P) * 32 + lane) * 2) * 8;
+  // T^T fragment address in the packed tile: [subtile g = ns*4+s][P][lane][2 doubles]
+  const uint32_t toff0 = (uint32_t)((ns * 4 * 2 * 32 + lane) * 16);
 
   double acc[4][4][2];
   double accW[4][NW][2];
@@ -211,6 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   int st = 0;
   uint32_t ph = 0;
   uint32_t rbc = 0;
+  Frag F0, F1;
   for (int64_t panel = blockIdx.x; panel < kp.num_panels; panel += gridDim.x) {
     for (int i = 0; i < NB; ++i, ++rbc) {
 #pragma unroll
@@ -218,32 +257,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int s = 0; s < 4; ++s) acc[t][s][0] = acc[t][s][1] = 0.0;
       const int nkt = (i + 1) * kKTPerRB;
-      for (int kt = 0; kt < nkt; ++kt) {
-        mbar_wait(&full[st], ph);
-        const uint8_t* xs = sX + (size_t)st * kXStageBytes;
-        const uint8_t* ts = sT + (size_t)st * kTStageBytes;
-#pragma unroll
-        for (int P = 0; P < 2; ++P) {
-          double2 a[4], b[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) a[t] = *(const double2*)(xs + xoff[t][P]);
-#pragma unroll
-          for (int s = 0; s < 4; ++s) b[s] = *(const double2*)(ts + toff[s][P]);
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-#pragma unroll
-            for (int s = 0; s < 4; ++s) dmma(acc[t][s], a[t].x, b[s].x);
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-#pragma unroll
-            for (int s = 0; s < 4; ++s) dmma(acc[t][s], a[t].y, b[s].y);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+      // software pipeline: the P=0 fragments of stage k+1 are loaded while stage k's P=1 DMMAs run
+      mbar_wait(&full[st], ph);
+      load_frag<ALIGNED>(F0, sX + st * kXStageBytes, sT + st * kTStageBytes, xoff, toff0, 0);
+      for (int kt = kt0; kt < nkt; ++kt) {
+        load_frag<ALIGNED>(F1, sX + st * kXStageBytes, sT + st * kTStageBytes, xoff, toff0, 1);
+        mma_frag(acc, F0);
+        const int cur = st;
         if (++st == C::STAGES) {
           st = 0;
           ph ^= 1;
         }
+        if (kt + 1 < nkt) {
+          mbar_wait(&full[st], ph);
+          load_frag<ALIGNED>(F0, sX + st * kXStageBytes, sT + st * kTStageBytes, xoff, toff0, 0);
+        }
+        mma_frag(acc, F1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[cur]);
       }
       // ---- row-block epilogue: reductions of z_i on the tensor pipe (z_i stays in registers)
       const double* wb = sW + (size_t)(rbc & 1) * (C::kWBytes / 8);
@@ -258,6 +289,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             dmma(accW[t][w], acc[t][s][1], wf.y);
           }
         }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&wempty[rbc & 1]);
       if (!FULL) {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
@@ -397,9 +430,12 @@ __global__ void pack_T_kernel(const double* __restrict__ T, int64_t ld, int64_t 
   const int64_t kt = tile - tpk_tile_offset(i);
   for (int w = threadIdx.x; w < kTileDoubles; w += blockDim.x) {
     const int g = w >> 7, rem = w & 127, P = rem >> 6, ln = (rem & 63) >> 1, e = rem & 1;
-    const int64_t row = i * kNB + g * 8 + (ln >> 2);
-    const int64_t col = kt * kKT + 4 * (ln & 3) + 2 * P + e;
-    Tpk[tile * kTileDoubles + w] = (row < n && col <= row) ? T[row + col * ld] : 0.0;
+    // virtual (row, col) -> real (row - pad, col - pad); the padding sits at the top-left
+    const int64_t pad = row_pad(n, NB);
+    const int64_t row = i * kNB + g * 8 + (ln >> 2) - pad;
+    const int64_t col = kt * kKT + 4 * (ln & 3) + 2 * P + e - pad;
+    Tpk[tile * kTileDoubles + w] =
+        (row >= 0 && row < n && col >= 0 && col <= row) ? T[row + col * ld] : 0.0;
   }
 }
 
@@ -415,9 +451,10 @@ __global__ void pack_W_kernel(const double* __restrict__ W, int64_t ld, int64_t 
     const int w = (int)(r % NW); r /= NW;
     const int ns = r & 3; r >>= 2;
     const int64_t i = r;
-    const int64_t row = i * kNB + ns * 32 + s * 8 + 2 * (lane & 3) + e;
+    const int64_t pad = row_pad(n, (n + kNB - 1) / kNB);
+    const int64_t row = i * kNB + ns * 32 + s * 8 + 2 * (lane & 3) + e - pad;
     const int col = w * 8 + (lane >> 2);
-    Wpk[o] = (row < n && col < ncolsW) ? W[row + col * ld] : 0.0;
+    Wpk[o] = (row >= 0 && row < n && col < ncolsW) ? W[row + col * ld] : 0.0;
   }
 }
 
@@ -439,18 +476,18 @@ PFN_encodeTiled get_encode() {
   return fn;
 }
 
-template <int NW, bool FULL>
+template <int NW, bool FULL, bool ALIGNED>
 cudaError_t launch_variant(cudaStream_t s, const CUtensorMap& map, const KParams& kp, int num_sms) {
   using C = KCfg<NW, FULL>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(fused_trsm_gls_kernel<NW, FULL>,
+    cudaError_t e = cudaFuncSetAttribute(fused_trsm_gls_kernel<NW, FULL, ALIGNED>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::bytes);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
   const int64_t grid = kp.num_panels < num_sms ? kp.num_panels : num_sms;
-  fused_trsm_gls_kernel<NW, FULL><<<(unsigned)grid, kThreads, C::bytes, s>>>(map, kp);
+  fused_trsm_gls_kernel<NW, FULL, ALIGNED><<<(unsigned)grid, kThreads, C::bytes, s>>>(map, kp);
   return cudaGetLastError();
 }
 
@@ -481,7 +518,8 @@ cudaError_t launch_fused_trsm_gls(cudaStream_t s, const SolveArgs& a, int num_sm
   const PanelGeom pg = panel_geom(a.pR);
   CUtensorMap map;
   const int64_t cols = a.m_blk * a.pR;
-  cuuint64_t gdim[2] = {(cuuint64_t)a.n, (cuuint64_t)cols};
+  // dim0 = ldx (>= n, even): rows in [n, ldx) are the zero pad row of the staged copy (odd n).
+  cuuint64_t gdim[2] = {(cuuint64_t)a.ldx, (cuuint64_t)cols};
   cuuint64_t gstride[1] = {(cuuint64_t)(a.ldx * 8)};
   cuuint32_t box[2] = {(cuuint32_t)kKT, (cuuint32_t)pg.cpp};
   cuuint32_t estr[2] = {1, 1};
@@ -506,6 +544,8 @@ cudaError_t launch_fused_trsm_gls(cudaStream_t s, const SolveArgs& a, int num_sm
   kp.m_blk = a.m_blk;
   kp.num_panels = (a.m_blk + pg.gpp - 1) / pg.gpp;
   kp.NB = (int)a.NB;
+  kp.pad = (int)row_pad(a.n, a.NB);
+  kp.kt0 = kp.pad / kKT;
   kp.pL = a.pL;
   kp.pR = a.pR;
   kp.p = a.pL + a.pR;
@@ -515,14 +555,21 @@ cudaError_t launch_fused_trsm_gls(cudaStream_t s, const SolveArgs& a, int num_sm
   kp.gpp = pg.gpp;
   const int NW = (a.pL + 1 + 7) / 8;
   cudaError_t e;
+  // ALIGNED: every warp's column range starts on an 8-column boundary (pR divides 32), so the
+  // swizzle phase is the same for the 4 column tiles and fragment addresses are immediates.
+  const bool aligned = (pg.cpw % 8) == 0;
   if (!pg.full_gram) {
-    e = NW == 1 ? launch_variant<1, false>(s, map, kp, num_sms)
-      : NW == 2 ? launch_variant<2, false>(s, map, kp, num_sms)
-                : launch_variant<3, false>(s, map, kp, num_sms);
+    e = NW == 1 ? launch_variant<1, false, true>(s, map, kp, num_sms)
+      : NW == 2 ? launch_variant<2, false, true>(s, map, kp, num_sms)
+                : launch_variant<3, false, true>(s, map, kp, num_sms);
+  } else if (aligned) {
+    e = NW == 1 ? launch_variant<1, true, true>(s, map, kp, num_sms)
+      : NW == 2 ? launch_variant<2, true, true>(s, map, kp, num_sms)
+                : launch_variant<3, true, true>(s, map, kp, num_sms);
   } else {
-    e = NW == 1 ? launch_variant<1, true>(s, map, kp, num_sms)
-      : NW == 2 ? launch_variant<2, true>(s, map, kp, num_sms)
-                : launch_variant<3, true>(s, map, kp, num_sms);
+    e = NW == 1 ? launch_variant<1, true, false>(s, map, kp, num_sms)
+      : NW == 2 ? launch_variant<2, true, false>(s, map, kp, num_sms)
+                : launch_variant<3, true, false>(s, map, kp, num_sms);
   }
   if (lc) ++*lc;
   if (e != cudaSuccess && msg) *msg = std::string("fused_trsm_gls launch: ") + cudaGetErrorString(e);

@@ -219,6 +219,7 @@ int ensure_staging(gls_ctx* c, int64_t chunk_groups) {
   free_staging(c);
   for (int k = 0; k < 2; ++k) {
     CK(c, cudaMalloc(&c->stage[k], (size_t)ld * cols * sizeof(double)));
+    CK(c, cudaMemset(c->stage[k], 0, (size_t)ld * cols * sizeof(double)));  // pad row (odd n) stays 0
     CK(c, cudaMalloc(&c->bstage[k], (size_t)chunk_groups * c->p * sizeof(double)));
     CK(c, cudaMalloc(&c->sstage[k], (size_t)chunk_groups * sizeof(int32_t)));
   }

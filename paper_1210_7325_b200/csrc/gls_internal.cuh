@@ -20,6 +20,10 @@ constexpr int kMaxPanelCols = 64;        // 2 warps x 32 columns
 // Packed-T tile index of (row block i, K tile kt): row block i holds K tiles 0..8(i+1)-1.
 __host__ __device__ inline int64_t tpk_tile_offset(int64_t i) { return 4 * i * (i + 1); }
 inline int64_t tpk_total_tiles(int64_t NB) { return 4 * NB * (NB + 1); }
+// Zero rows placed ABOVE the data so that the last row block ends at row n:
+// real row r sits at virtual row r + pad.  Kept even so every TMA box starts on a 16-byte boundary
+// (an odd start row faults the TMA unit); for odd n one zero row is left below the data instead.
+__host__ __device__ inline int64_t row_pad(int64_t n, int64_t NB) { return (NB * kNB - n) & ~(int64_t)1; }
 // Packed W per row block: 4 slices x NW x 4 subtiles x 32 lanes x 2 doubles.
 inline int64_t wpk_rb_doubles(int NW) { return 1024 * (int64_t)NW; }
 
