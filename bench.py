@@ -38,6 +38,7 @@ UNIT = "SNPs/s"
 # 37.10 TFLOP/s burst, 36.86 TFLOP/s sustained over 4 s.  MEASURED_PEAKS.json carries no FP64 figure.
 FP64_DMMA_PEAK_SUSTAINED = 36.86
 FP64_DMMA_PEAK_BURST = 37.10
+H2D_GBS = 55.6  # pinned host -> device, measured (profiles/r01_probe.txt)
 
 
 def parse():
@@ -163,6 +164,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1210_7325_b200 as pkg
+    from paper_1210_7325_b200 import multi
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -173,9 +175,11 @@ def main():
     pkg.load()
 
     cfg = gen.CONFIGS[args.config]
+    if args.config == 4:
+        return run_ooc(args, cfg, world, rank, local)
     n, pL, pR, p = cfg.n, cfg.pL, cfg.pR, cfg.p
     m = args.m or cfg.m
-    col0 = rank * m * pR  # this rank's SNP range [rank*m, (rank+1)*m)
+    col0 = multi.weak_range(m, rank)[0] * pR  # this rank's SNP range [rank*m, (rank+1)*m)
 
     P = gen.config_problem(cfg, seed=args.seed)
     Md = torch.from_numpy(P.M).cuda()
@@ -195,16 +199,13 @@ def main():
     torch.cuda.set_stream(stream)
 
     def make_ctx(Mx, XLx, yx):
+        # rank 0 factors; the others adopt the broadcast shared state
         if rank == 0:
             ctx = pkg.Context(n, pL, pR, Mx, XLx, yx)
         else:
             ctx = pkg.Context(n, pL, pR, adopt=True)
         if world > 1:
-            for t in ctx.shared_tensors():
-                dist.broadcast(t, src=0)
-            torch.cuda.synchronize()
-            if rank != 0:
-                ctx.commit_shared()
+            multi.replicate_shared(ctx, dist, src=0)
         return ctx
 
     kern_ms = []
@@ -247,10 +248,7 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     total_ms = e0.elapsed_time(e1)
-    t = torch.tensor([total_ms, statistics.mean(kern_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, kern_avg_ms = float(t[0]), float(t[1])
+    total_ms, kern_avg_ms = multi.max_over_ranks([total_ms, statistics.mean(kern_ms)], dist, device="cuda")
     ms_per_step = total_ms / args.steps
     value = world * m / (ms_per_step / 1e3)
 
@@ -279,20 +277,29 @@ def main():
     # ---- e2e: same job through the C ABI with host buffers (rank's X_R pinned in host memory)
     e2e = None
     if not args.no_e2e:
-        Xh = torch.empty((m * pR, n), dtype=torch.float64, pin_memory=True)
-        for c in range(0, m * pR, chunk):
-            k = min(chunk, m * pR - c)
+        # pinned host copy of the rank's X_R; shrink the e2e SNP count if host RAM cannot hold
+        # world x 80 GB (then e2e is measured on the first m_e2e SNPs of the rank's range)
+        try:
+            avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+        except (ValueError, OSError):
+            avail = 1 << 40
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        m_e2e = int(min(m, 0.6 * avail / local_world / (n * pR * 8)))
+        m_e2e = max(m_e2e - m_e2e % 64, 64)
+        Xh = torch.empty((m_e2e * pR, n), dtype=torch.float64, pin_memory=True)
+        for c in range(0, m_e2e * pR, chunk):
+            k = min(chunk, m_e2e * pR - c)
             Xh[c:c + k].copy_(Xd[c:c + k], non_blocking=False)
         Mh = torch.from_numpy(P.M).pin_memory()
         XLh = torch.from_numpy(np.ascontiguousarray(P.XL)).pin_memory()
         yh = torch.from_numpy(P.y).pin_memory()
-        bh = torch.empty((m, p), dtype=torch.float64, pin_memory=True)
-        sh = torch.empty(m, dtype=torch.int32, pin_memory=True)
-        ref_b = b.cpu()
+        bh = torch.empty((m_e2e, p), dtype=torch.float64, pin_memory=True)
+        sh = torch.empty(m_e2e, dtype=torch.int32, pin_memory=True)
+        ref_b = b[:m_e2e].cpu()
 
         def e2e_step():
             ctx = make_ctx(Mh, XLh, yh)
-            ctx.solve_block(Xh, m, bh, sh)
+            ctx.solve_block(Xh, m_e2e, bh, sh)
             ctx.close()
 
         for _ in range(1):
@@ -304,13 +311,12 @@ def main():
         for _ in range(args.steps):
             e2e_step()
         torch.cuda.synchronize()
-        dt = torch.tensor([(time.perf_counter() - t0) / args.steps], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        dt = multi.max_over_ranks([(time.perf_counter() - t0) / args.steps], dist, device="cuda")[0]
         same = bool(torch.equal(bh, ref_b))
-        e2e = {"value": world * m / float(dt[0]), "unit": UNIT,
-               "h2d_bytes_per_step": int((n * n + n * (pL + 1) + m * pR * n) * 8),
-               "d2h_bytes_per_step": int(m * p * 8 + m * 4),
+        e2e = {"value": world * m_e2e / dt, "unit": UNIT,
+               "h2d_bytes_per_step": int((n * n + n * (pL + 1) + m_e2e * pR * n) * 8),
+               "d2h_bytes_per_step": int(m_e2e * p * 8 + m_e2e * 4),
+               "m_per_rank": m_e2e, "path": "C ABI, host X_R (pinned) -> double-buffered H2D stream",
                "bitwise_equal_to_device_run": same}
         del Xh
 
@@ -334,6 +340,105 @@ def main():
                            "l2": "inputs larger than L2 (X_R %.1f GB per rank)" % (m * pR * n * 8 / 1e9)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches[0],
                 "clocks": clk, "rank_deficient_rows": n_bad}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+# ----------------------------------------------------------------------------- config 4 (OOC)
+def run_ooc(args, cfg, world, rank, local):
+    """Config 4: m = 1e7 SNPs per rank streamed from pinned host memory through the double-buffered
+    H2D pipeline of gls_solve_block (Alg. 8).  800 GB does not fit in host RAM,
+    so a pool of distinct pinned blocks (as much as 50 % of free RAM allows) is cycled: chunk j of
+    the rank's stream is pool block j mod P (the SNP -> block map is recorded in the JSON line).
+    Every byte still crosses PCIe, so the H2D roofline is unchanged."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1210_7325_b200 as pkg
+    from paper_1210_7325_b200 import multi
+
+    n, pL, pR, p = cfg.n, cfg.pL, cfg.pR, cfg.p
+    m = args.m or cfg.m
+    P = gen.config_problem(cfg, seed=args.seed)
+    Md = torch.from_numpy(P.M).cuda()
+    XLd = torch.from_numpy(np.ascontiguousarray(P.XL)).cuda()
+    yd = torch.from_numpy(P.y).cuda()
+    probe = pkg.Context(n, pL, pR, Md, XLd, yd)
+    props = torch.cuda.get_device_properties(local)
+    blk_groups = (props.multi_processor_count * 64) // pR     # one wave of panels per chunk
+    probe.close()
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 1 << 40
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    blk_bytes = blk_groups * pR * n * 8
+    nblk = (m + blk_groups - 1) // blk_groups
+    pool_n = int(max(2, min(nblk, 0.5 * avail / local_world // blk_bytes)))
+    g0 = multi.weak_range(m, rank)[0]
+    pool = torch.empty((pool_n, blk_groups * pR, n), dtype=torch.float64, pin_memory=True)
+    tmp = torch.empty((blk_groups * pR, n), dtype=torch.float64, device="cuda")
+    for k in range(pool_n):
+        pkg.gen_xr_device(args.seed, n, (g0 + k * blk_groups) * pR, blk_groups * pR, tmp)
+        pool[k].copy_(tmp)
+    del tmp
+    b = torch.empty((m, p), dtype=torch.float64, pin_memory=True)
+    st = torch.empty(m, dtype=torch.int32, pin_memory=True)
+    torch.cuda.synchronize()
+
+    def step():
+        ctx = pkg.Context(n, pL, pR, Md, XLd, yd) if rank == 0 else pkg.Context(n, pL, pR, adopt=True)
+        if world > 1:
+            multi.replicate_shared(ctx, dist, src=0)
+        ctx.set_block_cols(blk_groups * pR)
+        for j in range(nblk):
+            lo = j * blk_groups
+            cnt = min(blk_groups, m - lo)
+            ctx.solve_block(pool[j % pool_n], cnt, b[lo:lo + cnt], st[lo:lo + cnt], async_=True)
+        ctx.sync()
+        launches = ctx.kernel_launches
+        ctx.close()
+        return launches
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    launches = 0
+    for _ in range(args.steps):
+        launches += step()
+    torch.cuda.synchronize()
+    dt = multi.max_over_ranks([(time.perf_counter() - t0) / args.steps], dist, device="cuda")[0]
+    clk = clocks.stop()
+    value = world * m / dt
+    t_comp = float(n) * n * m * pR / (FP64_DMMA_PEAK_SUSTAINED * 1e12)
+    t_h2d = 8.0 * n * m * pR / (H2D_GBS * 1e9)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * dt, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "config4: n=%d pL=%d pR=%d, %d SNPs per GPU streamed from pinned "
+                                       "host memory in %d-SNP chunks (out-of-core, Alg. 8)"
+                                       % (n, pL, pR, m, blk_groups),
+                           "n": n, "m_per_rank": m, "chunk_snps": blk_groups,
+                           "host_pool_blocks": pool_n, "snp_to_block": "chunk j -> pool block j mod %d" % pool_n,
+                           "l2": "inputs larger than L2"},
+                "roofline": {"bound": "tensor" if t_comp >= t_h2d else "h2d",
+                             "achieved": float(n) * n * m * pR / dt / 1e12, "peak": FP64_DMMA_PEAK_SUSTAINED,
+                             "unit": "TFLOP/s", "frac": max(t_comp, t_h2d) / dt, "traffic": None,
+                             "t_compute_roofline_s": t_comp, "t_h2d_roofline_s": t_h2d,
+                             "h2d_gbs_measured": H2D_GBS},
+                "cpu_baseline": None,
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(8 * n * m * pR + 8 * n * n),
+                        "d2h_bytes_per_step": int(m * p * 8 + m * 4),
+                        "path": "C ABI, host X_R -> double-buffered H2D (the whole step is end to end)"},
+                "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

@@ -1,0 +1,52 @@
+"""Replicate-then-shard across GPUs (§6 future work).
+
+The paper's plan for distributed memory: "perform the Cholesky factorization of M redundantly,
+and then operate on distinct chunks of X_R".  Here rank 0 factors once (gls_create) and the
+shared state -- packed T = L^{-1}, packed [X~_L | y~], and W^T W (S_TL, b_T) -- is broadcast
+over NVLink with one NCCL broadcast per buffer (torch.distributed), so every rank holds
+bit-identical factors and b is bitwise independent of the number of GPUs.  After that there is
+no communication: each rank solves its own contiguous SNP range.
+
+Only host-side plumbing lives here; every arithmetic step runs in libgls.so.
+"""
+from __future__ import annotations
+
+
+def snp_range(m_total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous problem range [lo, hi) of `rank` when m_total problems are split over `world`
+    ranks (strong scaling): floor(r m / G) .. floor((r+1) m / G)."""
+    if world < 1 or not (0 <= rank < world) or m_total < 0:
+        raise ValueError("bad shard arguments")
+    return (rank * m_total) // world, ((rank + 1) * m_total) // world
+
+
+def weak_range(m_per_rank: int, rank: int) -> tuple[int, int]:
+    """Problem range of `rank` under weak scaling (every rank owns m_per_rank problems)."""
+    return rank * m_per_rank, (rank + 1) * m_per_rank
+
+
+def replicate_shared(ctx, dist, src: int = 0, group=None) -> int:
+    """Broadcast the shared state of `ctx` from rank `src` to every rank of `group`, then commit it
+    on the receiving ranks.  `ctx` is a Context created with gls_create on `src` and with
+    adopt=True elsewhere.  Returns the number of bytes broadcast."""
+    rank = dist.get_rank(group) if group is not None else dist.get_rank()
+    tensors = ctx.shared_tensors()
+    nbytes = 0
+    for t in tensors:
+        dist.broadcast(t, src=src, group=group)
+        nbytes += t.numel() * t.element_size()
+    if tensors and tensors[0].is_cuda:
+        import torch
+        torch.cuda.synchronize()
+    if rank != src:
+        ctx.commit_shared()
+    return nbytes
+
+
+def max_over_ranks(values, dist, device=None):
+    """Element-wise max of a list of floats over all ranks (timings are max-over-ranks)."""
+    import torch
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
