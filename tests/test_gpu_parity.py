@@ -231,3 +231,56 @@ def test_adopt_shared_state_bitwise(glsmod):
     finally:
         root.close()
         other.close()
+
+
+@pytest.fixture(scope="module")
+def n1e4_factor():
+    """Oracle Cholesky of the n = 1e4 M of configs 2-4 (computed once, ~10 s on 16 cores)."""
+    P = gen.config_problem(gen.CONFIGS[2])
+    return P, oracle.cholesky(P.M)
+
+
+def test_config2_full_size_sampled_parity_and_planted_beta(glsmod, n1e4_factor):
+    """Config 2 at full size (n=1e4, m=1e6, one launch, the bench configuration): oracle parity on a
+    seeded sample plus panel / wave / tail edges; then the planted-beta identity on ALL 1e6 SNPs."""
+    cfg = gen.CONFIGS[2]
+    P, L = n1e4_factor
+    Xd = torch.empty((cfg.cols, cfg.n), dtype=torch.float64, device="cuda")
+    for c in range(0, cfg.cols, 65536):
+        k = min(65536, cfg.cols - c)
+        glsmod.gen_xr_device(SEED, cfg.n, c, k, Xd[c:c + k])
+    b, st, _ = run_gpu(glsmod, P, Xd, cfg.m, cfg.pR)
+    assert np.all(st == 0)
+    rng = np.random.default_rng(2)
+    wave = 148 * 64
+    edges = [0, 63, 64, wave - 1, wave, 105 * wave, cfg.m - 64, cfg.m - 1]
+    sel = np.unique(np.concatenate([rng.choice(cfg.m, 40, replace=False), edges]))
+    XRs = np.concatenate([gen.make_XR(SEED, cfg.n, int(i), 1) for i in sel])
+    b_or, st_or = oracle.gls_sequence(L, P.XL, P.y, XRs, 1, sel=sel, xr_is_selected=True)
+    err = assert_parity(b[sel], st[sel], b_or, st_or, label="config2 sample")
+    print("config2 sampled guarded err %.3e normwise %.3e" % (err, normwise_err(b[sel], b_or)))
+    P0 = gen.config_problem(cfg, noise=0.0)
+    b0, st0, _ = run_gpu(glsmod, P0, Xd, cfg.m, cfg.pR)
+    ref = np.concatenate([P0.beta_L, [0.0]])
+    assert np.all(st0 == 0)
+    assert np.max(np.abs(b0 - ref)) / np.max(np.abs(P0.beta_L)) <= 1e-10
+
+
+def test_config3_shape_sampled_parity(glsmod, n1e4_factor):
+    """Config-3 shape (n=1e4, pL=16 covariates, pR=4, p=20) on 4000 groups: sampled oracle parity;
+    the planted-beta identity on all groups."""
+    cfg = gen.CONFIGS[3]
+    m = 4000
+    P = gen.config_problem(cfg)
+    L = oracle.cholesky(P.M) if P.M.shape != n1e4_factor[0].M.shape or not np.array_equal(
+        P.M, n1e4_factor[0].M) else n1e4_factor[1]
+    XR = gen.make_XR(SEED, cfg.n, 0, m * cfg.pR)
+    b, st, _ = run_gpu(glsmod, P, dev(XR), m, cfg.pR)
+    sel = np.unique(np.concatenate([np.random.default_rng(3).choice(m, 24, replace=False), [0, 7, 8, 15, m - 1]]))
+    b_or, st_or = oracle.gls_sequence(L, P.XL, P.y, XR, cfg.pR, sel=sel)
+    err = assert_parity(b[sel], st[sel], b_or, st_or, label="config3 sample")
+    print("config3 sampled guarded err %.3e" % err)
+    P0 = gen.config_problem(cfg, noise=0.0)
+    b0, st0, _ = run_gpu(glsmod, P0, dev(XR), m, cfg.pR)
+    ref = np.concatenate([P0.beta_L, np.zeros(cfg.pR)])
+    assert np.max(np.abs(b0 - ref)) / np.max(np.abs(P0.beta_L)) <= 1e-10
