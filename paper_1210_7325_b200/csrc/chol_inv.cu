@@ -9,16 +9,18 @@
 //     A22 -= L21 L21^T                 (trailing SYRK, lower tiles only)
 //     (L22, T22) = chol_inv(A22)
 //     T21  = -T22 (L21 T11)            ([[L11,0],[L21,L22]]^{-1} = [[T11,0],[-T22 L21 T11, T22]])
-// Leaves (n <= 64) factor and invert one diagonal block inside one CTA.
+// Leaves (n <= 64) factor and invert one diagonal block inside one CTA in a single sweep.
 // NotSPD (reading A5): a pivot d_j <= 2^-52 * max_k M_kk records min(j) in st->fail.
 #include <climits>
+#include <vector>
 
 #include "gls_internal.cuh"
 
 namespace gls {
 namespace {
 
-constexpr int LEAF = 64;
+constexpr int LEAF = 96;
+constexpr int LEAF_THREADS = 1024;
 constexpr int LLD = LEAF + 1;
 
 __global__ void maxdiag_kernel(int64_t n, const double* A, int64_t ld, CholStatus* st) {
@@ -37,9 +39,12 @@ __global__ void maxdiag_kernel(int64_t n, const double* A, int64_t ld, CholStatu
   }
 }
 
-// One CTA: Cholesky of the nb x nb diagonal block at A (lower read), then its inverse.
-// Writes L into A's lower triangle and T = L^{-1} (with explicit zeros above the diagonal).
-__global__ void __launch_bounds__(256) chol_inv_leaf(int nb, double* A, double* T, int64_t ld,
+// One CTA: Cholesky of the nb x nb diagonal block at A (lower read) and, in the same sweep, its
+// inverse by forward elimination on [L | I]: after column j of L is final, row j of T is
+// T[j,:] /= L_jj and every later row is updated T[i,:] -= L_ij T[j,:] (i > j), so that on exit
+// L T = I.  Three barriers per column; writes L into A's lower triangle and T = L^{-1} (zeros
+// above the diagonal).
+__global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A, double* T, int64_t ld,
                                                      int64_t goff, CholStatus* st) {
   extern __shared__ double leaf_smem[];
   double* L = leaf_smem;
@@ -49,6 +54,7 @@ __global__ void __launch_bounds__(256) chol_inv_leaf(int nb, double* A, double* 
   for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
     const int i = idx % nb, j = idx / nb;
     L[i * LLD + j] = (i >= j) ? A[i + (int64_t)j * ld] : 0.0;
+    Ti[i * LLD + j] = (i == j) ? 1.0 : 0.0;
   }
   if (tid == 0) failed = 0;
   __syncthreads();
@@ -66,34 +72,46 @@ __global__ void __launch_bounds__(256) chol_inv_leaf(int nb, double* A, double* 
     }
     __syncthreads();
     const double ljj = L[j * LLD + j];
-    for (int i = j + 1 + tid; i < nb; i += blockDim.x) L[i * LLD + j] /= ljj;
-    __syncthreads();
     const int r = nb - j - 1;
-    for (int idx = tid; idx < r * r; idx += blockDim.x) {
-      const int i = j + 1 + idx / r, k = j + 1 + idx % r;
-      if (k <= i) L[i * LLD + k] -= L[i * LLD + j] * L[k * LLD + j];
+    const double rinv = 1.0 / ljj;
+    // scale: column j of L below the diagonal, row j of T (columns 0..j)
+    for (int idx = tid; idx < r + j + 1; idx += blockDim.x) {
+      if (idx < r) L[(j + 1 + idx) * LLD + j] *= rinv;
+      else Ti[j * LLD + (idx - r)] *= rinv;
+    }
+    __syncthreads();
+    // update: trailing lower triangle of L, and rows below j of T (columns 0..j); 32 x 32 threads
+    const int ty = tid >> 5, tx = tid & 31;
+    for (int i = j + 1 + ty; i < nb; i += 32) {
+      const double lij = L[i * LLD + j];
+      for (int k = j + 1 + tx; k <= i; k += 32) L[i * LLD + k] -= lij * L[k * LLD + j];
+      for (int k = tx; k <= j; k += 32) Ti[i * LLD + k] -= lij * Ti[j * LLD + k];
     }
     __syncthreads();
   }
-  // T = L^{-1}: column j solves L t = e_j by forward substitution (rows j..nb-1).
-  for (int j = tid; j < nb; j += blockDim.x) {
-    for (int i = 0; i < j; ++i) Ti[i * LLD + j] = 0.0;
-    for (int i = j; i < nb; ++i) {
-      double s = (i == j) ? 1.0 : 0.0;
-      for (int k = j; k < i; ++k) s -= L[i * LLD + k] * Ti[k * LLD + j];
-      Ti[i * LLD + j] = s / L[i * LLD + i];
-    }
-  }
-  __syncthreads();
   for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
     const int i = idx % nb, j = idx / nb;
     if (i >= j) A[i + (int64_t)j * ld] = L[i * LLD + j];
-    T[i + (int64_t)j * ld] = Ti[i * LLD + j];
+    T[i + (int64_t)j * ld] = (i >= j) ? Ti[i * LLD + j] : 0.0;
   }
 }
 
-void chol_inv_rec(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, int64_t goff,
-                  CholStatus* st, int64_t* lc) {
+struct RecCtx {
+  cudaStream_t s, aux;  // Y = L21 T11 runs on aux, overlapping the recursion on A22
+  std::vector<cudaEvent_t>* events;
+  CholStatus* st;
+  int64_t* lc;
+};
+
+cudaEvent_t new_event(RecCtx& rc) {
+  cudaEvent_t e;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  rc.events->push_back(e);
+  return e;
+}
+
+void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64_t goff) {
+  cudaStream_t s = rc.s;
   if (n <= LEAF) {
     constexpr int kLeafSmem = 2 * LEAF * LLD * sizeof(double);
     static bool attr = false;
@@ -101,8 +119,8 @@ void chol_inv_rec(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, i
       cudaFuncSetAttribute(chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
       attr = true;
     }
-    chol_inv_leaf<<<1, 256, kLeafSmem, s>>>((int)n, A, T, ld, goff, st);
-    if (lc) ++*lc;
+    chol_inv_leaf<<<1, LEAF_THREADS, kLeafSmem, s>>>((int)n, A, T, ld, goff, rc.st);
+    if (rc.lc) ++*rc.lc;
     return;
   }
   const int64_t nblk = (n + LEAF - 1) / LEAF;
@@ -113,15 +131,22 @@ void chol_inv_rec(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, i
   double* T11 = T;
   double* T21 = T + h1;
   double* T22 = T + h1 + h1 * ld;
-  chol_inv_rec(s, h1, A11, T11, ld, goff, st, lc);
+  chol_inv_rec(rc, h1, A11, T11, ld, goff);
   // L21 = A21 T11^T  -> stored in T21's (still unused) place
-  dgemm(s, h2, h1, h1, 1.0, A21, ld, 'N', T11, ld, 'T', 0.0, T21, ld, GEMM_KMAX_COL, lc);
+  dgemm(s, h2, h1, h1, 1.0, A21, ld, 'N', T11, ld, 'T', 0.0, T21, ld, GEMM_KMAX_COL, rc.lc);
   // A22 -= L21 L21^T (lower)
-  dgemm(s, h2, h2, h1, -1.0, T21, ld, 'N', T21, ld, 'T', 1.0, A22, ld, GEMM_LOWER_C, lc);
-  chol_inv_rec(s, h2, A22, T22, ld, goff + h1, st, lc);
-  // Y = L21 T11 -> A21's place;  T21 = -T22 Y
-  dgemm(s, h2, h1, h1, 1.0, T21, ld, 'N', T11, ld, 'N', 0.0, A21, ld, GEMM_KMIN_COL, lc);
-  dgemm(s, h2, h1, h2, -1.0, T22, ld, 'N', A21, ld, 'N', 0.0, T21, ld, GEMM_KMAX_ROW, lc);
+  dgemm(s, h2, h2, h1, -1.0, T21, ld, 'N', T21, ld, 'T', 1.0, A22, ld, GEMM_LOWER_C, rc.lc);
+  // Y = L21 T11 -> A21's place, on the aux stream: it only needs L21 and T11, so it overlaps the
+  // (latency-bound) recursion on A22, which touches A22 and T22 only.
+  cudaEvent_t e1 = new_event(rc), e2 = new_event(rc);
+  cudaEventRecord(e1, s);
+  cudaStreamWaitEvent(rc.aux, e1, 0);
+  dgemm(rc.aux, h2, h1, h1, 1.0, T21, ld, 'N', T11, ld, 'N', 0.0, A21, ld, GEMM_KMIN_COL, rc.lc);
+  cudaEventRecord(e2, rc.aux);
+  chol_inv_rec(rc, h2, A22, T22, ld, goff + h1);
+  // T21 = -T22 Y  (overwrites L21: Y must be complete)
+  cudaStreamWaitEvent(s, e2, 0);
+  dgemm(s, h2, h1, h2, -1.0, T22, ld, 'N', A21, ld, 'N', 0.0, T21, ld, GEMM_KMAX_ROW, rc.lc);
 }
 
 }  // namespace
@@ -134,7 +159,19 @@ void chol_prepare(cudaStream_t s, int64_t n, const double* A, int64_t ld, CholSt
 
 void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholStatus* st,
               int64_t* lc) {
-  chol_inv_rec(s, n, A, T, ld, 0, st, lc);
+  cudaStream_t aux;
+  cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
+  std::vector<cudaEvent_t> events;
+  RecCtx rc{s, aux, &events, st, lc};
+  chol_inv_rec(rc, n, A, T, ld, 0);
+  // join: everything issued on aux is ordered before later work on s
+  cudaEvent_t done;
+  cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+  cudaEventRecord(done, aux);
+  cudaStreamWaitEvent(s, done, 0);
+  cudaEventDestroy(done);
+  for (cudaEvent_t e : events) cudaEventDestroy(e);
+  cudaStreamDestroy(aux);
 }
 
 }  // namespace gls

@@ -1,23 +1,35 @@
 // dgemm.cu -- generic FP64 GEMM on the B200 FP64 tensor pipe (mma.sync m8n8k4 f64 -> DMMA.8x8x4).
 //
 // Used only by the once-per-context setup (gls_create): the recursive Cholesky + inverse of M
-// (PAPER.md:312, Alg. 5 line 1; DESIGN.md "Setup"), X~_L = L^{-1} X_L, y~ = L^{-1} y
+// (PAPER.md:312, Alg. 5 line 1; DESIGN.md §5.3), X~_L = L^{-1} X_L, y~ = L^{-1} y
 // (Alg. 5 lines 2, 4) and S_TL / b_T (Alg. 5 lines 5, 6).  Not on the per-block hot path.
 //
-// Tile 64 x 64 x 16, 4 warps (2 x 2, 32 x 32 each), register-prefetched double buffer.
+// Tile 128 x 64 x 16, 8 warps (4 x 2, 32 x 32 each), 3-stage cp.async (LDGSTS) pipeline with
+// zero-fill for ragged edges, any leading dimension / transpose.  Shared tiles are [row][k] with a
+// 20-double row stride: the m8n8k4 fragment loads (lane (m, k) = (l/4, l%4)) are conflict-free.
 // Triangular operands skip all-zero K ranges through GemmFlags.
 #include "gls_internal.cuh"
 
 namespace gls {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, LDS_ = 20;  // smem row stride 20 doubles: conflict-free frags
+constexpr int BM = 128, BN = 64, BK = 16, LDS_ = 20, STAGES = 3, THREADS = 256;
+constexpr int A_TILE = BM * LDS_, B_TILE = BN * LDS_;
+constexpr int SMEM_BYTES = STAGES * (A_TILE + B_TILE) * 8;
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  const int sz = valid ? 8 : 0;  // src-size 0 -> zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 struct GemmParams {
   int64_t M, N, K;
@@ -32,83 +44,83 @@ struct GemmParams {
 };
 
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(128) dgemm_kernel(GemmParams p) {
-  __shared__ double As[2][BM * LDS_];
-  __shared__ double Bs[2][BN * LDS_];
+__global__ void __launch_bounds__(THREADS, 2) dgemm_kernel(GemmParams p) {
+  extern __shared__ double sm[];
+  double* As = sm;
+  double* Bs = sm + STAGES * A_TILE;
   const int64_t r0 = (int64_t)blockIdx.x * BM, c0 = (int64_t)blockIdx.y * BN;
   if ((p.flags & GEMM_LOWER_C) && c0 >= r0 + BM) return;
   int64_t kb = 0, ke = p.K;
   if (p.flags & GEMM_KMIN_COL) kb = (c0 / BK) * BK;
   if (p.flags & GEMM_KMAX_ROW) ke = min(ke, r0 + BM);
   if (p.flags & GEMM_KMAX_COL) ke = min(ke, c0 + BN);
+  const int64_t kbeg = kb;  // element-level lower bound for the zero fill
+  kb = (kb / BK) * BK;
+  const int nk = (ke > kb) ? (int)((ke - kb + BK - 1) / BK) : 0;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
+  const int wm = warp & 3, wn = warp >> 2;
+
+  auto issue = [&](int kt, int stg) {
+    const int64_t k0 = kb + (int64_t)kt * BK;
+    double* as = As + stg * A_TILE;
+    double* bs = Bs + stg * B_TILE;
+#pragma unroll
+    for (int j = 0; j < (BM * BK) / THREADS; ++j) {  // 8
+      const int idx = tid + j * THREADS;
+      int m, k;
+      if (!TA) { m = idx % BM; k = idx / BM; } else { k = idx % BK; m = idx / BK; }
+      const int64_t gm = r0 + m, gk = k0 + k;
+      const bool v = gm < p.M && gk < ke && gk >= kbeg;
+      const double* src = v ? (TA ? p.A + gk + gm * p.lda : p.A + gm + gk * p.lda) : p.A;
+      cp_async8(as + m * LDS_ + k, src, v);
+    }
+#pragma unroll
+    for (int j = 0; j < (BN * BK) / THREADS; ++j) {  // 4
+      const int idx = tid + j * THREADS;
+      int n, k;
+      if (!TB) { k = idx % BK; n = idx / BK; } else { n = idx % BN; k = idx / BN; }
+      const int64_t gn = c0 + n, gk = k0 + k;
+      const bool v = gn < p.N && gk < ke && gk >= kbeg;
+      const double* src = v ? (TB ? p.B + gn + gk * p.ldb : p.B + gk + gn * p.ldb) : p.B;
+      cp_async8(bs + n * LDS_ + k, src, v);
+    }
+  };
+
   double acc[4][4][2];
 #pragma unroll
   for (int t = 0; t < 4; ++t)
 #pragma unroll
     for (int s = 0; s < 4; ++s) acc[t][s][0] = acc[t][s][1] = 0.0;
 
-  double ra[8], rb[8];
-  auto load = [&](int64_t k0) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int idx = tid + j * 128;
-      // op(A)[m][k]
-      int m, k;
-      if (!TA) { m = idx % BM; k = idx / BM; } else { k = idx % BK; m = idx / BK; }
-      const int64_t gm = r0 + m, gk = k0 + k;
-      double v = 0.0;
-      if (gm < p.M && gk < ke && gk >= kb) v = TA ? p.A[gk + gm * p.lda] : p.A[gm + gk * p.lda];
-      ra[j] = v;
-      // op(B)[k][n]
-      int n;
-      if (!TB) { k = idx % BK; n = idx / BK; } else { n = idx % BN; k = idx / BN; }
-      const int64_t gn = c0 + n, gk2 = k0 + k;
-      double w = 0.0;
-      if (gn < p.N && gk2 < ke && gk2 >= kb) w = TB ? p.B[gn + gk2 * p.ldb] : p.B[gk2 + gn * p.ldb];
-      rb[j] = w;
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int idx = tid + j * 128;
-      int m, k, n;
-      if (!TA) { m = idx % BM; k = idx / BM; } else { k = idx % BK; m = idx / BK; }
-      As[buf][m * LDS_ + k] = ra[j];
-      if (!TB) { k = idx % BK; n = idx / BK; } else { n = idx % BN; k = idx / BN; }
-      Bs[buf][n * LDS_ + k] = rb[j];
-    }
-  };
-
   const int l4 = lane >> 2, kk = lane & 3;
-  int buf = 0;
-  if (kb < ke) {
-    load(kb);
-    store(0);
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) issue(s, s);
+    cp_async_commit();
   }
-  __syncthreads();
-  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
-    const bool more = k0 + BK < ke;
-    if (more) load(k0 + BK);
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nxt = kt + STAGES - 1;
+    if (nxt < nk) issue(nxt, nxt % STAGES);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * A_TILE;
+    const double* bs = Bs + (kt % STAGES) * B_TILE;
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       double a[4], b[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) a[t] = As[buf][(wm * 32 + t * 8 + l4) * LDS_ + ks * 4 + kk];
+      for (int t = 0; t < 4; ++t) a[t] = as[(wm * 32 + t * 8 + l4) * LDS_ + ks * 4 + kk];
 #pragma unroll
-      for (int s = 0; s < 4; ++s) b[s] = Bs[buf][(wn * 32 + s * 8 + l4) * LDS_ + ks * 4 + kk];
+      for (int s = 0; s < 4; ++s) b[s] = bs[(wn * 32 + s * 8 + l4) * LDS_ + ks * 4 + kk];
 #pragma unroll
       for (int t = 0; t < 4; ++t)
 #pragma unroll
         for (int s = 0; s < 4; ++s) dmma(acc[t][s], a[t], b[s]);
     }
-    if (more) store(buf ^ 1);
-    __syncthreads();
-    buf ^= 1;
   }
+  cp_async_wait<0>();
   // epilogue: lane holds C[m = l4][n = 2kk + e] of each 8x8 tile
 #pragma unroll
   for (int t = 0; t < 4; ++t)
@@ -127,6 +139,16 @@ __global__ void __launch_bounds__(128) dgemm_kernel(GemmParams p) {
       }
 }
 
+template <bool TA, bool TB>
+void launch(cudaStream_t s, dim3 grid, const GemmParams& p) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dgemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr = true;
+  }
+  dgemm_kernel<TA, TB><<<grid, THREADS, SMEM_BYTES, s>>>(p);
+}
+
 }  // namespace
 
 void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
@@ -136,10 +158,10 @@ void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const 
   GemmParams p{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, flags};
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
   const bool ta = (opA == 'T'), tb = (opB == 'T');
-  if (!ta && !tb) dgemm_kernel<false, false><<<grid, 128, 0, s>>>(p);
-  else if (!ta && tb) dgemm_kernel<false, true><<<grid, 128, 0, s>>>(p);
-  else if (ta && !tb) dgemm_kernel<true, false><<<grid, 128, 0, s>>>(p);
-  else dgemm_kernel<true, true><<<grid, 128, 0, s>>>(p);
+  if (!ta && !tb) launch<false, false>(s, grid, p);
+  else if (!ta && tb) launch<false, true>(s, grid, p);
+  else if (ta && !tb) launch<true, false>(s, grid, p);
+  else launch<true, true>(s, grid, p);
   if (launch_counter) ++*launch_counter;
 }
 

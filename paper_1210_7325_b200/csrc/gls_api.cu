@@ -4,8 +4,10 @@
 // (Alg. 8 ooc-hp-gwas; workspaces fig:workspaces PAPER.md:633-653).
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -162,17 +164,31 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
       return rc;                               \
     }                                          \
   } while (0)
+  // GLS_TRACE=1 prints host-side phase times of the setup (diagnostics only)
+  static const bool trace = getenv("GLS_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(s);
+    auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[gls] setup %-10s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   const size_t nn = (size_t)n * (size_t)n * sizeof(double);
   CKS(cudaMalloc(&A, nn));
   CKS(cudaMalloc(&T, nn));
   CKS(cudaMalloc(&B, (size_t)n * (pL + 1) * sizeof(double)));
   CKS(cudaMalloc(&W, (size_t)n * (pL + 1) * sizeof(double)));
   CKS(cudaMalloc(&st, sizeof(CholStatus)));
+  mark("alloc");
   CKS(cudaMemcpyAsync(A, M, nn, cudaMemcpyDefault, s));
   CKS(cudaMemsetAsync(T, 0, nn, s));
+  mark("copy+zero");
   chol_prepare(s, n, A, n, st, &c->launches);
   chol_inv(s, n, A, T, n, st, &c->launches);
   CKS(cudaGetLastError());
+  mark("chol_inv");
   CKS(cudaMemcpyAsync(&hst, st, sizeof hst, cudaMemcpyDeviceToHost, s));
   CKS(cudaStreamSynchronize(s));
   if (hst.fail != ULLONG_MAX) {
@@ -189,11 +205,14 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   CKS(cudaMemcpyAsync(B + (size_t)n * pL, y, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
   dgemm(s, n, pL + 1, n, 1.0, T, n, 'N', B, n, 'N', 0.0, W, n, GEMM_KMAX_ROW, &c->launches);
   dgemm(s, pL + 1, pL + 1, n, 1.0, W, n, 'T', W, n, 'N', 0.0, c->G, pL + 1, 0, &c->launches);
+  mark("W,G");
   pack_T(s, T, n, n, c->NB, c->Tpk, &c->launches);
   pack_W(s, W, n, n, pL + 1, c->NB, c->NW, c->Wpk, &c->launches);
   CKS(cudaGetLastError());
   CKS(cudaStreamSynchronize(s));
+  mark("pack");
   cleanup();
+  mark("free");
 #undef CKS
   return GLS_OK;
 }
