@@ -90,6 +90,34 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync on the context's own
+// stream); freed blocks stay cached in the pool (release threshold GLS_POOL_KEEP_BYTES, default
+// 8 GiB) so a create/destroy cycle does not pay cudaMalloc/cudaFree page mapping every time.
+void configure_pool(int device) {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  uint64_t keep = 8ull << 30;
+  if (const char* e = getenv("GLS_POOL_KEEP_BYTES")) keep = strtoull(e, nullptr, 10);
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t dalloc(gls_ctx* c, T** p, size_t bytes) {
+  return cudaMallocAsync((void**)p, bytes, c->own_stream);
+}
+template <typename T>
+void dfree(gls_ctx* c, T*& p) {
+  if (p) cudaFreeAsync(p, c->own_stream);
+  p = nullptr;
+}
+
 int check_dims(int64_t n, int32_t pL, int32_t pR) {
   if (pL < 0 || pR < 1) return GLS_ERR_DIM;
   const int64_t p = (int64_t)pL + pR;
@@ -120,19 +148,19 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
   c->Tpk_bytes = (size_t)tpk_total_tiles(c->NB) * kTileDoubles * sizeof(double);
   c->Wpk_bytes = (size_t)c->NB * wpk_rb_doubles(c->NW) * sizeof(double);
   c->G_bytes = (size_t)(pL + 1) * (pL + 1) * sizeof(double);
-  CK(c, cudaMalloc(&c->Tpk, c->Tpk_bytes));
-  CK(c, cudaMalloc(&c->Wpk, c->Wpk_bytes));
-  CK(c, cudaMalloc(&c->G, c->G_bytes));
+  configure_pool(c->device);
+  CK(c, dalloc(c, &c->Tpk, c->Tpk_bytes));
+  CK(c, dalloc(c, &c->Wpk, c->Wpk_bytes));
+  CK(c, dalloc(c, &c->G, c->G_bytes));
+  CK(c, cudaStreamSynchronize(c->own_stream));  // buffers are used from other streams too
   return GLS_OK;
 }
 
 void free_staging(gls_ctx* c) {
   for (int k = 0; k < 2; ++k) {
-    if (c->stage[k]) cudaFree(c->stage[k]);
-    if (c->bstage[k]) cudaFree(c->bstage[k]);
-    if (c->sstage[k]) cudaFree(c->sstage[k]);
-    c->stage[k] = c->bstage[k] = nullptr;
-    c->sstage[k] = nullptr;
+    dfree(c, c->stage[k]);
+    dfree(c, c->bstage[k]);
+    dfree(c, c->sstage[k]);
   }
   c->stage_cols = 0;
   c->bstage_groups = 0;
@@ -148,11 +176,11 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   CholStatus hst;
   int rc = GLS_OK;
   auto cleanup = [&]() {
-    if (A) cudaFree(A);
-    if (T) cudaFree(T);
-    if (B) cudaFree(B);
-    if (W) cudaFree(W);
-    if (st) cudaFree(st);
+    dfree(c, A);
+    dfree(c, T);
+    dfree(c, B);
+    dfree(c, W);
+    dfree(c, st);
   };
 #define CKS(call)                              \
   do {                                         \
@@ -176,11 +204,11 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
     t0 = t1;
   };
   const size_t nn = (size_t)n * (size_t)n * sizeof(double);
-  CKS(cudaMalloc(&A, nn));
-  CKS(cudaMalloc(&T, nn));
-  CKS(cudaMalloc(&B, (size_t)n * (pL + 1) * sizeof(double)));
-  CKS(cudaMalloc(&W, (size_t)n * (pL + 1) * sizeof(double)));
-  CKS(cudaMalloc(&st, sizeof(CholStatus)));
+  CKS(dalloc(c, &A, nn));
+  CKS(dalloc(c, &T, nn));
+  CKS(dalloc(c, &B, (size_t)n * (pL + 1) * sizeof(double)));
+  CKS(dalloc(c, &W, (size_t)n * (pL + 1) * sizeof(double)));
+  CKS(dalloc(c, &st, sizeof(CholStatus)));
   mark("alloc");
   CKS(cudaMemcpyAsync(A, M, nn, cudaMemcpyDefault, s));
   CKS(cudaMemsetAsync(T, 0, nn, s));
@@ -219,13 +247,13 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
 
 int ensure_scratch(gls_ctx* c, int64_t groups) {
   if (groups <= c->scratch_groups) return GLS_OK;
-  if (c->bscratch) cudaFree(c->bscratch);
-  if (c->sscratch) cudaFree(c->sscratch);
-  c->bscratch = nullptr;
-  c->sscratch = nullptr;
+  CK(c, cudaStreamSynchronize(c->stream));  // the old scratch may still be in use there
+  dfree(c, c->bscratch);
+  dfree(c, c->sscratch);
   c->scratch_groups = 0;
-  CK(c, cudaMalloc(&c->bscratch, (size_t)groups * c->p * sizeof(double)));
-  CK(c, cudaMalloc(&c->sscratch, (size_t)groups * sizeof(int32_t)));
+  CK(c, dalloc(c, &c->bscratch, (size_t)groups * c->p * sizeof(double)));
+  CK(c, dalloc(c, &c->sscratch, (size_t)groups * sizeof(int32_t)));
+  CK(c, cudaStreamSynchronize(c->own_stream));
   c->scratch_groups = groups;
   return GLS_OK;
 }
@@ -237,11 +265,13 @@ int ensure_staging(gls_ctx* c, int64_t chunk_groups) {
   CK(c, cudaDeviceSynchronize());
   free_staging(c);
   for (int k = 0; k < 2; ++k) {
-    CK(c, cudaMalloc(&c->stage[k], (size_t)ld * cols * sizeof(double)));
-    CK(c, cudaMemset(c->stage[k], 0, (size_t)ld * cols * sizeof(double)));  // pad row (odd n) stays 0
-    CK(c, cudaMalloc(&c->bstage[k], (size_t)chunk_groups * c->p * sizeof(double)));
-    CK(c, cudaMalloc(&c->sstage[k], (size_t)chunk_groups * sizeof(int32_t)));
+    CK(c, dalloc(c, &c->stage[k], (size_t)ld * cols * sizeof(double)));
+    if (ld != c->n)  // the pad row of the odd-n staged copy must read as zero
+      CK(c, cudaMemsetAsync(c->stage[k], 0, (size_t)ld * cols * sizeof(double), c->own_stream));
+    CK(c, dalloc(c, &c->bstage[k], (size_t)chunk_groups * c->p * sizeof(double)));
+    CK(c, dalloc(c, &c->sstage[k], (size_t)chunk_groups * sizeof(int32_t)));
   }
+  CK(c, cudaStreamSynchronize(c->own_stream));
   c->stage_cols = cols;
   c->ld_stage = ld;
   c->bstage_groups = chunk_groups;
@@ -465,11 +495,12 @@ void gls_destroy(gls_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->d2h) cudaStreamSynchronize(c->d2h);
   free_staging(c);
-  if (c->bscratch) cudaFree(c->bscratch);
-  if (c->sscratch) cudaFree(c->sscratch);
-  if (c->Tpk) cudaFree(c->Tpk);
-  if (c->Wpk) cudaFree(c->Wpk);
-  if (c->G) cudaFree(c->G);
+  dfree(c, c->bscratch);
+  dfree(c, c->sscratch);
+  dfree(c, c->Tpk);
+  dfree(c, c->Wpk);
+  dfree(c, c->G);
+  if (c->own_stream) cudaStreamSynchronize(c->own_stream);
   for (int k = 0; k < 2; ++k) {
     if (c->ev_h2d[k]) cudaEventDestroy(c->ev_h2d[k]);
     if (c->ev_comp[k]) cudaEventDestroy(c->ev_comp[k]);
