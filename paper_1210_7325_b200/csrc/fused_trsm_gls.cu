@@ -102,9 +102,14 @@ struct KParams {
 template <int NW, bool FULL>
 struct KCfg {
   static constexpr int NG = FULL ? 10 : 4;  // Gram tiles per warp
-  static constexpr int STAGES = (NW == 1 && !FULL) ? 6 : 5;
   static constexpr int kWBytes = 1024 * NW * 8;  // packed W per row block
   static constexpr int kRedDoubles = (4 * NW + NG) * 64;
+  // as many 24 KiB stages as fit next to the W double buffer and the reduction scratch (<= 8)
+  static constexpr int kSmemCap = 232448 - 1024 - 256;
+  static constexpr int kFixed = 2 * kWBytes + 2 * kRedDoubles * 8;
+  static constexpr int kFit = (kSmemCap - kFixed) / (kXStageBytes + kTStageBytes);
+  static constexpr int STAGES = kFit < 8 ? kFit : 8;
+  static_assert(STAGES >= 3, "shared memory budget");
   static constexpr uint32_t off_X = 0;
   static constexpr uint32_t off_T = off_X + STAGES * kXStageBytes;
   static constexpr uint32_t off_W = off_T + STAGES * kTStageBytes;
@@ -218,8 +223,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // ------------------------------------------------------------------ DMMA consumers
-  const int mw = warp & 1;   // column half
-  const int ns = warp >> 1;  // z-row slice (32 rows of the 128-row block)
+  // warp -> (column half mw, z-row slice ns).  Warp w issues on SM sub-partition w % 4; slices are
+  // paired {0,3} on SMSPs 0-1 and {1,2} on SMSPs 2-3 so that the skipped all-zero tiles of the
+  // diagonal block (slice ns needs only its first 2ns+2 K tiles there) save the same time on every
+  // SMSP: 10 of 16 tile-units instead of 16.
+  const int smsp = warp & 3, half = warp >> 2;
+  const int mw = smsp & 1;                                             // column half
+  const int ns = (smsp < 2) ? (half ? 3 : 0) : (half ? 2 : 1);         // z-row slice (32 rows)
+  const int diag_keep = 2 * ns + 1;  // last useful K tile (within the diagonal block) of this slice
   const int kk = lane & 3, l4 = lane >> 2;
 
   // X^T fragment addresses: smem row = panel-local column, 16-byte chunk c = 2kk+P holds K rows
@@ -261,8 +272,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&full[st], ph);
       load_frag<ALIGNED>(F0, sX + st * kXStageBytes, sT + st * kTStageBytes, xoff, toff0, 0);
       for (int kt = kt0; kt < nkt; ++kt) {
+        // all-zero T tile for this slice (strictly above the diagonal of T_ii): loads and barriers
+        // stay in lock step, the DMMAs are skipped
+        const bool active = (kt - 8 * i) <= diag_keep;
         load_frag<ALIGNED>(F1, sX + st * kXStageBytes, sT + st * kTStageBytes, xoff, toff0, 1);
-        mma_frag(acc, F0);
+        if (active) mma_frag(acc, F0);
         const int cur = st;
         if (++st == C::STAGES) {
           st = 0;
@@ -272,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[st], ph);
           load_frag<ALIGNED>(F0, sX + st * kXStageBytes, sT + st * kTStageBytes, xoff, toff0, 0);
         }
-        mma_frag(acc, F1);
+        if (active) mma_frag(acc, F1);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[cur]);
       }
