@@ -284,3 +284,54 @@ def test_config3_shape_sampled_parity(glsmod, n1e4_factor):
     b0, st0, _ = run_gpu(glsmod, P0, dev(XR), m, cfg.pR)
     ref = np.concatenate([P0.beta_L, np.zeros(cfg.pR)])
     assert np.max(np.abs(b0 - ref)) / np.max(np.abs(P0.beta_L)) <= 1e-10
+
+
+def test_api_async_streams_and_errors(glsmod):
+    """gls_solve_block_ex async mode + gls_sync, gls_set_stream onto a torch stream, status NULL,
+    host b_out from device X_R, and argument errors (GLS_ERR_DIM / GLS_ERR_ARG)."""
+    n, m = 256, 300
+    P = gen.make_problem(n, 3, 1, seed=9)
+    XR = gen.make_XR(9, n, 0, m)
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, 1)
+    Xd = dev(XR)
+    with glsmod.Context(n, 3, 1, dev(P.M), dev(P.XL), dev(P.y)) as ctx:
+        s = torch.cuda.Stream()
+        ctx.set_stream(s.cuda_stream)
+        b1 = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+        ctx.solve_block(Xd, m, b1, None, async_=True)
+        ctx.sync()
+        assert_parity(b1.cpu().numpy(), np.zeros(m, np.int32), b_or, st_or, label="async")
+        ctx.set_stream(None)
+        bh = np.empty((m, 4))
+        sh = np.empty(m, dtype=np.int32)
+        ctx.solve_block(Xd, m, bh, sh)             # device X_R, host outputs
+        np.testing.assert_array_equal(bh, b1.cpu().numpy())
+        assert np.all(sh == 0)
+        # async host stream: several calls in flight, one sync
+        XRh = torch.from_numpy(XR).pin_memory()
+        bh2 = torch.empty((m, 4), dtype=torch.float64).pin_memory()
+        ctx.set_block_cols(64)
+        ctx.solve_block(XRh[:100], 100, bh2[:100], None, async_=True)
+        ctx.solve_block(XRh[100:], m - 100, bh2[100:], None, async_=True)
+        ctx.sync()
+        np.testing.assert_array_equal(bh2.numpy(), bh)
+        with pytest.raises(glsmod.GLSError) as e:
+            ctx.solve_block(Xd, 0, b1)
+        assert e.value.code == 2
+        import ctypes
+        L = glsmod.load()
+        assert L.gls_solve_block(ctx._h, None, m, b1.data_ptr()) == 1
+        assert L.gls_solve_block_ex(ctx._h, Xd.data_ptr(), m, b1.data_ptr(), None, 7) == 1
+
+
+def test_repeated_create_destroy_is_deterministic(glsmod):
+    """Pool-allocated contexts: create/solve/destroy three times gives identical bits."""
+    n, m = 300, 150
+    P = gen.make_problem(n, 2, 2, with_sex=False, seed=10)
+    Xd = dev(gen.make_XR(10, n, 0, 2 * m))
+    outs = []
+    for _ in range(3):
+        b, st, _ = run_gpu(glsmod, P, Xd, m, 2)
+        outs.append(b)
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])
