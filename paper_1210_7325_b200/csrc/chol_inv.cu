@@ -42,8 +42,10 @@ __global__ void maxdiag_kernel(int64_t n, const double* A, int64_t ld, CholStatu
 // One CTA: Cholesky of the nb x nb diagonal block at A (lower read) and, in the same sweep, its
 // inverse by forward elimination on [L | I]: after column j of L is final, row j of T is
 // T[j,:] /= L_jj and every later row is updated T[i,:] -= L_ij T[j,:] (i > j), so that on exit
-// L T = I.  Three barriers per column; writes L into A's lower triangle and T = L^{-1} (zeros
-// above the diagonal).
+// L T = I.  Two barriers per column: (A) every warp forms L_jj = sqrt(d_j) itself and the column
+// j of L / row j of T are scaled; (B) the rank-1 updates, with the operands of each thread's
+// (at most 3 x 3) items loaded into registers before the stores.  Writes L into A's lower
+// triangle and T = L^{-1} (zeros above the diagonal).
 __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A, double* T, int64_t ld,
                                                      int64_t goff, CholStatus* st) {
   extern __shared__ double leaf_smem[];
@@ -59,33 +61,60 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A,
   if (tid == 0) failed = 0;
   __syncthreads();
   const double tol = st->tol;
+  const int ty = tid >> 5, tx = tid & 31;
+  constexpr int R = LEAF / 32;  // items per thread per dimension
   for (int j = 0; j < nb; ++j) {
-    if (tid == 0) {
-      const double d = L[j * LLD + j];
-      if (!(d > tol) || failed) {
-        if (!failed) atomicMin(&st->fail, (unsigned long long)(goff + j));
-        failed = 1;
-        L[j * LLD + j] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: poisons the rest
-      } else {
-        L[j * LLD + j] = sqrt(d);
-      }
+    // (A) pivot (computed redundantly by every thread; thread 0 records failures) and scaling
+    // one lane per warp takes the square root and the reciprocal; shuffles broadcast them (the
+    // FP64 pipe is too slow for 1024 redundant sqrt/div per column)
+    const double d = L[j * LLD + j];
+    const bool bad = !(d > tol) || failed;
+    double ljj = 0.0, rinv = 0.0;
+    if ((tid & 31) == 0) {
+      ljj = bad ? __longlong_as_double(0x7ff8000000000000LL) : sqrt(d);  // NaN poisons the rest
+      rinv = 1.0 / ljj;
     }
-    __syncthreads();
-    const double ljj = L[j * LLD + j];
+    ljj = __shfl_sync(0xffffffffu, ljj, 0);
+    rinv = __shfl_sync(0xffffffffu, rinv, 0);
     const int r = nb - j - 1;
-    const double rinv = 1.0 / ljj;
-    // scale: column j of L below the diagonal, row j of T (columns 0..j)
     for (int idx = tid; idx < r + j + 1; idx += blockDim.x) {
       if (idx < r) L[(j + 1 + idx) * LLD + j] *= rinv;
       else Ti[j * LLD + (idx - r)] *= rinv;
     }
     __syncthreads();
-    // update: trailing lower triangle of L, and rows below j of T (columns 0..j); 32 x 32 threads
-    const int ty = tid >> 5, tx = tid & 31;
-    for (int i = j + 1 + ty; i < nb; i += 32) {
-      const double lij = L[i * LLD + j];
-      for (int k = j + 1 + tx; k <= i; k += 32) L[i * LLD + k] -= lij * L[k * LLD + j];
-      for (int k = tx; k <= j; k += 32) Ti[i * LLD + k] -= lij * Ti[j * LLD + k];
+    if (tid == 0) {
+      if (bad && !failed) {
+        atomicMin(&st->fail, (unsigned long long)(goff + j));
+        failed = 1;
+      }
+      L[j * LLD + j] = ljj;
+    }
+    // (B) trailing lower triangle of L and rows below j of T (columns 0..j); 32 x 32 threads
+#pragma unroll
+    for (int a = 0; a < R; ++a) {
+      const int i = j + 1 + ty + 32 * a;
+      if (i < nb) {
+        const double lij = L[i * LLD + j];
+        double lk[R], li[R], tj[R], ti[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+          const int k = j + 1 + tx + 32 * c;
+          const bool v = k <= i;
+          lk[c] = v ? L[k * LLD + j] : 0.0;
+          li[c] = v ? L[i * LLD + k] : 0.0;
+          const int k2 = tx + 32 * c;
+          const bool v2 = k2 <= j;
+          tj[c] = v2 ? Ti[j * LLD + k2] : 0.0;
+          ti[c] = v2 ? Ti[i * LLD + k2] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+          const int k = j + 1 + tx + 32 * c;
+          if (k <= i) L[i * LLD + k] = li[c] - lij * lk[c];
+          const int k2 = tx + 32 * c;
+          if (k2 <= j) Ti[i * LLD + k2] = ti[c] - lij * tj[c];
+        }
+      }
     }
     __syncthreads();
   }
