@@ -117,6 +117,19 @@ int gls_commit_shared(gls_ctx* ctx);
 /* Number of kernel launches this context issued so far (evidence counter for bench.py). */
 int64_t gls_kernel_launches(const gls_ctx* ctx);
 
+/* Arithmetic path of the trsm (Alg. 5 line 3).  Both give FP64-accurate b.
+ *   GLS_PATH_AUTO (default): blocks whose X_R values are all integers in [-128, 127] (SNP
+ *     genotypes) run on the int8 tensor cores with T = L^{-1} split into seven
+ *     base-256 digits per element (exact int32 digit products, one rounding of T to 55 bits per
+ *     row, reading A15); any other block runs on the FP64 tensor pipe.  Decided per device chunk
+ *     of the block, on the device (no host synchronisation).  Only for n <= 131071.
+ *   GLS_PATH_FP64: every block on the FP64 tensor pipe (DMMA).
+ * The environment variable GLS_PATH=fp64 sets the default of new contexts. */
+enum { GLS_PATH_AUTO = 0, GLS_PATH_FP64 = 1 };
+int gls_set_path(gls_ctx* ctx, int32_t path);  /* GLS_ERR_ARG for an unknown path */
+/* Evidence: how many int8 and FP64 hot-kernel launches did their work so far (synchronises). */
+int gls_path_counts(gls_ctx* ctx, int64_t* int8_launches, int64_t* fp64_launches);
+
 #ifdef __cplusplus
 }
 #endif

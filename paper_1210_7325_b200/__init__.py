@@ -3,4 +3,4 @@
 `gls` is the ctypes binding of libgls.so (C ABI in include/gls.h); `build` compiles the
 in-tree CUDA libraries for sm_100a.  See DESIGN.md.
 """
-from .gls import Context, GLSError, gen_xr_device, load  # noqa: F401
+from .gls import GLS_PATH_AUTO, GLS_PATH_FP64, Context, GLSError, gen_xr_device, load  # noqa: F401

@@ -90,6 +90,8 @@ struct KParams {
   const double* G;  // (pL+1)^2, column-major, ld = pL+1
   double* b_out;
   int32_t* status_out;
+  const int* gate;  // nullable: when set, run only if *gate != 0 (int8 path rejected the block)
+  unsigned long long* ran;  // nullable: block 0 adds 1 when the kernel does its work
   int64_t m_blk;
   int64_t num_panels;
   int NB;
@@ -157,6 +159,8 @@ __device__ __forceinline__ void mma_frag(double (&acc)[4][4][2], const Frag& f) 
 template <int NW, bool FULL, bool ALIGNED>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_trsm_gls_kernel(const __grid_constant__ CUtensorMap xmap, const KParams kp) {
+  if (kp.gate && *(volatile const int*)kp.gate == 0) return;  // uniform across the grid
+  if (kp.ran && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(kp.ran, 1ull);
   using C = KCfg<NW, FULL>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzled TMA destination, in the shared window
@@ -523,7 +527,7 @@ void pack_W(cudaStream_t s, const double* W, int64_t ld, int64_t n, int ncolsW, 
 }
 
 cudaError_t launch_fused_trsm_gls(cudaStream_t s, const SolveArgs& a, int num_sms, std::string* msg,
-                                  int64_t* lc) {
+                                  int64_t* lc, const int* gate, unsigned long long* ran) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) {
     if (msg) *msg = "cuTensorMapEncodeTiled unavailable from the driver";
@@ -555,6 +559,8 @@ cudaError_t launch_fused_trsm_gls(cudaStream_t s, const SolveArgs& a, int num_sm
   kp.G = a.G;
   kp.b_out = a.b_out;
   kp.status_out = a.status_out;
+  kp.gate = gate;
+  kp.ran = ran;
   kp.m_blk = a.m_blk;
   kp.num_panels = (a.m_blk + pg.gpp - 1) / pg.gpp;
   kp.NB = (int)a.NB;

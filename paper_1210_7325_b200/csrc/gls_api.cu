@@ -37,6 +37,21 @@ struct gls_ctx {
   size_t Wpk_bytes = 0;
   double* G = nullptr;
   size_t G_bytes = 0;
+  // int8 (Ozaki-split) path, ozaki_gls.cu: digit tiles of T and the per-row [sigma | W~] table
+  int8_t* T8 = nullptr;
+  size_t T8_bytes = 0;
+  double* aux = nullptr;
+  size_t aux_bytes = 0;
+  int path = GLS_PATH_AUTO;
+  bool oz_ok = false;  // n small enough for exact int32 digit products
+  // int8 conversion workspaces (two, swapping roles) and their rejection flags
+  cudaStream_t conv = nullptr;
+  int64_t x8_cols = 0, ld8 = 0;
+  int8_t* x8[2] = {nullptr, nullptr};
+  int* flags = nullptr;                  // 2 ints
+  unsigned long long* ran = nullptr;     // [0] int8 kernel launches that ran, [1] FP64 ones
+  cudaEvent_t ev_conv[2] = {}, ev_oz[2] = {};
+  uint64_t oseq = 0;
   // host-streaming workspaces (two, swapping roles -- fig:workspaces)
   int64_t block_cols = 0;
   int64_t stage_cols = 0, ld_stage = 0;
@@ -137,14 +152,21 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
   CK(c, cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+  CK(c, cudaStreamCreateWithFlags(&c->conv, cudaStreamNonBlocking));
   c->stream = c->own_stream;
   for (int k = 0; k < 2; ++k) {
+    CK(c, cudaEventCreateWithFlags(&c->ev_conv[k], cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_oz[k], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_h2d[k], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_comp[k], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_d2h[k], cudaEventDisableTiming));
   }
   const PanelGeom pg = panel_geom(pR);
-  c->block_cols = (int64_t)c->num_sms * pg.cpp;  // one wave of panels per chunk
+  c->oz_ok = n <= kOzMaxN;
+  if (const char* e = getenv("GLS_PATH")) c->path = (strcmp(e, "fp64") == 0) ? GLS_PATH_FP64 : GLS_PATH_AUTO;
+  // host-streamed chunks: one wave of FP64 panels, or 4 waves of 128-column int8 tiles
+  c->block_cols = c->oz_ok ? (int64_t)c->num_sms * 4 * 4 * (32 / pR) * pR
+                           : (int64_t)c->num_sms * pg.cpp;
   c->Tpk_bytes = (size_t)tpk_total_tiles(c->NB) * kTileDoubles * sizeof(double);
   c->Wpk_bytes = (size_t)c->NB * wpk_rb_doubles(c->NW) * sizeof(double);
   c->G_bytes = (size_t)(pL + 1) * (pL + 1) * sizeof(double);
@@ -152,6 +174,16 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
   CK(c, dalloc(c, &c->Tpk, c->Tpk_bytes));
   CK(c, dalloc(c, &c->Wpk, c->Wpk_bytes));
   CK(c, dalloc(c, &c->G, c->G_bytes));
+  CK(c, dalloc(c, &c->flags, 2 * sizeof(int)));
+  CK(c, dalloc(c, &c->ran, 2 * sizeof(unsigned long long)));
+  CK(c, cudaMemsetAsync(c->ran, 0, 2 * sizeof(unsigned long long), c->own_stream));
+  if (c->oz_ok) {
+    const int64_t NBR = (n + kOzR - 1) / kOzR;
+    c->T8_bytes = (size_t)oz_total_tiles(NBR) * kOzTileBytes;
+    c->aux_bytes = (size_t)NBR * kOzR * (pL + 2) * sizeof(double);
+    CK(c, dalloc(c, &c->T8, c->T8_bytes));
+    CK(c, dalloc(c, &c->aux, c->aux_bytes));
+  }
   CK(c, cudaStreamSynchronize(c->own_stream));  // buffers are used from other streams too
   return GLS_OK;
 }
@@ -172,6 +204,7 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   const int pL = c->pL;
   cudaStream_t s = c->stream;
   double *A = nullptr, *T = nullptr, *B = nullptr, *W = nullptr;
+  int* esc = nullptr;
   CholStatus* st = nullptr;
   CholStatus hst;
   int rc = GLS_OK;
@@ -180,6 +213,7 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
     dfree(c, T);
     dfree(c, B);
     dfree(c, W);
+    dfree(c, esc);
     dfree(c, st);
   };
 #define CKS(call)                              \
@@ -209,6 +243,7 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   CKS(dalloc(c, &B, (size_t)n * (pL + 1) * sizeof(double)));
   CKS(dalloc(c, &W, (size_t)n * (pL + 1) * sizeof(double)));
   CKS(dalloc(c, &st, sizeof(CholStatus)));
+  if (c->oz_ok) CKS(dalloc(c, &esc, (size_t)((n + kOzR - 1) / kOzR) * kOzR * sizeof(int)));
   mark("alloc");
   CKS(cudaMemcpyAsync(A, M, nn, cudaMemcpyDefault, s));
   CKS(cudaMemsetAsync(T, 0, nn, s));
@@ -236,6 +271,7 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   mark("W,G");
   pack_T(s, T, n, n, c->NB, c->Tpk, &c->launches);
   pack_W(s, W, n, n, pL + 1, c->NB, c->NW, c->Wpk, &c->launches);
+  if (c->oz_ok) oz_setup(s, T, n, n, W, pL + 1, c->T8, c->aux, esc, &c->launches);
   CKS(cudaGetLastError());
   CKS(cudaStreamSynchronize(s));
   mark("pack");
@@ -278,7 +314,8 @@ int ensure_staging(gls_ctx* c, int64_t chunk_groups) {
   return GLS_OK;
 }
 
-int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt) {
+int run_fp64(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt,
+             const int* gate) {
   SolveArgs a;
   a.X = X;
   a.ldx = ldx;
@@ -293,12 +330,103 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
   a.b_out = b;
   a.status_out = stt;
   std::string msg;
-  cudaError_t e = launch_fused_trsm_gls(c->stream, a, c->num_sms, &msg, &c->launches);
+  cudaError_t e = launch_fused_trsm_gls(c->stream, a, c->num_sms, &msg, &c->launches, gate, c->ran + 1);
   if (e != cudaSuccess) {
     c->err = msg;
     cudaGetLastError();
     return GLS_ERR_CUDA;
   }
+  return GLS_OK;
+}
+
+int ensure_x8(gls_ctx* c, int64_t cols) {
+  const int64_t ld8 = (c->n + 15) & ~(int64_t)15;
+  if (c->x8_cols >= cols && c->ld8 == ld8) return GLS_OK;
+  CK(c, cudaDeviceSynchronize());
+  dfree(c, c->x8[0]);
+  dfree(c, c->x8[1]);
+  c->x8_cols = 0;
+  for (int k = 0; k < 2; ++k) CK(c, dalloc(c, &c->x8[k], (size_t)ld8 * cols));
+  CK(c, cudaStreamSynchronize(c->own_stream));
+  c->x8_cols = cols;
+  c->ld8 = ld8;
+  return GLS_OK;
+}
+
+int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* b, int32_t* stt,
+             const int* gate) {
+  OzArgs a;
+  a.X8 = X8;
+  a.ld8 = ld8;
+  a.n = c->n;
+  a.pL = c->pL;
+  a.pR = c->pR;
+  a.m_blk = groups;
+  a.T8 = c->T8;
+  a.aux = c->aux;
+  a.G = c->G;
+  a.gate = gate;
+  a.ran = c->ran;
+  a.b_out = b;
+  a.status_out = stt;
+  std::string msg;
+  cudaError_t e = launch_ozaki_gls(c->stream, a, c->num_sms, &msg, &c->launches);
+  if (e != cudaSuccess) {
+    c->err = msg;
+    cudaGetLastError();
+    return GLS_ERR_CUDA;
+  }
+  return GLS_OK;
+}
+
+// One block of device-resident double X (column-major, ld = ldx, even, 16-byte aligned).
+// Path AUTO: chunks of 8 waves of int8 tiles; chunk j is converted to int8 on the conv stream
+// (flagging values that are not integers in [-128, 127]) while chunk j-1 is solved; then the int8
+// kernel and the FP64 kernel are both launched, each gated on the device by the chunk's flag, so
+// exactly one of them does the work and the host never waits.
+int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt) {
+  if (c->path == GLS_PATH_FP64 || !c->oz_ok) return run_fp64(c, X, ldx, groups, b, stt, nullptr);
+  const int pR = c->pR, p = c->p;
+  const int64_t cpt = 4 * (int64_t)((32 / pR) * pR);
+  int64_t chunk_groups = (int64_t)c->num_sms * cpt * 8 / pR;
+  if (chunk_groups > groups) chunk_groups = groups;
+  int rc = ensure_x8(c, chunk_groups * pR);
+  if (rc) return rc;
+  const int64_t nchunks = (groups + chunk_groups - 1) / chunk_groups;
+  auto issue_conv = [&](int64_t j) -> int {
+    const int buf = (int)((c->oseq + j) & 1);
+    const int64_t g0 = j * chunk_groups;
+    const int64_t gc = (groups - g0 < chunk_groups) ? groups - g0 : chunk_groups;
+    // ev_oz[buf] is recorded on the compute stream before the kernels of chunk j-1, i.e. after those
+    // of chunk j-2 (the previous users of x8[buf] and flags[buf]) and after whatever produced X.
+    CK(c, cudaEventRecord(c->ev_oz[buf], c->stream));
+    CK(c, cudaStreamWaitEvent(c->conv, c->ev_oz[buf], 0));
+    CK(c, cudaMemsetAsync(c->flags + buf, 0, sizeof(int), c->conv));
+    oz_convert(c->conv, X + (size_t)g0 * pR * ldx, ldx, c->n, gc * pR, c->x8[buf], c->ld8, c->flags + buf,
+               c->num_sms, &c->launches);
+    CK(c, cudaGetLastError());
+    CK(c, cudaEventRecord(c->ev_conv[buf], c->conv));
+    return GLS_OK;
+  };
+  rc = issue_conv(0);
+  if (rc) return rc;
+  for (int64_t j = 0; j < nchunks; ++j) {
+    const int buf = (int)((c->oseq + j) & 1);
+    const int64_t g0 = j * chunk_groups;
+    const int64_t gc = (groups - g0 < chunk_groups) ? groups - g0 : chunk_groups;
+    CK(c, cudaStreamWaitEvent(c->stream, c->ev_conv[buf], 0));
+    if (j + 1 < nchunks) {
+      rc = issue_conv(j + 1);
+      if (rc) return rc;
+    }
+    double* bj = b + (size_t)g0 * p;
+    int32_t* sj = stt ? stt + g0 : nullptr;
+    rc = run_int8(c, c->x8[buf], c->ld8, gc, bj, sj, c->flags + buf);
+    if (rc) return rc;
+    rc = run_fp64(c, X + (size_t)g0 * pR * ldx, ldx, gc, bj, sj, c->flags + buf);
+    if (rc) return rc;
+  }
+  c->oseq += nchunks;
   return GLS_OK;
 }
 
@@ -352,6 +480,7 @@ int solve_streamed(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out, 
 
 int sync_all(gls_ctx* c) {
   CK(c, cudaStreamSynchronize(c->h2d));
+  CK(c, cudaStreamSynchronize(c->conv));
   CK(c, cudaStreamSynchronize(c->stream));
   CK(c, cudaStreamSynchronize(c->d2h));
   return GLS_OK;
@@ -415,6 +544,13 @@ int gls_shared_view(gls_ctx* c, void** ptrs, int64_t* bytes, int32_t* count) {
   ptrs[2] = c->G;
   bytes[2] = (int64_t)c->G_bytes;
   *count = 3;
+  if (c->oz_ok) {
+    ptrs[3] = c->T8;
+    bytes[3] = (int64_t)c->T8_bytes;
+    ptrs[4] = c->aux;
+    bytes[4] = (int64_t)c->aux_bytes;
+    *count = 5;
+  }
   return GLS_OK;
 }
 
@@ -492,6 +628,7 @@ void gls_destroy(gls_ctx* c) {
   if (!c) return;
   DeviceGuard g(c->device);
   if (c->h2d) cudaStreamSynchronize(c->h2d);
+  if (c->conv) cudaStreamSynchronize(c->conv);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->d2h) cudaStreamSynchronize(c->d2h);
   free_staging(c);
@@ -500,17 +637,47 @@ void gls_destroy(gls_ctx* c) {
   dfree(c, c->Tpk);
   dfree(c, c->Wpk);
   dfree(c, c->G);
+  dfree(c, c->T8);
+  dfree(c, c->aux);
+  dfree(c, c->x8[0]);
+  dfree(c, c->x8[1]);
+  dfree(c, c->flags);
+  dfree(c, c->ran);
+  if (c->conv) cudaStreamSynchronize(c->conv);
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
   for (int k = 0; k < 2; ++k) {
     if (c->ev_h2d[k]) cudaEventDestroy(c->ev_h2d[k]);
     if (c->ev_comp[k]) cudaEventDestroy(c->ev_comp[k]);
     if (c->ev_d2h[k]) cudaEventDestroy(c->ev_d2h[k]);
+    if (c->ev_conv[k]) cudaEventDestroy(c->ev_conv[k]);
+    if (c->ev_oz[k]) cudaEventDestroy(c->ev_oz[k]);
   }
+  if (c->conv) cudaStreamDestroy(c->conv);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
   cudaGetLastError();
   delete c;
+}
+
+int gls_set_path(gls_ctx* c, int32_t path) {
+  if (!c) return GLS_ERR_ARG;
+  if (path != GLS_PATH_AUTO && path != GLS_PATH_FP64) return GLS_ERR_ARG;
+  c->path = path;
+  return GLS_OK;
+}
+
+int gls_path_counts(gls_ctx* c, int64_t* int8_launches, int64_t* fp64_launches) {
+  if (!c || !int8_launches || !fp64_launches) return GLS_ERR_ARG;
+  if (!c->ran) return GLS_ERR_STATE;
+  DeviceGuard g(c->device);
+  int rc = sync_all(c);
+  if (rc) return rc;
+  unsigned long long h[2];
+  CK(c, cudaMemcpy(h, c->ran, sizeof h, cudaMemcpyDeviceToHost));
+  *int8_launches = (int64_t)h[0];
+  *fp64_launches = (int64_t)h[1];
+  return GLS_OK;
 }
 
 int64_t gls_failed_pivot(const gls_ctx* c) { return c ? c->failed_pivot : -1; }

@@ -89,7 +89,47 @@ struct SolveArgs {
   int32_t* status_out;  // device or nullptr
 };
 // Returns cudaSuccess or the launch error; msg receives a description on failure.
+// gate (nullable, device): when non-null the kernel returns at once unless *gate != 0 (it is the
+// fallback for blocks the int8 path rejected).
 cudaError_t launch_fused_trsm_gls(cudaStream_t s, const SolveArgs& a, int num_sms, std::string* msg,
-                                  int64_t* launch_counter);
+                                  int64_t* launch_counter, const int* gate = nullptr,
+                                  unsigned long long* ran = nullptr);
+
+// ---------------------------------------------------------------- int8 (Ozaki-split) hot path
+constexpr int kOzR = 32;          // z rows per row block
+constexpr int kOzKC = 128;        // K per stage
+constexpr int kOzSlices = 7;      // base-256 digits per element of T (55-bit fixed point per row)
+constexpr int kOzTileBytes = kOzSlices * kOzR * kOzKC;  // 28 KiB packed digit tile
+// Largest n for which every digit product sum fits int32: 128 * 128 * n < 2^31.
+constexpr int64_t kOzMaxN = 131071;
+// Packed tile index of (row block i, K chunk 0); row block i holds i/4 + 1 chunks.
+__host__ __device__ inline int64_t oz_tile_offset(int64_t i) {
+  const int64_t q = i >> 2, r = i & 3;
+  return (q + 1) * (2 * q + r);
+}
+int64_t oz_total_tiles(int64_t NBR);
+// T (n x n lower, column-major) and W = [X~_L | y~] (n x pl1) -> digit tiles T8 and the per-row
+// aux table [sigma_r, W~_r,0 .. W~_r,pL] (stride pl1 + 1, ceil(n/32)*32 rows).  escale: int[rows].
+void oz_setup(cudaStream_t s, const double* T, int64_t ld, int64_t n, const double* W, int pl1,
+              int8_t* T8, double* aux, int* escale, int64_t* launch_counter);
+// X (double) -> X8 (int8, ld8 % 16 == 0); *flag |= 1 if some value is not an integer in [-128,127].
+void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t cols, int8_t* X8,
+                int64_t ld8, int* flag, int num_sms, int64_t* launch_counter);
+struct OzArgs {
+  const int8_t* X8;     // column-major, ld8 (multiple of 16), device
+  int64_t ld8;
+  int64_t n;
+  int pL, pR;
+  int64_t m_blk;
+  const int8_t* T8;
+  const double* aux;
+  const double* G;
+  const int* gate;      // nullable; the kernel does nothing when *gate != 0
+  unsigned long long* ran;  // nullable; block 0 adds 1 when the kernel does its work
+  double* b_out;
+  int32_t* status_out;
+};
+cudaError_t launch_ozaki_gls(cudaStream_t s, const OzArgs& a, int num_sms, std::string* msg,
+                             int64_t* launch_counter);
 
 }  // namespace gls

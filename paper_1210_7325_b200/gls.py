@@ -21,12 +21,14 @@ GLS_ERR_NOT_SPD = 3
 GLS_ERR_CUDA = 4
 GLS_ERR_OOM = 5
 GLS_ERR_STATE = 6
+GLS_PATH_AUTO = 0
+GLS_PATH_FP64 = 1
 
 ABI_SYMBOLS = (
     "gls_create", "gls_solve_block", "gls_solve_block_ex", "gls_sync", "gls_set_stream",
     "gls_set_block_cols", "gls_destroy", "gls_failed_pivot", "gls_last_error",
     "gls_error_string", "gls_create_adopt", "gls_shared_view", "gls_commit_shared",
-    "gls_kernel_launches",
+    "gls_kernel_launches", "gls_set_path", "gls_path_counts",
 )
 
 
@@ -80,6 +82,10 @@ def load(build_if_missing: bool = True):
     L.gls_commit_shared.restype = ctypes.c_int
     L.gls_kernel_launches.argtypes = [vp]
     L.gls_kernel_launches.restype = i64
+    L.gls_set_path.argtypes = [vp, i32]
+    L.gls_set_path.restype = ctypes.c_int
+    L.gls_path_counts.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.gls_path_counts.restype = ctypes.c_int
     _lib = L
     return L
 
@@ -177,6 +183,16 @@ class Context:
 
     def commit_shared(self):
         self._check(self._lib.gls_commit_shared(self._h))
+
+    def set_path(self, path: int):
+        """GLS_PATH_AUTO (int8 tensor cores for integer genotype blocks) or GLS_PATH_FP64."""
+        self._check(self._lib.gls_set_path(self._h, path))
+
+    def path_counts(self):
+        """(int8 hot-kernel launches that did work, FP64 ones) -- synchronises the context."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self._lib.gls_path_counts(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
 
     @property
     def kernel_launches(self) -> int:

@@ -31,10 +31,12 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def run_gpu(pkg, P, XR_dev, m, pR, host_out=False, status=True):
+def run_gpu(pkg, P, XR_dev, m, pR, host_out=False, status=True, path=None, counts=None):
     p = P.pL + pR
     ctx = pkg.Context(P.n, P.pL, pR, dev(P.M), dev(P.XL) if P.pL else None, dev(P.y))
     try:
+        if path is not None:
+            ctx.set_path(path)
         if host_out:
             b = np.empty((m, p))
             st = np.empty(m, dtype=np.int32)
@@ -43,6 +45,8 @@ def run_gpu(pkg, P, XR_dev, m, pR, host_out=False, status=True):
             st = torch.empty(m, dtype=torch.int32, device="cuda")
         ctx.solve_block(XR_dev, m, b, st if status else None)
         launches = ctx.kernel_launches
+        if counts is not None:
+            counts.extend(ctx.path_counts())
     finally:
         ctx.close()
     if not host_out:
@@ -87,11 +91,55 @@ def test_config0_all_snps(glsmod):
     (771, 19, 1, 40, False),    # p = 20 with pL = 19 (3 W tiles)
 ])
 def test_ragged_shapes(glsmod, n, pL, pR, m, sex):
+    """Both arithmetic paths (int8 digit split on tcgen05, FP64 DMMA) against the oracle."""
     P = gen.make_problem(n, pL, pR, with_sex=sex, seed=SEED + n)
     XR = gen.make_XR(SEED + n, n, 0, m * pR)
     b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, pR)
-    b, st, _ = run_gpu(glsmod, P, dev(XR), m, pR)
-    assert_parity(b, st, b_or, st_or, label="n=%d pL=%d pR=%d" % (n, pL, pR))
+    for path, want in ((glsmod.GLS_PATH_AUTO, 0), (glsmod.GLS_PATH_FP64, 1)):
+        counts = []
+        b, st, _ = run_gpu(glsmod, P, dev(XR), m, pR, path=path, counts=counts)
+        assert counts[want] >= 1 and counts[1 - want] == 0, counts
+        assert_parity(b, st, b_or, st_or, label="n=%d pL=%d pR=%d path=%d" % (n, pL, pR, path))
+
+
+def test_non_integer_block_falls_back_to_fp64(glsmod):
+    """Imputed dosages (non-integer X_R) are not int8-representable: AUTO must run the FP64 kernel
+    for that block, decided on the device, and still match the oracle."""
+    n, pL, pR, m = 700, 3, 1, 300
+    P = gen.make_problem(n, pL, pR, seed=21)
+    XR = gen.make_XR(21, n, 0, m)
+    XR = XR + 0.25 * (np.arange(XR.size).reshape(XR.shape) % 3 == 0)  # dosage-like fractions
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, pR)
+    counts = []
+    b, st, _ = run_gpu(glsmod, P, dev(XR), m, pR, counts=counts)
+    assert counts == [0, 1], counts
+    assert_parity(b, st, b_or, st_or, label="dosage fallback")
+    # a single out-of-range value (200 > 127) also rejects the block
+    XR2 = gen.make_XR(21, n, 0, m)
+    XR2[5, 17] = 200.0
+    b_or2, st_or2 = oracle.solve(P.M, P.XL, P.y, XR2, pR)
+    counts = []
+    b2, st2, _ = run_gpu(glsmod, P, dev(XR2), m, pR, counts=counts)
+    assert counts == [0, 1], counts
+    assert_parity(b2, st2, b_or2, st_or2, label="out-of-range fallback")
+
+
+def test_mixed_chunks_pick_paths_independently(glsmod):
+    """A device block spanning two int8 conversion chunks (8 waves of 128-column tiles each):
+    the integer chunk runs on int8, the chunk holding a dosage runs on FP64; all rows match."""
+    n, pL, pR = 64, 2, 1
+    chunk = 148 * 128 * 8
+    m = chunk + 5000
+    P = gen.make_problem(n, pL, pR, seed=22)
+    XR = gen.make_XR(22, n, 0, m)
+    XR[chunk + 123, 9] = 0.5
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, pR)
+    counts = []
+    b, st, _ = run_gpu(glsmod, P, dev(XR), m, pR, counts=counts)
+    props = torch.cuda.get_device_properties(0)
+    if props.multi_processor_count == 148:
+        assert counts == [1, 1], counts
+    assert_parity(b, st, b_or, st_or, label="mixed chunks")
 
 
 def test_host_stream_equals_device_bitwise(glsmod):
