@@ -39,6 +39,20 @@ UNIT = "SNPs/s"
 FP64_DMMA_PEAK_SUSTAINED = 36.86
 FP64_DMMA_PEAK_BURST = 37.10
 H2D_GBS = 55.6  # pinned host -> device, measured (profiles/r01_probe.txt)
+# int8 digit products per FP64 multiply-add of the trsm: T is split into 7 digits
+OZ_SLICES = 7
+
+
+def int8_peak():
+    """Dense int8 tensor peak for a kernel timed inside a long step: the driver-measured sustained
+    bf16 GEMM rate (MEASURED_PEAKS.json) x the nominal int8:bf16 ratio 4.5:2.25 (B200_PROFILING.md)."""
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return 2.0 * float(mp["bf16_tflops_sustained"]), (
+            "2 x bf16_tflops_sustained %.1f of MEASURED_PEAKS.json (nominal int8:bf16 = 4.5:2.25 PF dense)"
+            % float(mp["bf16_tflops_sustained"]))
+    except Exception:
+        return 2.0 * 1400.0, "2 x 1400 TF/s sustained bf16 (B200_PROFILING.md fallback)"
 
 
 def parse():
@@ -210,6 +224,7 @@ def main():
 
     kern_ms = []
     create_ms = []
+    timing = []
     launches = [0]
 
     def step(timed: bool):
@@ -218,6 +233,7 @@ def main():
         if timed:
             create_ms.append(1e3 * (time.perf_counter() - tc))
         ctx.set_stream(stream.cuda_stream)
+        ctx.set_timing(timed)
         k0 = torch.cuda.Event(enable_timing=True)
         k1 = torch.cuda.Event(enable_timing=True)
         k0.record(stream)
@@ -228,6 +244,8 @@ def main():
             launches[0] += ctx.kernel_launches
             k1.synchronize()
             kern_ms.append(k0.elapsed_time(k1))
+            timing.append(ctx.read_timing())
+            timing[-1]["paths"] = ctx.path_counts()
         ctx.close()
 
     for _ in range(args.warmup):
@@ -256,9 +274,13 @@ def main():
     # a sanity count of RankDeficient rows (seeded data has none).
     n_bad = int(st.sum().item())
 
-    # ---- roofline of the dominant kernel (fused_trsm_gls), algorithmic n^2 flops per column
-    flops_per_launch = float(n) * n * m * pR
-    achieved_tf = flops_per_launch / (kern_avg_ms / 1e3) / 1e12
+    # ---- roofline of the dominant kernel, timed per launch with CUDA events on its own stream
+    int8_ms = statistics.mean(t["int8_ms"] for t in timing)
+    fp64_ms = statistics.mean(t["fp64_ms"] for t in timing)
+    conv_ms = statistics.mean(t["conv_ms"] for t in timing)
+    int8_ms, fp64_ms, conv_ms, kern_avg_ms = multi.max_over_ranks([int8_ms, fp64_ms, conv_ms, kern_avg_ms],
+                                                                  dist, device="cuda")
+    flops_per_launch = float(n) * n * m * pR          # FP64 trsm flops, n^2 per X_R column (north star)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
@@ -266,59 +288,94 @@ def main():
             traffic = json.load(open(tfile)).get("config%d" % args.config)
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_DMMA_PEAK_SUSTAINED,
-                "unit": "TFLOP/s", "frac": achieved_tf / FP64_DMMA_PEAK_SUSTAINED, "traffic": traffic,
-                "kernel": "fused_trsm_gls_kernel", "kernel_ms": kern_avg_ms,
-                "create_ms": statistics.mean(create_ms),
-                "flops_per_launch": flops_per_launch,
-                "peak_source": "FP64 DMMA.8x8x4 microbenchmark on this pool's B200, 4 s sustained "
-                               "(profiles/r01_probe.txt); MEASURED_PEAKS.json has no FP64 entry"}
+    paths = timing[-1]["paths"]
+    if paths[0] > 0:   # int8 digit-split path (integer genotypes)
+        ops = OZ_SLICES * flops_per_launch           # int8 ops: 7 digit products per FP64 MAC
+        peak, psrc = int8_peak()
+        achieved = ops / (int8_ms / 1e3) / 1e12
+        fp64eq = flops_per_launch / (int8_ms / 1e3) / 1e12
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s (int8)",
+                    "frac": achieved / peak, "traffic": traffic, "kernel": "ozaki_trsm_gls_kernel",
+                    "kernel_ms": int8_ms, "int8_conversion_ms": conv_ms, "fp64_fallback_ms": fp64_ms,
+                    "solve_block_ms": kern_avg_ms, "create_ms": statistics.mean(create_ms),
+                    "int8_ops_per_launch": ops, "peak_source": psrc,
+                    "fp64_equivalent": {"achieved_tflops": fp64eq, "dmma_peak_tflops": FP64_DMMA_PEAK_SUSTAINED,
+                                        "ratio_to_dmma_peak": fp64eq / FP64_DMMA_PEAK_SUSTAINED,
+                                        "note": "n^2 FP64 trsm flops per column / kernel time; the FP64 "
+                                                "DMMA pipe peak is measured in profiles/r01_probe.txt"}}
+    else:              # FP64 DMMA path
+        achieved_tf = flops_per_launch / (fp64_ms / 1e3) / 1e12
+        roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_DMMA_PEAK_SUSTAINED,
+                    "unit": "TFLOP/s", "frac": achieved_tf / FP64_DMMA_PEAK_SUSTAINED, "traffic": traffic,
+                    "kernel": "fused_trsm_gls_kernel", "kernel_ms": fp64_ms, "solve_block_ms": kern_avg_ms,
+                    "create_ms": statistics.mean(create_ms), "flops_per_launch": flops_per_launch,
+                    "peak_source": "FP64 DMMA.8x8x4 microbenchmark on this pool's B200, 4 s sustained "
+                                   "(profiles/r01_probe.txt); MEASURED_PEAKS.json has no FP64 entry"}
 
-    # ---- e2e: same job through the C ABI with host buffers (rank's X_R pinned in host memory)
+    # ---- e2e: the same job through the C ABI with HOST buffers, host<->device copies inside the
+    # timed region (Alg. 8 double-buffered stream).  Primary: X_R as genotype codes (int8, one byte
+    # per genotype -- gls_solve_block_i8); secondary: X_R as FP64 (gls_solve_block, 8 bytes).
     e2e = None
     if not args.no_e2e:
-        # pinned host copy of the rank's X_R; shrink the e2e SNP count if host RAM cannot hold
-        # world x 80 GB (then e2e is measured on the first m_e2e SNPs of the rank's range)
         try:
             avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
         except (ValueError, OSError):
             avail = 1 << 40
         local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
-        m_e2e = int(min(m, 0.6 * avail / local_world / (n * pR * 8)))
-        m_e2e = max(m_e2e - m_e2e % 64, 64)
-        Xh = torch.empty((m_e2e * pR, n), dtype=torch.float64, pin_memory=True)
-        for c in range(0, m_e2e * pR, chunk):
-            k = min(chunk, m_e2e * pR - c)
-            Xh[c:c + k].copy_(Xd[c:c + k], non_blocking=False)
         Mh = torch.from_numpy(P.M).pin_memory()
         XLh = torch.from_numpy(np.ascontiguousarray(P.XL)).pin_memory()
         yh = torch.from_numpy(P.y).pin_memory()
-        bh = torch.empty((m_e2e, p), dtype=torch.float64, pin_memory=True)
-        sh = torch.empty(m_e2e, dtype=torch.int32, pin_memory=True)
-        ref_b = b[:m_e2e].cpu()
 
-        def e2e_step():
-            ctx = make_ctx(Mh, XLh, yh)
-            ctx.solve_block(Xh, m_e2e, bh, sh)
-            ctx.close()
+        def timed_e2e(solve, m_e):
+            bh = torch.empty((m_e, p), dtype=torch.float64, pin_memory=True)
+            sh = torch.empty(m_e, dtype=torch.int32, pin_memory=True)
 
-        for _ in range(1):
-            e2e_step()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_step()
-        torch.cuda.synchronize()
-        dt = multi.max_over_ranks([(time.perf_counter() - t0) / args.steps], dist, device="cuda")[0]
-        same = bool(torch.equal(bh, ref_b))
-        e2e = {"value": world * m_e2e / dt, "unit": UNIT,
-               "h2d_bytes_per_step": int((n * n + n * (pL + 1) + m_e2e * pR * n) * 8),
-               "d2h_bytes_per_step": int(m_e2e * p * 8 + m_e2e * 4),
-               "m_per_rank": m_e2e, "path": "C ABI, host X_R (pinned) -> double-buffered H2D stream",
-               "bitwise_equal_to_device_run": same}
+            def one():
+                ctx = make_ctx(Mh, XLh, yh)
+                solve(ctx, m_e, bh, sh)
+                ctx.close()
+
+            one()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                one()
+            torch.cuda.synchronize()
+            dt = multi.max_over_ranks([(time.perf_counter() - t0) / args.steps], dist, device="cuda")[0]
+            return dt, bool(torch.equal(bh, b[:m_e].cpu()))
+
+        # int8 genotype codes: m x n bytes per rank
+        m_i8 = int(min(m, 0.6 * avail / local_world / (n * pR)))
+        m_i8 = max(m_i8 - m_i8 % 64, 64)
+        Gh = torch.empty((m_i8 * pR, n), dtype=torch.int8, pin_memory=True)
+        for c in range(0, m_i8 * pR, chunk):
+            k = min(chunk, m_i8 * pR - c)
+            Gh[c:c + k].copy_(Xd[c:c + k].to(torch.int8))
+        dt8, same8 = timed_e2e(lambda ctx, me, bh, sh: ctx.solve_block_i8(Gh, me, bh, sh), m_i8)
+        del Gh
+        e2e = {"value": world * m_i8 / dt8, "unit": UNIT,
+               "h2d_bytes_per_step": int((n * n + n * (pL + 1)) * 8 + m_i8 * pR * n),
+               "d2h_bytes_per_step": int(m_i8 * p * 8 + m_i8 * 4),
+               "m_per_rank": m_i8,
+               "path": "C ABI gls_solve_block_i8: M, X_L, y (FP64) and X_R as int8 genotype codes in pinned "
+                       "host memory -> double-buffered H2D stream; b and status back to pinned host memory",
+               "bitwise_equal_to_device_run": same8}
+        # FP64 X_R from host (8 bytes per genotype over PCIe)
+        m_f = int(min(m, 0.6 * avail / local_world / (n * pR * 8)))
+        m_f = max(m_f - m_f % 64, 64)
+        Xh = torch.empty((m_f * pR, n), dtype=torch.float64, pin_memory=True)
+        for c in range(0, m_f * pR, chunk):
+            k = min(chunk, m_f * pR - c)
+            Xh[c:c + k].copy_(Xd[c:c + k])
+        dtf, samef = timed_e2e(lambda ctx, me, bh, sh: ctx.solve_block(Xh, me, bh, sh), m_f)
         del Xh
+        e2e["fp64_host_input"] = {"value": world * m_f / dtf, "unit": UNIT, "m_per_rank": m_f,
+                                  "h2d_bytes_per_step": int((n * n + n * (pL + 1) + m_f * pR * n) * 8),
+                                  "d2h_bytes_per_step": int(m_f * p * 8 + m_f * 4),
+                                  "path": "C ABI gls_solve_block, FP64 X_R in pinned host memory",
+                                  "bitwise_equal_to_device_run": samef}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

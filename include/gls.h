@@ -130,6 +130,22 @@ int gls_set_path(gls_ctx* ctx, int32_t path);  /* GLS_ERR_ARG for an unknown pat
 /* Evidence: how many int8 and FP64 hot-kernel launches did their work so far (synchronises). */
 int gls_path_counts(gls_ctx* ctx, int64_t* int8_launches, int64_t* fp64_launches);
 
+/* gls_solve_block_i8 -- as gls_solve_block_ex, with X_R given as genotype codes: G is n x
+ * (m_blk*pR) int8, column-major with leading dimension ldg >= n (element (r, c) at G[r + c*ldg]),
+ * each value the exact integer X_R entry (e.g. minor-allele counts 0/1/2).  Always the int8 path
+ * (GLS_ERR_DIM when n > 131071).  Device G with ldg % 16 == 0 and a 16-byte aligned base is read
+ * in place (no conversion pass); host G is streamed with double buffering (Alg. 8) at one byte
+ * per genotype.  Ownership and errors as gls_solve_block_ex; GLS_ERR_ARG if ldg < n. */
+int gls_solve_block_i8(gls_ctx* ctx, const int8_t* G, int64_t ldg, int64_t m_blk, double* b_out,
+                       int32_t* status_out, int async);
+
+/* Diagnostics for the benchmark: when enabled, every hot-kernel launch (and every int8 conversion
+ * pass) is bracketed by CUDA events on the stream it runs on.  gls_read_timing synchronises,
+ * returns the summed device milliseconds per kind since the last read, the number of timed
+ * launches, and resets. */
+int gls_set_timing(gls_ctx* ctx, int32_t enable);
+int gls_read_timing(gls_ctx* ctx, double* ms_int8, double* ms_fp64, double* ms_conv, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/gls.h"
 #include "gls_internal.cuh"
@@ -50,8 +51,20 @@ struct gls_ctx {
   int8_t* x8[2] = {nullptr, nullptr};
   int* flags = nullptr;                  // 2 ints
   unsigned long long* ran = nullptr;     // [0] int8 kernel launches that ran, [1] FP64 ones
-  cudaEvent_t ev_conv[2] = {}, ev_oz[2] = {};
+  cudaEvent_t ev_conv[2] = {}, ev_oz[2] = {}, ev_fb[2] = {};
+  cudaStream_t fb = nullptr;  // gated FP64 fallback launches (off the int8 kernel's stream)
   uint64_t oseq = 0;
+  // host int8 staging (gls_solve_block_i8 with a host or unaligned source)
+  int8_t* stage8[2] = {nullptr, nullptr};
+  int64_t stage8_cols = 0;
+  // optional per-launch timing of the hot kernels (gls_set_timing): event pairs on the launch stream
+  bool timing = false;
+  struct TimedLaunch {
+    cudaEvent_t a, b;
+    int kind;  // 0 int8 kernel, 1 FP64 kernel, 2 int8 conversion
+  };
+  std::vector<TimedLaunch> tl;
+  std::vector<cudaEvent_t> ev_pool;
   // host-streaming workspaces (two, swapping roles -- fig:workspaces)
   int64_t block_cols = 0;
   int64_t stage_cols = 0, ld_stage = 0;
@@ -153,10 +166,13 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
   CK(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->conv, cudaStreamNonBlocking));
+  CK(c, cudaStreamCreateWithFlags(&c->fb, cudaStreamNonBlocking));
   c->stream = c->own_stream;
   for (int k = 0; k < 2; ++k) {
     CK(c, cudaEventCreateWithFlags(&c->ev_conv[k], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_oz[k], cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_fb[k], cudaEventDisableTiming));
+    CK(c, cudaEventRecord(c->ev_fb[k], c->own_stream));
     CK(c, cudaEventCreateWithFlags(&c->ev_h2d[k], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_comp[k], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_d2h[k], cudaEventDisableTiming));
@@ -314,8 +330,41 @@ int ensure_staging(gls_ctx* c, int64_t chunk_groups) {
   return GLS_OK;
 }
 
+cudaEvent_t pool_event(gls_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return e;
+}
+// Brackets one launch on `s` with an event pair when timing is on (diagnostics for bench.py).
+struct LaunchTimer {
+  gls_ctx* c;
+  cudaStream_t s;
+  int kind;
+  cudaEvent_t a = nullptr;
+  LaunchTimer(gls_ctx* c_, cudaStream_t s_, int k) : c(c_), s(s_), kind(k) {
+    if (c->timing && (a = pool_event(c))) cudaEventRecord(a, s);
+  }
+  ~LaunchTimer() {
+    if (!a) return;
+    cudaEvent_t b = pool_event(c);
+    if (!b) return;
+    cudaEventRecord(b, s);
+    c->tl.push_back({a, b, kind});
+  }
+};
+
 int run_fp64(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt,
-             const int* gate) {
+             const int* gate, cudaStream_t strm = nullptr) {
+  if (!strm) strm = c->stream;
+  LaunchTimer lt(c, strm, 1);
   SolveArgs a;
   a.X = X;
   a.ldx = ldx;
@@ -330,7 +379,7 @@ int run_fp64(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b
   a.b_out = b;
   a.status_out = stt;
   std::string msg;
-  cudaError_t e = launch_fused_trsm_gls(c->stream, a, c->num_sms, &msg, &c->launches, gate, c->ran + 1);
+  cudaError_t e = launch_fused_trsm_gls(strm, a, c->num_sms, &msg, &c->launches, gate, c->ran + 1);
   if (e != cudaSuccess) {
     c->err = msg;
     cudaGetLastError();
@@ -355,6 +404,7 @@ int ensure_x8(gls_ctx* c, int64_t cols) {
 
 int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* b, int32_t* stt,
              const int* gate) {
+  LaunchTimer lt(c, c->stream, 0);
   OzArgs a;
   a.X8 = X8;
   a.ld8 = ld8;
@@ -401,7 +451,9 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
     // of chunk j-2 (the previous users of x8[buf] and flags[buf]) and after whatever produced X.
     CK(c, cudaEventRecord(c->ev_oz[buf], c->stream));
     CK(c, cudaStreamWaitEvent(c->conv, c->ev_oz[buf], 0));
+    CK(c, cudaStreamWaitEvent(c->conv, c->ev_fb[buf], 0));  // the fallback of chunk j-2 read flags[buf]
     CK(c, cudaMemsetAsync(c->flags + buf, 0, sizeof(int), c->conv));
+    LaunchTimer lt(c, c->conv, 2);
     oz_convert(c->conv, X + (size_t)g0 * pR * ldx, ldx, c->n, gc * pR, c->x8[buf], c->ld8, c->flags + buf,
                c->num_sms, &c->launches);
     CK(c, cudaGetLastError());
@@ -423,9 +475,15 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
     int32_t* sj = stt ? stt + g0 : nullptr;
     rc = run_int8(c, c->x8[buf], c->ld8, gc, bj, sj, c->flags + buf);
     if (rc) return rc;
-    rc = run_fp64(c, X + (size_t)g0 * pR * ldx, ldx, gc, bj, sj, c->flags + buf);
+    // the gated FP64 kernel runs on its own stream, so when it has nothing to do its launch never
+    // holds back the next int8 kernel (it would queue behind the running conversion pass)
+    CK(c, cudaStreamWaitEvent(c->fb, c->ev_conv[buf], 0));
+    rc = run_fp64(c, X + (size_t)g0 * pR * ldx, ldx, gc, bj, sj, c->flags + buf, c->fb);
     if (rc) return rc;
+    CK(c, cudaEventRecord(c->ev_fb[buf], c->fb));
   }
+  // the block is complete on the compute stream only when its fallback launches are
+  for (int k = 0; k < 2; ++k) CK(c, cudaStreamWaitEvent(c->stream, c->ev_fb[k], 0));
   c->oseq += nchunks;
   return GLS_OK;
 }
@@ -478,9 +536,77 @@ int solve_streamed(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out, 
   return GLS_OK;
 }
 
+int ensure_stage8(gls_ctx* c, int64_t cols) {
+  const int64_t ld8 = (c->n + 15) & ~(int64_t)15;
+  if (c->stage8_cols >= cols && c->ld8 == ld8) return GLS_OK;
+  CK(c, cudaDeviceSynchronize());
+  dfree(c, c->stage8[0]);
+  dfree(c, c->stage8[1]);
+  c->stage8_cols = 0;
+  for (int k = 0; k < 2; ++k) CK(c, dalloc(c, &c->stage8[k], (size_t)ld8 * cols));
+  CK(c, cudaStreamSynchronize(c->own_stream));
+  c->stage8_cols = cols;
+  c->ld8 = ld8;
+  return GLS_OK;
+}
+
+// Genotype codes (int8) from host memory, or from device memory with an unaligned layout:
+// the same double-buffered stream as solve_streamed (Alg. 8), one byte per genotype on the link.
+int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, double* b_out, bool b_dev,
+                      int32_t* status_out, bool s_dev) {
+  const int pR = c->pR, p = c->p;
+  const int64_t n = c->n;
+  int64_t chunk_groups = c->block_cols / pR;
+  if (chunk_groups < 1) chunk_groups = 1;
+  if (chunk_groups > m_blk) chunk_groups = m_blk;
+  int rc = ensure_stage8(c, chunk_groups * pR);
+  if (rc) return rc;
+  if (!b_dev || (status_out && !s_dev)) {
+    // the b / status staging of the double path, sized for these chunks
+    if (c->bstage_groups < chunk_groups) {
+      CK(c, cudaDeviceSynchronize());
+      for (int k = 0; k < 2; ++k) {
+        dfree(c, c->bstage[k]);
+        dfree(c, c->sstage[k]);
+        CK(c, dalloc(c, &c->bstage[k], (size_t)chunk_groups * p * sizeof(double)));
+        CK(c, dalloc(c, &c->sstage[k], (size_t)chunk_groups * sizeof(int32_t)));
+      }
+      CK(c, cudaStreamSynchronize(c->own_stream));
+      c->bstage_groups = chunk_groups;
+    }
+  }
+  for (int64_t g0 = 0; g0 < m_blk; g0 += chunk_groups) {
+    const int64_t gc = (m_blk - g0 < chunk_groups) ? m_blk - g0 : chunk_groups;
+    const int buf = (int)(c->seq++ & 1);
+    CK(c, cudaStreamWaitEvent(c->h2d, c->ev_comp[buf], 0));
+    CK(c, cudaMemcpy2DAsync(c->stage8[buf], c->ld8, G + (size_t)g0 * pR * ldg, ldg, n, gc * pR,
+                            cudaMemcpyDefault, c->h2d));
+    CK(c, cudaEventRecord(c->ev_h2d[buf], c->h2d));
+    CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d[buf], 0));
+    CK(c, cudaStreamWaitEvent(c->stream, c->ev_d2h[buf], 0));
+    double* bdst = b_dev ? b_out + (size_t)g0 * p : c->bstage[buf];
+    int32_t* sdst = status_out ? (s_dev ? status_out + g0 : c->sstage[buf]) : nullptr;
+    rc = run_int8(c, c->stage8[buf], c->ld8, gc, bdst, sdst, nullptr);
+    if (rc) return rc;
+    CK(c, cudaEventRecord(c->ev_comp[buf], c->stream));
+    if (!b_dev || (status_out && !s_dev)) {
+      CK(c, cudaStreamWaitEvent(c->d2h, c->ev_comp[buf], 0));
+      if (!b_dev)
+        CK(c, cudaMemcpyAsync(b_out + (size_t)g0 * p, c->bstage[buf], (size_t)gc * p * sizeof(double),
+                              cudaMemcpyDeviceToHost, c->d2h));
+      if (status_out && !s_dev)
+        CK(c, cudaMemcpyAsync(status_out + g0, c->sstage[buf], (size_t)gc * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, c->d2h));
+      CK(c, cudaEventRecord(c->ev_d2h[buf], c->d2h));
+    }
+  }
+  return GLS_OK;
+}
+
 int sync_all(gls_ctx* c) {
   CK(c, cudaStreamSynchronize(c->h2d));
   CK(c, cudaStreamSynchronize(c->conv));
+  CK(c, cudaStreamSynchronize(c->fb));
   CK(c, cudaStreamSynchronize(c->stream));
   CK(c, cudaStreamSynchronize(c->d2h));
   return GLS_OK;
@@ -601,6 +727,80 @@ int gls_solve_block_ex(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_o
   return GLS_OK;
 }
 
+int gls_solve_block_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, double* b_out,
+                       int32_t* status_out, int async) {
+  if (!c) return GLS_ERR_ARG;
+  if (c->state != ST_OK) return GLS_ERR_STATE;
+  if (!G || !b_out || (async != 0 && async != 1) || ldg < c->n) return GLS_ERR_ARG;
+  if (m_blk < 1) return GLS_ERR_DIM;
+  if (!c->oz_ok) {
+    c->err = "gls_solve_block_i8 needs n <= 131071 (exact int32 digit products)";
+    return GLS_ERR_DIM;
+  }
+  DeviceGuard g(c->device);
+  c->err.clear();
+  const bool x_dev = is_device_ptr(G);
+  const bool b_dev = is_device_ptr(b_out);
+  const bool s_dev = status_out ? is_device_ptr(status_out) : false;
+  int rc;
+  if (x_dev && ldg % 16 == 0 && ((uintptr_t)G & 15) == 0) {
+    double* bdst = b_out;
+    int32_t* sdst = status_out;
+    if (!b_dev || (status_out && !s_dev)) {
+      rc = ensure_scratch(c, m_blk);
+      if (rc) return rc;
+      if (!b_dev) bdst = c->bscratch;
+      if (status_out && !s_dev) sdst = c->sscratch;
+    }
+    // one launch covers at most 2^31 - 1 columns (TMA coordinates are int32)
+    const int64_t max_groups = ((int64_t)1 << 30) / c->pR;
+    for (int64_t g0 = 0; g0 < m_blk; g0 += max_groups) {
+      const int64_t gc = (m_blk - g0 < max_groups) ? m_blk - g0 : max_groups;
+      rc = run_int8(c, G + (size_t)g0 * c->pR * ldg, ldg, gc, bdst + (size_t)g0 * c->p,
+                    sdst ? sdst + g0 : nullptr, nullptr);
+      if (rc) return rc;
+    }
+    if (!b_dev)
+      CK(c, cudaMemcpyAsync(b_out, bdst, (size_t)m_blk * c->p * sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream));
+    if (status_out && !s_dev)
+      CK(c, cudaMemcpyAsync(status_out, sdst, (size_t)m_blk * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                            c->stream));
+  } else {
+    rc = solve_streamed_i8(c, G, ldg, m_blk, b_out, b_dev, status_out, s_dev);
+    if (rc) return rc;
+  }
+  if (!async) return sync_all(c);
+  return GLS_OK;
+}
+
+int gls_set_timing(gls_ctx* c, int32_t enable) {
+  if (!c) return GLS_ERR_ARG;
+  c->timing = enable != 0;
+  return GLS_OK;
+}
+
+int gls_read_timing(gls_ctx* c, double* ms_int8, double* ms_fp64, double* ms_conv, int64_t* launches) {
+  if (!c || !ms_int8 || !ms_fp64 || !ms_conv || !launches) return GLS_ERR_ARG;
+  DeviceGuard g(c->device);
+  int rc = sync_all(c);
+  if (rc) return rc;
+  double t[3] = {0, 0, 0};
+  for (auto& x : c->tl) {
+    float ms = 0.f;
+    CK(c, cudaEventElapsedTime(&ms, x.a, x.b));
+    t[x.kind] += ms;
+    c->ev_pool.push_back(x.a);
+    c->ev_pool.push_back(x.b);
+  }
+  *launches = (int64_t)c->tl.size();
+  c->tl.clear();
+  *ms_int8 = t[0];
+  *ms_fp64 = t[1];
+  *ms_conv = t[2];
+  return GLS_OK;
+}
+
 int gls_solve_block(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out) {
   return gls_solve_block_ex(c, X_R, m_blk, b_out, nullptr, 0);
 }
@@ -643,7 +843,15 @@ void gls_destroy(gls_ctx* c) {
   dfree(c, c->x8[1]);
   dfree(c, c->flags);
   dfree(c, c->ran);
+  dfree(c, c->stage8[0]);
+  dfree(c, c->stage8[1]);
+  for (auto& x : c->tl) {
+    cudaEventDestroy(x.a);
+    cudaEventDestroy(x.b);
+  }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->conv) cudaStreamSynchronize(c->conv);
+  if (c->fb) cudaStreamSynchronize(c->fb);
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
   for (int k = 0; k < 2; ++k) {
     if (c->ev_h2d[k]) cudaEventDestroy(c->ev_h2d[k]);
@@ -651,8 +859,10 @@ void gls_destroy(gls_ctx* c) {
     if (c->ev_d2h[k]) cudaEventDestroy(c->ev_d2h[k]);
     if (c->ev_conv[k]) cudaEventDestroy(c->ev_conv[k]);
     if (c->ev_oz[k]) cudaEventDestroy(c->ev_oz[k]);
+    if (c->ev_fb[k]) cudaEventDestroy(c->ev_fb[k]);
   }
   if (c->conv) cudaStreamDestroy(c->conv);
+  if (c->fb) cudaStreamDestroy(c->fb);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);

@@ -33,6 +33,7 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "gls_internal.cuh"
 #include "umma.cuh"
@@ -47,12 +48,12 @@ constexpr int kKC = kOzKC;               // K per stage (one 128-byte swizzle sp
 constexpr int kNSL = kOzSlices;          // digits per T element
 constexpr int kBN = kNSL * kR;           // MMA N = 224
 constexpr int kATile = 128 * kKC;        // 16 KiB
-constexpr int kBTile = kBN * kKC;        // 28 KiB
-constexpr int kStages = 4;
+constexpr int kBTile = kBN * kKC;        // 28 KiB (whole packed digit tile)
+constexpr int kBHalf = kBTile / 2;       // 14 KiB staged per CTA of a pair
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = (2 + kEpiWarps) * 32;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kIdesc = idesc_i8(128, kBN);
+constexpr uint32_t kIdesc = idesc_i8(256, kBN);  // CTA pair: M = 256
 static_assert(kOzTileBytes == kBTile, "packed T tile size");
 
 struct OzParams {
@@ -61,6 +62,7 @@ struct OzParams {
   const double* G;      // (pL+1)^2 column-major: S_TL = G[0:pL,0:pL], b_T = G[0:pL,pL]
   const int* gate;      // non-zero: X_R is not int8-representable -> this kernel does nothing
   unsigned long long* ran;
+  long long* prof;      // nullable diagnostics: per CTA 8 counters of clock cycles (GLS_OZ_PROF=1)
   double* b_out;
   int32_t* status_out;
   int64_t cols;         // m_blk * pR
@@ -114,159 +116,249 @@ __device__ void posv_store(double* S, double* rhs, int p, double* bo, int32_t* s
   if (st) *st = bad;
 }
 
-// NA: accumulators per column (>= pL + 1 + pR); PR1: pR == 1 (Gram = z^2, no shuffles).
-template <int NA, bool PR1>
-__global__ void __launch_bounds__(kThreads, 1)
-    ozaki_trsm_gls_kernel(const __grid_constant__ CUtensorMap xmap, const OzParams kp) {
+// Static schedule over CTA pairs: pair `pid` of `np` takes tiles 2 (r np + pid) + {0, 1} in round r
+// (rank 0 = pair leader, rank 1 = peer).  A CTA whose tile is past the end still runs the pipeline
+// (X reads as zeros, no output) while its partner has a real tile.
+struct Sched {
+  int pid, np, rank, rounds;
+  __device__ Sched(int num_tiles, int rank_) {
+    rank = rank_;
+    pid = (int)(blockIdx.x >> 1);
+    np = (int)(gridDim.x >> 1);
+    rounds = (num_tiles + 2 * np - 1) / (2 * np);
+  }
+  __device__ int tile(int r) const { return 2 * (r * np + pid) + rank; }
+  __device__ bool pair_active(int r, int num_tiles) const { return 2 * (r * np + pid) < num_tiles; }
+};
+
+__device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t ph, long long* acc) {
+  if (acc) {
+    const long long t0 = clock64();
+    mbar_wait(bar, ph);
+    *acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, ph);
+  }
+}
+
+// K chunk order of row block i: forward on even, reverse on odd row blocks (zig-zag), so each pass
+// over the X panel starts where the previous one ended and re-reads hit L2.  The digit products are
+// exact integers, so the order does not change any bit of the result.
+__device__ __forceinline__ int chunk_at(int i, int nc, int k) { return (i & 1) ? nc - 1 - k : k; }
+
+// One CTA pair (cluster of 2, one CTA per SM of a TPC) computes, per row block of 32 z rows and per
+// 128-row K chunk, D[256 SNP columns x 224] += X^T[256 x 128] T^T[128 x 224] as four
+// tcgen05.mma.cta_group::2.kind::i8 (M = 256, N = 224, K = 32) issued by the leader: each CTA stages
+// its own 128 X columns and half (112 rows) of the packed digit tile, so a stage is 30 KiB per SM and
+// the B operand is shared by the pair.  D lives in TMEM, double-buffered (2 x 224 of 512 columns):
+// CTA r's TMEM lanes hold its own 128 columns.
+// PL1C: pL + 1 when fixed at compile time (0: runtime); NA: accumulators per column
+// (>= pL + 1 + pR); PR1: pR == 1 (Gram = z^2, no shuffles); ST: pipeline stages.
+template <int PL1C, int NA, bool PR1, int ST>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    ozaki_trsm_gls_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap tmap,
+                          const OzParams kp) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
-  uint8_t* sB = sA + kStages * kATile;
-  double* red = (double*)(sB + kStages * kBTile);  // 128 columns x NA
+  uint8_t* sB = sA + ST * kATile;
+  double* red = (double*)(sB + ST * kBHalf);  // 128 columns x NA
   uint64_t* bars = (uint64_t*)(red + 128 * NA);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + kStages;
-  uint64_t* tfull = bars + 2 * kStages;
-  uint64_t* tempty = bars + 2 * kStages + 2;
-  uint32_t* tslot = (uint32_t*)(bars + 2 * kStages + 4);
+  uint64_t* full = bars;                 // used in the leader: all 60 KiB of a stage landed
+  uint64_t* empty = bars + ST;           // both CTAs: the pair's MMAs released the stage
+  uint64_t* tfull = bars + 2 * ST;       // both CTAs: accumulator buffer ready for the epilogue
+  uint64_t* tempty = bars + 2 * ST + 2;  // used in the leader: both epilogues drained the buffer
+  uint32_t* tslot = (uint32_t*)(bars + 2 * ST + 4);
 
   if (kp.gate && *(volatile const int*)kp.gate != 0) return;  // uniform across the grid
   if (kp.ran && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(kp.ran, 1ull);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], kEpiWarps);
+      mbar_init(&tempty[b], 2 * kEpiWarps);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tslot, kTmemCols);
+  if (warp == 1) tmem_alloc_pair(tslot, kTmemCols);
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / complete_tx
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  const int cpt = 4 * kp.cpw;  // columns per tile
+  const int cpt = 4 * kp.cpw;  // columns per tile (per CTA)
+  const Sched sc(kp.num_tiles, (int)rank);
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       prefetch_tmap(&xmap);
+      prefetch_tmap(&tmap);
       int stage = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < kp.num_tiles; tile += gridDim.x) {
-        const int col0 = tile * cpt;
+      long long tw = 0;
+      long long* pw = kp.prof ? &tw : nullptr;
+      const uint32_t full0 = mapa_shared(smem_u32(full), 0);  // leader's full[0]
+      for (int r = 0; r < sc.rounds; ++r) {
+        if (!sc.pair_active(r, kp.num_tiles)) break;
+        const int col0 = sc.tile(r) * cpt;
         for (int i = 0; i < kp.NBR; ++i) {
           const int nc = (i >> 2) + 1;
-          const int8_t* tsrc = kp.T8 + oz_tile_offset(i) * (int64_t)kBTile;
-          for (int c = 0; c < nc; ++c) {
-            mbar_wait(&empty[stage], ph ^ 1);
-            mbar_arrive_expect_tx(&full[stage], kATile + kBTile);
+          const int trow0 = (int)(oz_tile_offset(i) * kBN) + (int)rank * (kBN / 2);
+          for (int k = 0; k < nc; ++k) {
+            const int c = chunk_at(i, nc, k);
+            timed_wait(&empty[stage], ph ^ 1, pw);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kATile + kBHalf));
+            const uint32_t fb = full0 + stage * 8;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              tma_2d_g2s(sA + stage * kATile + q * 4096, &xmap, c * kKC, col0 + q * kp.cpw, &full[stage]);
-            bulk_g2s(sB + stage * kBTile, tsrc + (int64_t)c * kBTile, kBTile, &full[stage]);
-            if (++stage == kStages) {
+              tma_2d_g2s_pair(sA + stage * kATile + q * 4096, &xmap, c * kKC, col0 + q * kp.cpw, fb);
+            tma_2d_g2s_pair(sB + stage * kBHalf, &tmap, 0, trow0 + c * kBN, fb);
+            if (++stage == ST) {
               stage = 0;
               ph ^= 1;
             }
           }
         }
       }
+      if (kp.prof) kp.prof[blockIdx.x * 8 + 0] = tw;
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader && lane == 0) {
       int stage = 0;
       uint32_t ph = 0;
       uint32_t rbc = 0;
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-      for (int tile = blockIdx.x; tile < kp.num_tiles; tile += gridDim.x) {
+      long long twf = 0, twt = 0;
+      long long* pf = kp.prof ? &twf : nullptr;
+      long long* pt = kp.prof ? &twt : nullptr;
+      const long long tstart = clock64();
+      for (int r = 0; r < sc.rounds; ++r) {
+        if (!sc.pair_active(r, kp.num_tiles)) break;
         for (int i = 0; i < kp.NBR; ++i, ++rbc) {
           const int nc = (i >> 2) + 1;
           const uint32_t buf = rbc & 1, tph = (rbc >> 1) & 1;
-          mbar_wait(&tempty[buf], tph ^ 1);
+          timed_wait(&tempty[buf], tph ^ 1, pt);
           tc_fence_after();
           const uint32_t dt = tbase + buf * 256;
-          for (int c = 0; c < nc; ++c) {
-            mbar_wait(&full[stage], ph);
+          for (int k = 0; k < nc; ++k) {
+            timed_wait(&full[stage], ph, pf);
             tc_fence_after();
             const uint64_t ad = sdesc_k128(a0 + stage * kATile);
-            const uint64_t bd = sdesc_k128(b0 + stage * kBTile);
+            const uint64_t bd = sdesc_k128(b0 + stage * kBHalf);
 #pragma unroll
             for (int kk = 0; kk < kKC / 32; ++kk)
-              mma_i8(dt, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), kIdesc, (c | kk) != 0);
-            mma_commit(&empty[stage]);
-            if (++stage == kStages) {
+              mma_i8_pair(dt, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), kIdesc, (k | kk) != 0);
+            mma_commit_pair_mc(&empty[stage], 3);
+            if (++stage == ST) {
               stage = 0;
               ph ^= 1;
             }
           }
-          mma_commit(&tfull[buf]);
+          mma_commit_pair_mc(&tfull[buf], 3);
         }
+      }
+      if (kp.prof) {
+        kp.prof[blockIdx.x * 8 + 1] = twf;
+        kp.prof[blockIdx.x * 8 + 2] = twt;
+        kp.prof[blockIdx.x * 8 + 3] = clock64() - tstart;
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue
+    // ------------------------------------------------------------ epilogue (both CTAs)
     const int ew = warp - 2;
     const int q = warp & 3;      // TMEM lane quadrant this warp may access
     const int h = ew >> 2;       // which 16 of the 32 z rows
-    const int tc = q * 32 + lane;  // column of the tile held by this thread (TMEM lane)
-    const int pl1 = kp.pL + 1;
-    const int as = kp.pL + 2;      // aux row stride
+    const int tc = q * 32 + lane;  // column of the CTA's tile held by this thread (TMEM lane)
+    const int pl1 = PL1C > 0 ? PL1C : kp.pL + 1;
+    const int as = pl1 + 1;        // aux row stride
     const int a_in = PR1 ? 0 : lane % kp.pR;  // position inside the group
     const uint32_t trow = tbase + ((uint32_t)(q * 32) << 16) + h * 16;
+    const uint32_t tempty0 = mapa_shared(smem_u32(tempty), 0);  // leader's tempty[0]
     double acc[NA];
     zero_acc(acc);
     uint32_t rbc = 0;
-    for (int tile = blockIdx.x; tile < kp.num_tiles; tile += gridDim.x) {
+    long long twe = 0, prof_drain = 0, prof_busy = 0;
+    long long* pe = (kp.prof && ew == 0 && lane == 0) ? &twe : nullptr;
+    for (int rr = 0; rr < sc.rounds; ++rr) {
+      if (!sc.pair_active(rr, kp.num_tiles)) break;
+      const int tile = sc.tile(rr);
       for (int i = 0; i < kp.NBR; ++i, ++rbc) {
         const uint32_t buf = rbc & 1, tph = (rbc >> 1) & 1;
-        mbar_wait(&tfull[buf], tph);
+        timed_wait(&tfull[buf], tph, pe);
+        const long long tw0 = pe ? clock64() : 0;
         tc_fence_after();
-        double z[16];
+        // z = sum_s 256^(6-s) D_s: digit sums 0..3 and 4..6 combined exactly in int64 (IMAD.WIDE),
+        // then one rounding each into FP64 -- 2 conversions + 1 FMA per z instead of 7 + 6
+        long long hi[16], lo[16];
         {
           int32_t v[16];
           tmem_ld16(trow + buf * 256, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int r = 0; r < 16; ++r) z[r] = (double)v[r];
-        }
-#pragma unroll 1
-        for (int s = 1; s < kNSL; ++s) {
-          int32_t v[16];
-          tmem_ld16(trow + buf * 256 + s * kR, v);
+          for (int r = 0; r < 16; ++r) hi[r] = (long long)v[r] * 16777216LL;
+          tmem_ld16(trow + buf * 256 + 1 * kR, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int r = 0; r < 16; ++r) z[r] = fma(z[r], 256.0, (double)v[r]);
+          for (int r = 0; r < 16; ++r) hi[r] += (long long)v[r] * 65536LL;
+          tmem_ld16(trow + buf * 256 + 2 * kR, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int r = 0; r < 16; ++r) hi[r] += (long long)v[r] * 256LL;
+          tmem_ld16(trow + buf * 256 + 3 * kR, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int r = 0; r < 16; ++r) hi[r] += (long long)v[r];
+          tmem_ld16(trow + buf * 256 + 4 * kR, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int r = 0; r < 16; ++r) lo[r] = (long long)v[r] * 65536LL;
+          tmem_ld16(trow + buf * 256 + 5 * kR, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int r = 0; r < 16; ++r) lo[r] += (long long)v[r] * 256LL;
+          tmem_ld16(trow + buf * 256 + 6 * kR, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int r = 0; r < 16; ++r) lo[r] += (long long)v[r];
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (lane == 0) {
+          if (leader)
+            mbar_arrive(&tempty[buf]);
+          else
+            mbar_arrive_cluster(tempty0 + buf * 8);
+        }
+        if (pe) prof_drain += clock64() - tw0;
         const double* arow = kp.aux + (int64_t)(i * kR + h * 16) * as;
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
           const double* a = arow + r * as;
-          const double zr = z[r] * __ldg(a);
+          const double z = fma((double)hi[r], 16777216.0, (double)lo[r]);
+          const double zr = z * __ldg(a);
+          // acc[w] += zr * f_w, f = [W~_row (pl1 values) | z of the group's columns (pR values)];
+          // static indices only, so acc stays in registers
 #pragma unroll
-          for (int w = 0; w < NA; ++w)
-            if (w < pl1) acc[w] = fma(zr, __ldg(a + 1 + w), acc[w]);
-          if (PR1) {
-            acc[pl1 < NA ? pl1 : NA - 1] = fma(zr, zr, acc[pl1 < NA ? pl1 : NA - 1]);
-          } else {
-#pragma unroll
-            for (int b = 0; b < NA; ++b) {
-              if (b < kp.pR) {
-                const double zb = __shfl_sync(0xffffffffu, zr, lane - a_in + b);
-                if (pl1 + b < NA) acc[pl1 + b] = fma(zr, zb, acc[pl1 + b]);
-              }
+          for (int w = 0; w < NA; ++w) {
+            if (w < pl1) {
+              acc[w] = fma(zr, __ldg(a + 1 + w), acc[w]);
+            } else if (PR1) {
+              if (w == pl1) acc[w] = fma(zr, zr, acc[w]);
+            } else if (w - pl1 < kp.pR) {
+              acc[w] = fma(zr, __shfl_sync(0xffffffffu, zr, lane - a_in + (w - pl1)), acc[w]);
             }
           }
         }
+        if (pe) prof_busy += clock64() - tw0;
       }
       // ---- per-tile finalisation: sum the two row halves, assemble S_i, posv
       named_bar_sync(1, kEpiWarps * 32);
@@ -290,23 +382,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             rhs[a2] = __ldg(kp.G + a2 + pL * pl1);
           }
           for (int a2 = 0; a2 < pR; ++a2) {
-            const double* rr = red + (tc + a2) * NA;
+            const double* rr2 = red + (tc + a2) * NA;
             for (int k = 0; k < pL; ++k) {
-              S[(pL + a2) + k * 20] = rr[k];
-              S[k + (pL + a2) * 20] = rr[k];
+              S[(pL + a2) + k * 20] = rr2[k];
+              S[k + (pL + a2) * 20] = rr2[k];
             }
-            rhs[pL + a2] = rr[pL];
-            for (int b2 = 0; b2 < pR; ++b2) S[(pL + a2) + (pL + b2) * 20] = rr[pl1 + b2];
+            rhs[pL + a2] = rr2[pL];
+            for (int b2 = 0; b2 < pR; ++b2) S[(pL + a2) + (pL + b2) * 20] = rr2[pl1 + b2];
           }
           posv_store(S, rhs, p, kp.b_out + g * p, kp.status_out ? kp.status_out + g : nullptr);
         }
       }
       zero_acc(acc);
     }
+    if (pe) {
+      kp.prof[blockIdx.x * 8 + 4] = twe;
+      kp.prof[blockIdx.x * 8 + 5] = prof_drain;
+      kp.prof[blockIdx.x * 8 + 6] = prof_busy;
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tbase, kTmemCols);
+  cluster_sync_all();  // neither CTA leaves while its partner may still signal or fill it
+  if (warp == 1) tmem_dealloc_pair(tbase, kTmemCols);
 }
 
 // ---------------------------------------------------------------- setup kernels
@@ -338,7 +436,8 @@ __global__ void oz_rowscale_kernel(const double* __restrict__ T, int64_t ld, int
 }
 
 // Digits of every element of every packed tile: tile (i, c) holds rows 32i..32i+31, K columns
-// 128c..128c+127; B row s*32 + rr holds digit s of row 32i + rr, swizzled (umma::swz128).
+// 128c..128c+127; B row s*32 + rr holds digit s of row 32i + rr (plain 128-byte rows; the TMA load
+// applies the 128-byte swizzle).
 __global__ void oz_pack_kernel(const double* __restrict__ T, int64_t ld, int64_t n,
                                const int* __restrict__ escale, int NBR, int8_t* __restrict__ T8) {
   const int64_t tile = blockIdx.x;
@@ -363,7 +462,7 @@ __global__ void oz_pack_kernel(const double* __restrict__ T, int64_t ld, int64_t
     }
     d[0] = (int8_t)V;  // |top| <= 127 because |V| <= 127 * 2^48
 #pragma unroll
-    for (int s = 0; s < kNSL; ++s) dst[swz128(s * kR + rr, k)] = d[s];
+    for (int s = 0; s < kNSL; ++s) dst[(s * kR + rr) * kKC + k] = d[s];  // TMA applies the swizzle
   }
 }
 
@@ -425,18 +524,31 @@ PFN_encodeTiled get_encode() {
   return fn;
 }
 
-template <int NA, bool PR1>
-cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& map, const OzParams& kp, int num_sms) {
-  constexpr int smem = kStages * (kATile + kBTile) + 128 * NA * 8 + 16 * 8 + 1024;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(ozaki_trsm_gls_kernel<NA, PR1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+template <int PL1C, int NA, bool PR1>
+cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& xmap, const CUtensorMap& tmap,
+                              const OzParams& kp, int num_sms) {
+  constexpr int kFixed = 128 * NA * 8 + 1024 + 512;  // reduction scratch, alignment, barriers
+  constexpr int ST = (232448 - kFixed) / (kATile + kBHalf) < 8 ? (232448 - kFixed) / (kATile + kBHalf) : 8;
+  static_assert(ST >= 4, "shared memory budget");
+  constexpr int smem = ST * (kATile + kBHalf) + kFixed;
+  auto kern = ozaki_trsm_gls_kernel<PL1C, NA, PR1, ST>;
+  static int max_pairs = -1;
+  if (max_pairs < 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    max_pairs = num_sms / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * max_pairs));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, (void*)kern, &cfg) == cudaSuccess && nc > 0 && nc < max_pairs)
+      max_pairs = nc;
+    cudaGetLastError();
   }
-  const int grid = kp.num_tiles < num_sms ? kp.num_tiles : num_sms;
-  ozaki_trsm_gls_kernel<NA, PR1><<<grid, kThreads, smem, s>>>(map, kp);
+  const int need = (kp.num_tiles + 1) / 2;
+  const int np = need < max_pairs ? need : max_pairs;
+  kern<<<2 * np, kThreads, smem, s>>>(xmap, tmap, kp);
   return cudaGetLastError();
 }
 
@@ -499,6 +611,14 @@ cudaError_t launch_ozaki_gls(cudaStream_t s, const OzArgs& a, int num_sms, std::
   kp.G = a.G;
   kp.gate = a.gate;
   kp.ran = a.ran;
+  kp.prof = nullptr;
+  static long long* prof_buf = nullptr;
+  static bool prof_on = getenv("GLS_OZ_PROF") != nullptr;
+  if (prof_on) {
+    if (!prof_buf) cudaMalloc(&prof_buf, 8 * 1024 * sizeof(long long));
+    cudaMemsetAsync(prof_buf, 0, 8 * 1024 * sizeof(long long), s);
+    kp.prof = prof_buf;
+  }
   kp.b_out = a.b_out;
   kp.status_out = a.status_out;
   kp.cols = cols;
@@ -510,15 +630,48 @@ cudaError_t launch_ozaki_gls(cudaStream_t s, const OzArgs& a, int num_sms, std::
   kp.pR = a.pR;
   kp.p = a.pL + a.pR;
   kp.cpw = cpw;
+  // packed digit tiles as a 2D byte tensor [tiles * 224 rows][128]: TMA boxes of 112 rows (half a
+  // tile, one per CTA of the pair) with the 128-byte swizzle the smem descriptors expect
+  CUtensorMap tmap;
+  const int64_t trows = oz_total_tiles(kp.NBR) * kBN;
+  cuuint64_t tdim[2] = {(cuuint64_t)kKC, (cuuint64_t)trows};
+  cuuint64_t tstride[1] = {(cuuint64_t)kKC};
+  cuuint32_t tbox[2] = {(cuuint32_t)kKC, (cuuint32_t)(kBN / 2)};
+  r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)a.T8, tdim, tstride, tbox, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    if (msg) *msg = "cuTensorMapEncodeTiled (packed T digits) failed";
+    return cudaErrorInvalidValue;
+  }
   cudaError_t e;
-  if (a.pR == 1 && a.pL + 2 <= 8)
-    e = launch_oz_variant<8, true>(s, map, kp, num_sms);
+  if (a.pR == 1 && a.pL == 3)  // the configurations' covariate set: intercept, covariate, sex
+    e = launch_oz_variant<4, 5, true>(s, map, tmap, kp, num_sms);
+  else if (a.pR == 1 && a.pL + 2 <= 8)
+    e = launch_oz_variant<0, 8, true>(s, map, tmap, kp, num_sms);
   else if (a.pR == 1)
-    e = launch_oz_variant<21, true>(s, map, kp, num_sms);
+    e = launch_oz_variant<0, 21, true>(s, map, tmap, kp, num_sms);
   else
-    e = launch_oz_variant<21, false>(s, map, kp, num_sms);
+    e = launch_oz_variant<0, 21, false>(s, map, tmap, kp, num_sms);
   if (lc) ++*lc;
   if (e != cudaSuccess && msg) *msg = std::string("ozaki_trsm_gls launch: ") + cudaGetErrorString(e);
+  if (prof_on && e == cudaSuccess) {
+    long long h[8 * 1024];
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h, prof_buf, sizeof h, cudaMemcpyDeviceToHost);
+    double sum[7] = {0, 0, 0, 0, 0, 0, 0};
+    int nb = 0;
+    for (int b = 0; b < 1024; b += 2)
+      if (h[b * 8 + 3] > 0) {
+        ++nb;
+        for (int k = 0; k < 7; ++k) sum[k] += (double)h[b * 8 + k];
+      }
+    if (nb)
+      fprintf(stderr, "[oz prof] ctas %d  total %.3e cyc  mma wait full %.1f%%  wait tmem-empty %.1f%%  "
+              "producer wait empty %.1f%%  epilogue wait tmem-full %.1f%%  drain %.1f%%  busy %.1f%%\n", nb,
+              sum[3] / nb, 100 * sum[1] / sum[3], 100 * sum[2] / sum[3], 100 * sum[0] / sum[3],
+              100 * sum[4] / sum[3], 100 * sum[5] / sum[3], 100 * sum[6] / sum[3]);
+  }
   return e;
 }
 

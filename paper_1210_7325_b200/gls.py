@@ -28,7 +28,8 @@ ABI_SYMBOLS = (
     "gls_create", "gls_solve_block", "gls_solve_block_ex", "gls_sync", "gls_set_stream",
     "gls_set_block_cols", "gls_destroy", "gls_failed_pivot", "gls_last_error",
     "gls_error_string", "gls_create_adopt", "gls_shared_view", "gls_commit_shared",
-    "gls_kernel_launches", "gls_set_path", "gls_path_counts",
+    "gls_kernel_launches", "gls_set_path", "gls_path_counts", "gls_solve_block_i8",
+    "gls_set_timing", "gls_read_timing",
 )
 
 
@@ -86,6 +87,13 @@ def load(build_if_missing: bool = True):
     L.gls_set_path.restype = ctypes.c_int
     L.gls_path_counts.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.gls_path_counts.restype = ctypes.c_int
+    L.gls_solve_block_i8.argtypes = [vp, dp, i64, i64, dp, dp, ctypes.c_int]
+    L.gls_solve_block_i8.restype = ctypes.c_int
+    L.gls_set_timing.argtypes = [vp, i32]
+    L.gls_set_timing.restype = ctypes.c_int
+    dpp = ctypes.POINTER(ctypes.c_double)
+    L.gls_read_timing.argtypes = [vp, dpp, dpp, dpp, ctypes.POINTER(i64)]
+    L.gls_read_timing.restype = ctypes.c_int
     _lib = L
     return L
 
@@ -153,6 +161,22 @@ class Context:
     def solve_block(self, X_R, m_blk: int, b_out, status_out=None, async_: bool = False):
         self._check(self._lib.gls_solve_block_ex(self._h, _ptr(X_R), m_blk, _ptr(b_out),
                                                  _ptr(status_out, "int32"), 1 if async_ else 0))
+
+    def solve_block_i8(self, G, m_blk: int, b_out, status_out=None, async_: bool = False, ldg: int | None = None):
+        """X_R as int8 genotype codes: G of shape (m_blk*pR, ldg) (row j = column j of X_R)."""
+        ld = ldg if ldg is not None else int(G.shape[-1])
+        self._check(self._lib.gls_solve_block_i8(self._h, _ptr(G, "int8"), ld, m_blk, _ptr(b_out),
+                                                 _ptr(status_out, "int32"), 1 if async_ else 0))
+
+    def set_timing(self, enable: bool = True):
+        self._check(self._lib.gls_set_timing(self._h, 1 if enable else 0))
+
+    def read_timing(self):
+        """{'int8_ms', 'fp64_ms', 'conv_ms', 'launches'} summed since the last read (synchronises)."""
+        a, b, c, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        self._check(self._lib.gls_read_timing(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                                              ctypes.byref(k)))
+        return {"int8_ms": a.value, "fp64_ms": b.value, "conv_ms": c.value, "launches": k.value}
 
     def sync(self):
         self._check(self._lib.gls_sync(self._h))

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "gls.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(gls_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(gls_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
@@ -65,3 +65,14 @@ def test_null_handles(lib):
     assert lib.gls_last_error(None) == b""
     lib.gls_destroy(None)
     assert lib.gls_create(10, 1, 1, None, None, None, None) == 1
+
+
+def test_null_handles_extensions(lib):
+    i64 = ctypes.c_int64
+    a, b = i64(), i64()
+    assert lib.gls_set_path(None, 0) == 1
+    assert lib.gls_path_counts(None, ctypes.byref(a), ctypes.byref(b)) == 1
+    assert lib.gls_solve_block_i8(None, None, 10, 1, None, None, 0) == 1
+    assert lib.gls_set_timing(None, 1) == 1
+    d = ctypes.c_double()
+    assert lib.gls_read_timing(None, ctypes.byref(d), ctypes.byref(d), ctypes.byref(d), ctypes.byref(a)) == 1

@@ -383,3 +383,57 @@ def test_repeated_create_destroy_is_deterministic(glsmod):
         outs.append(b)
     np.testing.assert_array_equal(outs[0], outs[1])
     np.testing.assert_array_equal(outs[0], outs[2])
+
+
+def test_int8_genotype_entry_matches_double_entry(glsmod):
+    """gls_solve_block_i8 (genotype codes) gives the same bits as gls_solve_block on the same
+    values: device in place (ldg % 16 == 0), device with an odd leading dimension (staged),
+    pinned and pageable host sources, host outputs; ragged n (not a multiple of 16 or 32)."""
+    n, pL, pR, m = 1001, 3, 2, 333
+    P = gen.make_problem(n, pL, pR, seed=23)
+    XR = gen.make_XR(23, n, 0, m * pR)
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, pR)
+    G = XR.astype(np.int8)
+    with glsmod.Context(n, pL, pR, dev(P.M), dev(P.XL), dev(P.y)) as ctx:
+        ref = torch.empty((m, pL + pR), dtype=torch.float64, device="cuda")
+        ctx.solve_block(dev(XR), m, ref)
+        ref = ref.cpu().numpy()
+        assert_parity(ref, np.zeros(m, np.int32), b_or, st_or, label="i8 ref")
+        for ldg in (1008, 1001, 1013):
+            Gp = np.zeros((m * pR, ldg), dtype=np.int8)
+            Gp[:, :n] = G
+            Gd = torch.from_numpy(Gp).cuda()
+            b = torch.empty((m, pL + pR), dtype=torch.float64, device="cuda")
+            st = torch.empty(m, dtype=torch.int32, device="cuda")
+            ctx.solve_block_i8(Gd, m, b, st, ldg=ldg)
+            np.testing.assert_array_equal(b.cpu().numpy(), ref)
+            assert int(st.sum()) == 0
+            bh = np.empty((m, pL + pR))
+            ctx.set_block_cols(2 * 64)
+            ctx.solve_block_i8(torch.from_numpy(Gp).pin_memory(), m, bh, ldg=ldg)
+            np.testing.assert_array_equal(bh, ref)
+            bh2 = np.empty((m, pL + pR))
+            ctx.solve_block_i8(Gp, m, bh2, ldg=ldg)
+            np.testing.assert_array_equal(bh2, ref)
+        with pytest.raises(glsmod.GLSError) as e:
+            ctx.solve_block_i8(torch.from_numpy(G).cuda(), m, torch.empty((m, 5), dtype=torch.float64,
+                                                                           device="cuda"), ldg=n - 1)
+        assert e.value.code == 1
+
+
+def test_timing_hooks_and_counts(glsmod):
+    n, m = 512, 4000
+    P = gen.make_problem(n, 3, 1, seed=24)
+    Xd = dev(gen.make_XR(24, n, 0, m))
+    with glsmod.Context(n, 3, 1, dev(P.M), dev(P.XL), dev(P.y)) as ctx:
+        ctx.set_timing(True)
+        b = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+        ctx.solve_block(Xd, m, b)
+        t = ctx.read_timing()
+        assert t["launches"] == 3 and t["int8_ms"] > 0 and t["conv_ms"] > 0, t
+        assert ctx.path_counts() == (1, 0)
+        ctx.set_path(glsmod.GLS_PATH_FP64)
+        ctx.solve_block(Xd, m, b)
+        t = ctx.read_timing()
+        assert t["launches"] == 1 and t["fp64_ms"] > 0 and t["int8_ms"] == 0, t
+        assert ctx.path_counts() == (1, 1)
