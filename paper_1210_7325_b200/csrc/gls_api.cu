@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -438,15 +439,21 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
   if (c->path == GLS_PATH_FP64 || !c->oz_ok) return run_fp64(c, X, ldx, groups, b, stt, nullptr);
   const int pR = c->pR, p = c->p;
   const int64_t cpt = 4 * (int64_t)((32 / pR) * pR);
-  int64_t chunk_groups = (int64_t)c->num_sms * cpt * 8 / pR;
+  // chunk j covers groups [bnd[j], bnd[j+1]) and holds min(j+1, 8) waves of tiles: only the first
+  // (short) conversion is exposed, and each later one -- slowed by the running int8 kernel, with
+  // which it shares HBM -- still finishes before the previous chunk's kernel does
+  const int64_t wave_groups = (int64_t)c->num_sms * cpt / pR;
+  int64_t chunk_groups = 8 * wave_groups;
   if (chunk_groups > groups) chunk_groups = groups;
   int rc = ensure_x8(c, chunk_groups * pR);
   if (rc) return rc;
-  const int64_t nchunks = (groups + chunk_groups - 1) / chunk_groups;
+  std::vector<int64_t> bnd{0};
+  for (int64_t j = 1; bnd.back() < groups; ++j)
+    bnd.push_back(std::min(groups, bnd.back() + std::min<int64_t>(j, 8) * wave_groups));
+  const int64_t nchunks = (int64_t)bnd.size() - 1;
   auto issue_conv = [&](int64_t j) -> int {
     const int buf = (int)((c->oseq + j) & 1);
-    const int64_t g0 = j * chunk_groups;
-    const int64_t gc = (groups - g0 < chunk_groups) ? groups - g0 : chunk_groups;
+    const int64_t g0 = bnd[j], gc = bnd[j + 1] - bnd[j];
     // ev_oz[buf] is recorded on the compute stream before the kernels of chunk j-1, i.e. after those
     // of chunk j-2 (the previous users of x8[buf] and flags[buf]) and after whatever produced X.
     CK(c, cudaEventRecord(c->ev_oz[buf], c->stream));
@@ -464,8 +471,7 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
   if (rc) return rc;
   for (int64_t j = 0; j < nchunks; ++j) {
     const int buf = (int)((c->oseq + j) & 1);
-    const int64_t g0 = j * chunk_groups;
-    const int64_t gc = (groups - g0 < chunk_groups) ? groups - g0 : chunk_groups;
+    const int64_t g0 = bnd[j], gc = bnd[j + 1] - bnd[j];
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_conv[buf], 0));
     if (j + 1 < nchunks) {
       rc = issue_conv(j + 1);

@@ -125,7 +125,7 @@ def test_non_integer_block_falls_back_to_fp64(glsmod):
 
 
 def test_mixed_chunks_pick_paths_independently(glsmod):
-    """A device block spanning two int8 conversion chunks (8 waves of 128-column tiles each):
+    """A device block spanning two int8 conversion chunks (one wave of tiles, then up to 8 waves):
     the integer chunk runs on int8, the chunk holding a dosage runs on FP64; all rows match."""
     n, pL, pR = 64, 2, 1
     chunk = 148 * 128 * 8
