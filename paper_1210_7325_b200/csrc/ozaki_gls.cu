@@ -477,46 +477,64 @@ __global__ void oz_aux_w_kernel(const double* __restrict__ W, int64_t ldw, int64
   }
 }
 
+// x -> int8 bits for an integer-valued double in [-128, 127], by integer operations on its bits only
+// (FP64 arithmetic contends with the tensor core on this part); bad |= any other value.
+__device__ __forceinline__ uint32_t to_i8_bits(double v, int& bad) {
+  const long long b = __double_as_longlong(v);
+  const long long a = b & 0x7fffffffffffffffLL;
+  const int e = (int)(a >> 52);  // biased exponent
+  uint32_t mag = 0;
+  if (a != 0) {
+    if (e >= 1023 && e <= 1030) {
+      const int sh = 52 - (e - 1023);  // 45 .. 52
+      const long long mant = (a & 0xfffffffffffffLL) | (1LL << 52);
+      bad |= (mant & ((1LL << sh) - 1)) != 0;  // a fractional part
+      mag = (uint32_t)(mant >> sh);           // 1 .. 255
+      bad |= mag > (b < 0 ? 128u : 127u);
+    } else {
+      bad = 1;  // 0 < |v| < 1, |v| >= 256, inf, NaN
+    }
+  }
+  return (b < 0 ? (0u - mag) : mag) & 0xffu;
+}
+
 // X (double, column-major, ld = ldx) -> X8 (int8, column-major, ld = ld8), flagging any value that
-// is not an integer in [-128, 127] (NaN included).  One thread per 16 rows of one column: eight
-// 16-byte loads in flight per thread (the pass runs beside the hot kernel on the SMs' leftover
-// thread slots, so memory-level parallelism per thread is what sets its speed).  X rows start
-// 16-byte aligned (ldx even, base 16-byte aligned).
-__global__ void __launch_bounds__(256) oz_x_to_i8_kernel(const double* __restrict__ X, int64_t ldx, int64_t n,
-                                                         int64_t cols, int8_t* __restrict__ X8, int64_t ld8,
-                                                         int* __restrict__ flag) {
-  const int64_t per_col = (n + 15) >> 4;
+// is not an integer in [-128, 127] (NaN included).  One thread per 8 rows of one column (a warp
+// reads 2 KiB contiguous).  Small blocks and few registers on purpose: the pass runs beside the
+// int8 kernel, which leaves only a few thousand registers free per SM sub-partition, and it uses no
+// FP64 arithmetic, which would contend with that kernel's tensor-core work.  X rows start 16-byte
+// aligned (ldx even, base 16-byte aligned).
+__global__ void __launch_bounds__(64) oz_x_to_i8_kernel(const double* __restrict__ X, int64_t ldx, int64_t n,
+                                                        int64_t cols, int8_t* __restrict__ X8, int64_t ld8,
+                                                        int* __restrict__ flag) {
+  const int64_t per_col = (n + 7) >> 3;
   const int64_t total = per_col * cols;
   int bad = 0;
   for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
        o += (int64_t)gridDim.x * blockDim.x) {
     const int64_t col = o / per_col;
-    const int64_t r0 = (o - col * per_col) << 4;
+    const int64_t r0 = (o - col * per_col) << 3;
     const double* src = X + col * ldx + r0;
-    double v[16];
-    if (r0 + 16 <= n) {
+    uint32_t w0 = 0, w1 = 0;
+    if (r0 + 8 <= n) {
+      double2 v[4];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double2 t = __ldcs((const double2*)src + k);
-        v[2 * k] = t.x;
-        v[2 * k + 1] = t.y;
-      }
+      for (int k = 0; k < 4; ++k) v[k] = __ldcs((const double2*)src + k);
+      w0 = to_i8_bits(v[0].x, bad) | to_i8_bits(v[0].y, bad) << 8 | to_i8_bits(v[1].x, bad) << 16 |
+           to_i8_bits(v[1].y, bad) << 24;
+      w1 = to_i8_bits(v[2].x, bad) | to_i8_bits(v[2].y, bad) << 8 | to_i8_bits(v[3].x, bad) << 16 |
+           to_i8_bits(v[3].y, bad) << 24;
     } else {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = (r0 + k < n) ? __ldcs(src + k) : 0.0;
-    }
-    uint32_t w[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const double t = rint(v[k]);
-      bad |= !(t == v[k] && fabs(v[k]) <= 127.0);
-      w[k >> 2] |= (uint32_t)(uint8_t)(int8_t)(int)t << (8 * (k & 3));
+      for (int k = 0; r0 + k < n; ++k) {
+        const uint32_t t = to_i8_bits(__ldcs(src + k), bad) << (8 * (k & 3));
+        if (k < 4) w0 |= t; else w1 |= t;
+      }
     }
     int8_t* dst = X8 + col * ld8 + r0;
-    if (r0 + 16 <= ld8) {
-      *(uint4*)dst = make_uint4(w[0], w[1], w[2], w[3]);
+    if (r0 + 8 <= ld8) {
+      *(uint2*)dst = make_uint2(w0, w1);
     } else {
-      for (int k = 0; r0 + k < ld8; ++k) dst[k] = (int8_t)(w[k >> 2] >> (8 * (k & 3)));
+      for (int k = 0; r0 + k < ld8; ++k) dst[k] = (int8_t)((k < 4 ? w0 : w1) >> (8 * (k & 3)));
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
@@ -586,11 +604,11 @@ void oz_setup(cudaStream_t s, const double* T, int64_t ld, int64_t n, const doub
 
 void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t cols, int8_t* X8,
                 int64_t ld8, int* flag, int num_sms, int64_t* lc) {
-  const int64_t total = ((n + 15) >> 4) * cols;
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+  const int64_t total = ((n + 7) >> 3) * cols;
+  int64_t blocks = (total + 63) / 64;
+  if (blocks > (int64_t)num_sms * 32) blocks = (int64_t)num_sms * 32;
   if (blocks < 1) blocks = 1;
-  oz_x_to_i8_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, ldx, n, cols, X8, ld8, flag);
+  oz_x_to_i8_kernel<<<(unsigned)blocks, 64, 0, s>>>(X, ldx, n, cols, X8, ld8, flag);
   if (lc) ++*lc;
 }
 

@@ -254,3 +254,12 @@ __device__ __forceinline__ void mma_commit_pair_mc(uint64_t* bar, uint16_t mask)
 }
 }  // namespace umma
 }  // namespace gls
+
+namespace gls {
+namespace umma {
+// Orders this thread's generic-proxy global writes before later async-proxy (TMA) accesses.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+}  // namespace umma
+}  // namespace gls
