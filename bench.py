@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--codes", action="store_true",
+                    help="config 4: stream X_R as int8 genotype codes (gls_solve_block_i8) instead of FP64")
     ap.add_argument("--seed", type=int, default=gen.DEFAULT_SEED)
     return ap.parse_args()
 
@@ -425,24 +427,25 @@ def run_ooc(args, cfg, world, rank, local):
     Md = torch.from_numpy(P.M).cuda()
     XLd = torch.from_numpy(np.ascontiguousarray(P.XL)).cuda()
     yd = torch.from_numpy(P.y).cuda()
-    probe = pkg.Context(n, pL, pR, Md, XLd, yd)
     props = torch.cuda.get_device_properties(local)
-    blk_groups = (props.multi_processor_count * 64) // pR     # one wave of panels per chunk
-    probe.close()
+    # chunk = the library's default host block: 4 waves of 128-column int8 tiles
+    blk_groups = (props.multi_processor_count * 16 * (32 // pR) * pR) // pR
     try:
         avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
     except (ValueError, OSError):
         avail = 1 << 40
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
-    blk_bytes = blk_groups * pR * n * 8
+    esz = 1 if args.codes else 8
+    blk_bytes = blk_groups * pR * n * esz
     nblk = (m + blk_groups - 1) // blk_groups
     pool_n = int(max(2, min(nblk, 0.5 * avail / local_world // blk_bytes)))
     g0 = multi.weak_range(m, rank)[0]
-    pool = torch.empty((pool_n, blk_groups * pR, n), dtype=torch.float64, pin_memory=True)
+    pool = torch.empty((pool_n, blk_groups * pR, n), dtype=torch.int8 if args.codes else torch.float64,
+                       pin_memory=True)
     tmp = torch.empty((blk_groups * pR, n), dtype=torch.float64, device="cuda")
     for k in range(pool_n):
         pkg.gen_xr_device(args.seed, n, (g0 + k * blk_groups) * pR, blk_groups * pR, tmp)
-        pool[k].copy_(tmp)
+        pool[k].copy_(tmp.to(torch.int8) if args.codes else tmp)
     del tmp
     b = torch.empty((m, p), dtype=torch.float64, pin_memory=True)
     st = torch.empty(m, dtype=torch.int32, pin_memory=True)
@@ -456,7 +459,10 @@ def run_ooc(args, cfg, world, rank, local):
         for j in range(nblk):
             lo = j * blk_groups
             cnt = min(blk_groups, m - lo)
-            ctx.solve_block(pool[j % pool_n], cnt, b[lo:lo + cnt], st[lo:lo + cnt], async_=True)
+            if args.codes:
+                ctx.solve_block_i8(pool[j % pool_n], cnt, b[lo:lo + cnt], st[lo:lo + cnt], async_=True)
+            else:
+                ctx.solve_block(pool[j % pool_n], cnt, b[lo:lo + cnt], st[lo:lo + cnt], async_=True)
         ctx.sync()
         launches = ctx.kernel_launches
         ctx.close()
@@ -477,25 +483,31 @@ def run_ooc(args, cfg, world, rank, local):
     dt = multi.max_over_ranks([(time.perf_counter() - t0) / args.steps], dist, device="cuda")[0]
     clk = clocks.stop()
     value = world * m / dt
-    t_comp = float(n) * n * m * pR / (FP64_DMMA_PEAK_SUSTAINED * 1e12)
-    t_h2d = 8.0 * n * m * pR / (H2D_GBS * 1e9)
+    # int8 path (genotypes): 7 n^2 int8 ops per column at the int8 peak; H2D: esz bytes per genotype
+    peak8, _, psrc = int8_peak()
+    t_comp = OZ_SLICES * float(n) * n * m * pR / (peak8 * 1e12)
+    t_h2d = float(esz) * n * m * pR / (H2D_GBS * 1e9)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * dt, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": "config4: n=%d pL=%d pR=%d, %d SNPs per GPU streamed from pinned "
-                                       "host memory in %d-SNP chunks (out-of-core, Alg. 8)"
-                                       % (n, pL, pR, m, blk_groups),
+                                       "host memory in %d-SNP chunks (out-of-core, Alg. 8), X_R as %s"
+                                       % (n, pL, pR, m, blk_groups,
+                                          "int8 genotype codes" if args.codes else "FP64"),
                            "n": n, "m_per_rank": m, "chunk_snps": blk_groups,
                            "host_pool_blocks": pool_n, "snp_to_block": "chunk j -> pool block j mod %d" % pool_n,
                            "l2": "inputs larger than L2"},
                 "roofline": {"bound": "tensor" if t_comp >= t_h2d else "h2d",
-                             "achieved": float(n) * n * m * pR / dt / 1e12, "peak": FP64_DMMA_PEAK_SUSTAINED,
-                             "unit": "TFLOP/s", "frac": max(t_comp, t_h2d) / dt, "traffic": None,
+                             "achieved": (OZ_SLICES * float(n) * n * m * pR / dt / 1e12) if t_comp >= t_h2d
+                             else float(esz) * n * m * pR / dt / 1e9,
+                             "peak": peak8 if t_comp >= t_h2d else H2D_GBS,
+                             "unit": "TOP/s (int8)" if t_comp >= t_h2d else "GB/s (H2D)",
+                             "frac": max(t_comp, t_h2d) / dt, "traffic": None,
                              "t_compute_roofline_s": t_comp, "t_h2d_roofline_s": t_h2d,
-                             "h2d_gbs_measured": H2D_GBS},
+                             "h2d_gbs_measured": H2D_GBS, "int8_peak_source": psrc},
                 "cpu_baseline": None,
-                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(8 * n * m * pR + 8 * n * n),
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(esz * n * m * pR + 8 * n * n),
                         "d2h_bytes_per_step": int(m * p * 8 + m * 4),
                         "path": "C ABI, host X_R -> double-buffered H2D (the whole step is end to end)"},
                 "gpu_launches": launches, "clocks": clk}
