@@ -44,6 +44,10 @@ struct gls_ctx {
   size_t T8_bytes = 0;
   double* aux = nullptr;
   size_t aux_bytes = 0;
+  int8_t* V8 = nullptr;      // digits of V = M^{-1} [X_L | y]
+  size_t V8_bytes = 0;
+  double* vscale = nullptr;  // their column scales
+  size_t vscale_bytes = 0;
   int path = GLS_PATH_AUTO;
   bool oz_ok = false;  // n small enough for exact int32 digit products
   // int8 conversion workspaces (two, swapping roles) and their rejection flags
@@ -200,6 +204,10 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
     c->aux_bytes = (size_t)NBR * kOzR * (pL + 2) * sizeof(double);
     CK(c, dalloc(c, &c->T8, c->T8_bytes));
     CK(c, dalloc(c, &c->aux, c->aux_bytes));
+    c->V8_bytes = (size_t)oz_nchunks(n) * oz_nv(pL + 1) * kOzKC;
+    c->vscale_bytes = (size_t)(pL + 1) * sizeof(double);
+    CK(c, dalloc(c, &c->V8, c->V8_bytes));
+    CK(c, dalloc(c, &c->vscale, c->vscale_bytes));
   }
   CK(c, cudaStreamSynchronize(c->own_stream));  // buffers are used from other streams too
   return GLS_OK;
@@ -288,7 +296,11 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   mark("W,G");
   pack_T(s, T, n, n, c->NB, c->Tpk, &c->launches);
   pack_W(s, W, n, n, pL + 1, c->NB, c->NW, c->Wpk, &c->launches);
-  if (c->oz_ok) oz_setup(s, T, n, n, W, pL + 1, c->T8, c->aux, esc, &c->launches);
+  if (c->oz_ok) {
+    // V = T^T W = M^{-1} [X_L | y] into B (free again: W = T B is formed)
+    dgemm(s, n, pL + 1, n, 1.0, T, n, 'T', W, n, 'N', 0.0, B, n, 0, &c->launches);
+    oz_setup(s, T, n, n, W, pL + 1, c->T8, c->aux, esc, B, c->V8, c->vscale, &c->launches);
+  }
   CKS(cudaGetLastError());
   CKS(cudaStreamSynchronize(s));
   mark("pack");
@@ -418,6 +430,8 @@ int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* 
   a.G = c->G;
   a.gate = gate;
   a.ran = c->ran;
+  a.V8 = c->V8;
+  a.vscale = c->vscale;
   a.b_out = b;
   a.status_out = stt;
   std::string msg;
@@ -681,7 +695,11 @@ int gls_shared_view(gls_ctx* c, void** ptrs, int64_t* bytes, int32_t* count) {
     bytes[3] = (int64_t)c->T8_bytes;
     ptrs[4] = c->aux;
     bytes[4] = (int64_t)c->aux_bytes;
-    *count = 5;
+    ptrs[5] = c->V8;
+    bytes[5] = (int64_t)c->V8_bytes;
+    ptrs[6] = c->vscale;
+    bytes[6] = (int64_t)c->vscale_bytes;
+    *count = 7;
   }
   return GLS_OK;
 }
@@ -845,6 +863,8 @@ void gls_destroy(gls_ctx* c) {
   dfree(c, c->G);
   dfree(c, c->T8);
   dfree(c, c->aux);
+  dfree(c, c->V8);
+  dfree(c, c->vscale);
   dfree(c, c->x8[0]);
   dfree(c, c->x8[1]);
   dfree(c, c->flags);

@@ -108,10 +108,16 @@ __host__ __device__ inline int64_t oz_tile_offset(int64_t i) {
   return (q + 1) * (2 * q + r);
 }
 int64_t oz_total_tiles(int64_t NBR);
+inline int64_t oz_nchunks(int64_t n) { return (n + kOzKC - 1) / kOzKC; }
+// N of the V block (digits of V = M^{-1} [X_L | y], 8 rows per column): multiple of 32
+inline int oz_nv(int pl1) { return ((8 * pl1 + 31) / 32) * 32; }
 // T (n x n lower, column-major) and W = [X~_L | y~] (n x pl1) -> digit tiles T8 and the per-row
 // aux table [sigma_r, W~_r,0 .. W~_r,pL] (stride pl1 + 1, ceil(n/32)*32 rows).  escale: int[rows].
+// V = T^T W = M^{-1} [X_L | y] (n x pl1, column-major) -> column scales vscale[pl1] and digit tiles
+// V8 (oz_nchunks(n) x oz_nv(pl1) x 128 bytes): S_BL and b_B of a column x are x^T V (§5.4).
 void oz_setup(cudaStream_t s, const double* T, int64_t ld, int64_t n, const double* W, int pl1,
-              int8_t* T8, double* aux, int* escale, int64_t* launch_counter);
+              int8_t* T8, double* aux, int* escale, const double* V, int8_t* V8, double* vscale,
+              int64_t* launch_counter);
 // X (double) -> X8 (int8, ld8 % 16 == 0); *flag |= 1 if some value is not an integer in [-128,127].
 void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t cols, int8_t* X8,
                 int64_t ld8, int* flag, int num_sms, int64_t* launch_counter);
@@ -126,6 +132,8 @@ struct OzArgs {
   const double* G;
   const int* gate;      // nullable; the kernel does nothing when *gate != 0
   unsigned long long* ran;  // nullable; block 0 adds 1 when the kernel does its work
+  const int8_t* V8;     // digit tiles of V (oz_setup)
+  const double* vscale;
   double* b_out;
   int32_t* status_out;
 };

@@ -71,6 +71,9 @@ struct OzParams {
   int NBR;              // row blocks of 32
   int pL, pR, p;
   int cpw;              // columns per warp quadrant = floor(32 / pR) * pR
+  int NC;               // K chunks of 128 rows = ceil(n / 128)
+  int NV;               // N of the V block: 8 (pL+1) rounded up to a multiple of 32
+  const double* vscale; // pL+1 column scales 2^-(e_w+48) of V = M^{-1} [X_L | y]
 };
 
 template <int NA>
@@ -157,7 +160,7 @@ __device__ __forceinline__ int chunk_at(int i, int nc, int k) { return (i & 1) ?
 template <int PL1C, int NA, bool PR1, int ST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ozaki_trsm_gls_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap tmap,
-                          const OzParams kp) {
+                          const __grid_constant__ CUtensorMap vmap, const OzParams kp) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -227,6 +230,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
         }
+        // V block: all K chunks against the digits of V = M^{-1} [X_L | y] (-> S_BL, b_B)
+        for (int k = 0; k < kp.NC; ++k) {
+          const int c = chunk_at(kp.NBR, kp.NC, k);
+          timed_wait(&empty[stage], ph ^ 1, pw);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kATile + kp.NV * (kKC / 2)));
+          const uint32_t fb = full0 + stage * 8;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            tma_2d_g2s_pair(sA + stage * kATile + q * 4096, &xmap, c * kKC, col0 + q * kp.cpw, fb);
+          tma_2d_g2s_pair(sB + stage * kBHalf, &vmap, 0, c * kp.NV + (int)rank * (kp.NV / 2), fb);
+          if (++stage == ST) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
       }
       if (kp.prof) kp.prof[blockIdx.x * 8 + 0] = tw;
     }
@@ -257,6 +275,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < kKC / 32; ++kk)
               mma_i8_pair(dt, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), kIdesc, (k | kk) != 0);
+            mma_commit_pair_mc(&empty[stage], 3);
+            if (++stage == ST) {
+              stage = 0;
+              ph ^= 1;
+            }
+          }
+          mma_commit_pair_mc(&tfull[buf], 3);
+        }
+        {  // V block: N = NV
+          const uint32_t buf = rbc & 1, tph = (rbc >> 1) & 1;
+          ++rbc;
+          timed_wait(&tempty[buf], tph ^ 1, pt);
+          tc_fence_after();
+          const uint32_t dt = tbase + buf * 256;
+          const uint32_t idv = idesc_i8(256, kp.NV);
+          for (int k = 0; k < kp.NC; ++k) {
+            timed_wait(&full[stage], ph, pf);
+            tc_fence_after();
+            const uint64_t ad = sdesc_k128(a0 + stage * kATile);
+            const uint64_t bd = sdesc_k128(b0 + stage * kBHalf);
+#pragma unroll
+            for (int kk = 0; kk < kKC / 32; ++kk)
+              mma_i8_pair(dt, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idv, (k | kk) != 0);
             mma_commit_pair_mc(&empty[stage], 3);
             if (++stage == ST) {
               stage = 0;
@@ -345,12 +386,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const double* a = arow + r * as;
           const double z = fma((double)hi[r], 16777216.0, (double)lo[r]);
           const double zr = z * __ldg(a);
-          // acc[w] += zr * f_w, f = [W~_row (pl1 values) | z of the group's columns (pR values)];
-          // static indices only, so acc stays in registers
+          // Gram only: acc[pl1 + b] += zr * z_b over the group's columns (S_BR); S_BL and b_B come
+          // from the V block.  Static indices only, so acc stays in registers.
 #pragma unroll
           for (int w = 0; w < NA; ++w) {
             if (w < pl1) {
-              acc[w] = fma(zr, __ldg(a + 1 + w), acc[w]);
             } else if (PR1) {
               if (w == pl1) acc[w] = fma(zr, zr, acc[w]);
             } else if (w - pl1 < kp.pR) {
@@ -359,6 +399,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         if (pe) prof_busy += clock64() - tw0;
+      }
+      {  // V block: S_BL[w] (w < pL) and b_B (w = pL) of this column = 2^-(e_w+48) sum_s 256^(6-s) D[8w+s]
+        const uint32_t buf = rbc & 1, tph = (rbc >> 1) & 1;
+        ++rbc;
+        timed_wait(&tfull[buf], tph, pe);
+        tc_fence_after();
+        if (h == 0) {
+          const uint32_t tv = tbase + ((uint32_t)(q * 32) << 16) + buf * 256;
+#pragma unroll
+          for (int w = 0; w < NA; ++w) {
+            if (w < pl1) {
+              int32_t v[8];
+              tmem_ld8(tv + 8 * w, v);
+              tmem_wait_ld();
+              const long long vh = (long long)v[0] * 16777216LL + (long long)v[1] * 65536LL +
+                                   (long long)v[2] * 256LL + (long long)v[3];
+              const long long vl = (long long)v[4] * 65536LL + (long long)v[5] * 256LL + (long long)v[6];
+              acc[w] = fma((double)vh, 16777216.0, (double)vl) * __ldg(kp.vscale + w);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader)
+            mbar_arrive(&tempty[buf]);
+          else
+            mbar_arrive_cluster(tempty0 + buf * 8);
+        }
       }
       // ---- per-tile finalisation: sum the two row halves, assemble S_i, posv
       named_bar_sync(1, kEpiWarps * 32);
@@ -466,6 +535,60 @@ __global__ void oz_pack_kernel(const double* __restrict__ T, int64_t ld, int64_t
   }
 }
 
+// Column scales of V = M^{-1} [X_L | y] (n x pl1): e_w with max_r |V_rw| 2^e_w <= 127.  One CTA per column.
+__global__ void oz_vscale_kernel(const double* __restrict__ V, int64_t n, int* __restrict__ ev,
+                                 double* __restrict__ vscale) {
+  __shared__ double sm[256];
+  const int w = blockIdx.x;
+  double mx = 0.0;
+  for (int64_t r = threadIdx.x; r < n; r += blockDim.x) mx = fmax(mx, fabs(V[r + w * n]));
+  sm[threadIdx.x] = mx;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + k]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    mx = sm[0];
+    int e = 0;
+    double sig = 0.0;
+    if (mx > 0.0) {
+      int E;
+      const double f = frexp(mx, &E);
+      e = (f * 128.0 <= 127.0) ? 7 - E : 6 - E;
+      sig = ldexp(1.0, -(e + 48));
+    }
+    ev[w] = e;
+    vscale[w] = sig;
+  }
+}
+
+// Digit tiles of V: chunk c holds NV rows of 128 bytes (K = rows 128c..128c+127 of V); row 8w + s is
+// digit s (most significant first) of column w; rows 8w + 7 and w >= pl1 are zero.  Plain layout:
+// the TMA load applies the 128-byte swizzle.
+__global__ void oz_vpack_kernel(const double* __restrict__ V, int64_t n, int pl1, const int* __restrict__ ev,
+                                int NV, int8_t* __restrict__ V8) {
+  const int c = blockIdx.x;
+  int8_t* dst = V8 + (int64_t)c * NV * kKC;
+  for (int idx = threadIdx.x; idx < (NV / 8) * kKC; idx += blockDim.x) {
+    const int w = idx / kKC, k = idx % kKC;
+    const int64_t r = (int64_t)c * kKC + k;
+    long long X = 0;
+    if (w < pl1 && r < n) X = llrint(ldexp(V[r + w * n], ev[w] + 48));
+    int8_t d[8];
+    d[7] = 0;
+#pragma unroll
+    for (int s2 = kNSL - 1; s2 > 0; --s2) {
+      const int8_t lo = (int8_t)(X & 0xff);
+      d[s2] = lo;
+      X = (X - lo) >> 8;
+    }
+    d[0] = (int8_t)X;
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) dst[(8 * w + s2) * kKC + k] = d[s2];
+  }
+}
+
 __global__ void oz_aux_w_kernel(const double* __restrict__ W, int64_t ldw, int64_t n, int pl1,
                                 int64_t rows, double* __restrict__ aux) {
   const int as = pl1 + 1;
@@ -559,7 +682,7 @@ PFN_encodeTiled get_encode() {
 
 template <int PL1C, int NA, bool PR1>
 cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& xmap, const CUtensorMap& tmap,
-                              const OzParams& kp, int num_sms) {
+                              const CUtensorMap& vmap, const OzParams& kp, int num_sms) {
   constexpr int kFixed = 128 * NA * 8 + 1024 + 512;  // reduction scratch, alignment, barriers
   constexpr int ST = (232448 - kFixed) / (kATile + kBHalf) < 8 ? (232448 - kFixed) / (kATile + kBHalf) : 8;
   static_assert(ST >= 4, "shared memory budget");
@@ -581,7 +704,7 @@ cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& xmap, const CUt
   }
   const int need = (kp.num_tiles + 1) / 2;
   const int np = need < max_pairs ? need : max_pairs;
-  kern<<<2 * np, kThreads, smem, s>>>(xmap, tmap, kp);
+  kern<<<2 * np, kThreads, smem, s>>>(xmap, tmap, vmap, kp);
   return cudaGetLastError();
 }
 
@@ -590,7 +713,8 @@ cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& xmap, const CUt
 int64_t oz_total_tiles(int64_t NBR) { return oz_tile_offset(NBR); }
 
 void oz_setup(cudaStream_t s, const double* T, int64_t ld, int64_t n, const double* W, int pl1,
-              int8_t* T8, double* aux, int* escale, int64_t* lc) {
+              int8_t* T8, double* aux, int* escale, const double* V, int8_t* V8, double* vscale,
+              int64_t* lc) {
   const int NBR = (int)((n + kR - 1) / kR);
   const int as = pl1 + 1;
   oz_rowscale_kernel<<<NBR, 256, 0, s>>>(T, ld, n, escale, aux, as);
@@ -599,7 +723,10 @@ void oz_setup(cudaStream_t s, const double* T, int64_t ld, int64_t n, const doub
   const int64_t tot = rows * pl1;
   oz_aux_w_kernel<<<(unsigned)((tot + 255) / 256 < 2048 ? (tot + 255) / 256 : 2048), 256, 0, s>>>(
       W, n, n, pl1, rows, aux);
-  if (lc) *lc += 3;
+  // V digits (the row-exponent scratch is free again once oz_pack_kernel has run: same stream)
+  oz_vscale_kernel<<<pl1, 256, 0, s>>>(V, n, escale, vscale);
+  oz_vpack_kernel<<<(unsigned)oz_nchunks(n), 256, 0, s>>>(V, n, pl1, escale, oz_nv(pl1), V8);
+  if (lc) *lc += 5;
 }
 
 void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t cols, int8_t* X8,
@@ -677,15 +804,29 @@ cudaError_t launch_ozaki_gls(cudaStream_t s, const OzArgs& a, int num_sms, std::
     if (msg) *msg = "cuTensorMapEncodeTiled (packed T digits) failed";
     return cudaErrorInvalidValue;
   }
+  // digits of V = M^{-1} [X_L | y]: [NC * NV rows][128], boxes of NV/2 rows (one per CTA of a pair)
+  kp.NC = (int)oz_nchunks(a.n);
+  kp.NV = oz_nv(a.pL + 1);
+  kp.vscale = a.vscale;
+  CUtensorMap vmap;
+  cuuint64_t vdim[2] = {(cuuint64_t)kKC, (cuuint64_t)kp.NC * kp.NV};
+  cuuint32_t vbox[2] = {(cuuint32_t)kKC, (cuuint32_t)(kp.NV / 2)};
+  r = enc(&vmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)a.V8, vdim, tstride, vbox, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    if (msg) *msg = "cuTensorMapEncodeTiled (packed V digits) failed";
+    return cudaErrorInvalidValue;
+  }
   cudaError_t e;
   if (a.pR == 1 && a.pL == 3)  // the configurations' covariate set: intercept, covariate, sex
-    e = launch_oz_variant<4, 5, true>(s, map, tmap, kp, num_sms);
+    e = launch_oz_variant<4, 5, true>(s, map, tmap, vmap, kp, num_sms);
   else if (a.pR == 1 && a.pL + 2 <= 8)
-    e = launch_oz_variant<0, 8, true>(s, map, tmap, kp, num_sms);
+    e = launch_oz_variant<0, 8, true>(s, map, tmap, vmap, kp, num_sms);
   else if (a.pR == 1)
-    e = launch_oz_variant<0, 21, true>(s, map, tmap, kp, num_sms);
+    e = launch_oz_variant<0, 21, true>(s, map, tmap, vmap, kp, num_sms);
   else
-    e = launch_oz_variant<0, 21, false>(s, map, tmap, kp, num_sms);
+    e = launch_oz_variant<0, 21, false>(s, map, tmap, vmap, kp, num_sms);
   if (lc) ++*lc;
   if (e != cudaSuccess && msg) *msg = std::string("ozaki_trsm_gls launch: ") + cudaGetErrorString(e);
   if (prof_on && e == cudaSuccess) {
