@@ -73,6 +73,8 @@ struct OzParams {
   int cpw;              // columns per warp quadrant = floor(32 / pR) * pR
   int NC;               // K chunks of 128 rows = ceil(n / 128)
   int NV;               // N of the V block: 8 (pL+1) rounded up to a multiple of 32
+  int cpin;             // X chunks c < cpin are loaded L2::evict_last (they are re-read by every row
+                        // block of the tile), the others evict_first
   const double* vscale; // pL+1 column scales 2^-(e_w+48) of V = M^{-1} [X_L | y]
 };
 
@@ -209,6 +211,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       long long tw = 0;
       long long* pw = kp.prof ? &tw : nullptr;
       const uint32_t full0 = mapa_shared(smem_u32(full), 0);  // leader's full[0]
+      const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
       for (int r = 0; r < sc.rounds; ++r) {
         if (!sc.pair_active(r, kp.num_tiles)) break;
         const int col0 = sc.tile(r) * cpt;
@@ -220,9 +223,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             timed_wait(&empty[stage], ph ^ 1, pw);
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kATile + kBHalf));
             const uint32_t fb = full0 + stage * 8;
+            const uint64_t pol = c < kp.cpin ? pol_keep : pol_stream;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              tma_2d_g2s_pair(sA + stage * kATile + q * 4096, &xmap, c * kKC, col0 + q * kp.cpw, fb);
+              tma_2d_g2s_pair_hint(sA + stage * kATile + q * 4096, &xmap, c * kKC, col0 + q * kp.cpw, fb, pol);
             tma_2d_g2s_pair(sB + stage * kBHalf, &tmap, 0, trow0 + c * kBN, fb);
             if (++stage == ST) {
               stage = 0;
@@ -806,6 +810,13 @@ cudaError_t launch_ozaki_gls(cudaStream_t s, const OzArgs& a, int num_sms, std::
   }
   // digits of V = M^{-1} [X_L | y]: [NC * NV rows][128], boxes of NV/2 rows (one per CTA of a pair)
   kp.NC = (int)oz_nchunks(a.n);
+  // pin about 85 MB of X panels in L2 (of 126 MB): cpin chunks x 16 KiB x (CTAs in flight)
+  static int pin_mb = -1;
+  if (pin_mb < 0) {
+    pin_mb = 85;
+    if (const char* e = getenv("GLS_OZ_PIN_MB")) pin_mb = atoi(e);
+  }
+  kp.cpin = (int)((int64_t)pin_mb * 1000000 / ((int64_t)kATile * num_sms));
   kp.NV = oz_nv(a.pL + 1);
   kp.vscale = a.vscale;
   CUtensorMap vmap;
