@@ -130,6 +130,8 @@ struct RecCtx {
   std::vector<cudaEvent_t>* events;
   CholStatus* st;
   int64_t* lc;
+  double* ws_main;  // split-K workspaces, one per stream
+  double* ws_aux;
 };
 
 cudaEvent_t new_event(RecCtx& rc) {
@@ -162,20 +164,20 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
   double* T22 = T + h1 + h1 * ld;
   chol_inv_rec(rc, h1, A11, T11, ld, goff);
   // L21 = A21 T11^T  -> stored in T21's (still unused) place
-  dgemm(s, h2, h1, h1, 1.0, A21, ld, 'N', T11, ld, 'T', 0.0, T21, ld, GEMM_KMAX_COL, rc.lc);
+  dgemm(s, h2, h1, h1, 1.0, A21, ld, 'N', T11, ld, 'T', 0.0, T21, ld, GEMM_KMAX_COL, rc.lc, rc.ws_main);
   // A22 -= L21 L21^T (lower)
-  dgemm(s, h2, h2, h1, -1.0, T21, ld, 'N', T21, ld, 'T', 1.0, A22, ld, GEMM_LOWER_C, rc.lc);
+  dgemm(s, h2, h2, h1, -1.0, T21, ld, 'N', T21, ld, 'T', 1.0, A22, ld, GEMM_LOWER_C, rc.lc, rc.ws_main);
   // Y = L21 T11 -> A21's place, on the aux stream: it only needs L21 and T11, so it overlaps the
   // (latency-bound) recursion on A22, which touches A22 and T22 only.
   cudaEvent_t e1 = new_event(rc), e2 = new_event(rc);
   cudaEventRecord(e1, s);
   cudaStreamWaitEvent(rc.aux, e1, 0);
-  dgemm(rc.aux, h2, h1, h1, 1.0, T21, ld, 'N', T11, ld, 'N', 0.0, A21, ld, GEMM_KMIN_COL, rc.lc);
+  dgemm(rc.aux, h2, h1, h1, 1.0, T21, ld, 'N', T11, ld, 'N', 0.0, A21, ld, GEMM_KMIN_COL, rc.lc, rc.ws_aux);
   cudaEventRecord(e2, rc.aux);
   chol_inv_rec(rc, h2, A22, T22, ld, goff + h1);
   // T21 = -T22 Y  (overwrites L21: Y must be complete)
   cudaStreamWaitEvent(s, e2, 0);
-  dgemm(s, h2, h1, h2, -1.0, T22, ld, 'N', A21, ld, 'N', 0.0, T21, ld, GEMM_KMAX_ROW, rc.lc);
+  dgemm(s, h2, h1, h2, -1.0, T22, ld, 'N', A21, ld, 'N', 0.0, T21, ld, GEMM_KMAX_ROW, rc.lc, rc.ws_main);
 }
 
 }  // namespace
@@ -191,7 +193,12 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
   cudaStream_t aux;
   cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
   std::vector<cudaEvent_t> events;
-  RecCtx rc{s, aux, &events, st, lc};
+  double* ws = nullptr;  // split-K workspaces (main, aux) from the stream-ordered pool
+  if (cudaMallocAsync((void**)&ws, 2 * kSplitKWsDoubles * sizeof(double), s) != cudaSuccess) {
+    cudaGetLastError();
+    ws = nullptr;
+  }
+  RecCtx rc{s, aux, &events, st, lc, ws, ws ? ws + kSplitKWsDoubles : nullptr};
   chol_inv_rec(rc, n, A, T, ld, 0);
   // join: everything issued on aux is ordered before later work on s
   cudaEvent_t done;
@@ -199,6 +206,7 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
   cudaEventRecord(done, aux);
   cudaStreamWaitEvent(s, done, 0);
   cudaEventDestroy(done);
+  if (ws) cudaFreeAsync(ws, s);  // after the join: the aux stream's last use precedes it
   for (cudaEvent_t e : events) cudaEventDestroy(e);
   cudaStreamDestroy(aux);
 }

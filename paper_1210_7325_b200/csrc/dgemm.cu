@@ -41,7 +41,13 @@ struct GemmParams {
   int64_t ldc;
   double alpha, beta;
   int flags;
+  int nsplit;   // split-K: blockIdx.z takes K tiles [z*nk/nsplit, (z+1)*nk/nsplit) ...
+  double* ws;   // ... and writes its raw partial tile to ws[z][m + n*M] (reduced by dgemm_splitk_reduce)
 };
+
+__device__ __forceinline__ bool tile_skipped(const GemmParams& p, int64_t r0, int64_t c0) {
+  return (p.flags & GEMM_LOWER_C) && c0 >= r0 + BM;
+}
 
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(THREADS, 2) dgemm_kernel(GemmParams p) {
@@ -49,14 +55,20 @@ __global__ void __launch_bounds__(THREADS, 2) dgemm_kernel(GemmParams p) {
   double* As = sm;
   double* Bs = sm + STAGES * A_TILE;
   const int64_t r0 = (int64_t)blockIdx.x * BM, c0 = (int64_t)blockIdx.y * BN;
-  if ((p.flags & GEMM_LOWER_C) && c0 >= r0 + BM) return;
+  if (tile_skipped(p, r0, c0)) return;
   int64_t kb = 0, ke = p.K;
   if (p.flags & GEMM_KMIN_COL) kb = (c0 / BK) * BK;
   if (p.flags & GEMM_KMAX_ROW) ke = min(ke, r0 + BM);
   if (p.flags & GEMM_KMAX_COL) ke = min(ke, c0 + BN);
   const int64_t kbeg = kb;  // element-level lower bound for the zero fill
   kb = (kb / BK) * BK;
-  const int nk = (ke > kb) ? (int)((ke - kb + BK - 1) / BK) : 0;
+  int nk = (ke > kb) ? (int)((ke - kb + BK - 1) / BK) : 0;
+  if (p.nsplit > 1) {  // this split's share of the K tiles
+    const int z = blockIdx.z;
+    const int t0 = (int)((int64_t)z * nk / p.nsplit), t1 = (int)((int64_t)(z + 1) * nk / p.nsplit);
+    kb += (int64_t)t0 * BK;
+    nk = t1 - t0;
+  }
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 3, wn = warp >> 2;
@@ -131,12 +143,31 @@ __global__ void __launch_bounds__(THREADS, 2) dgemm_kernel(GemmParams p) {
         const int64_t gm = r0 + wm * 32 + t * 8 + l4;
         const int64_t gn = c0 + wn * 32 + s * 8 + 2 * kk + e;
         if (gm < p.M && gn < p.N) {
-          double* cp = p.C + gm + gn * p.ldc;
-          double v = p.alpha * acc[t][s][e];
-          if (p.beta != 0.0) v += p.beta * *cp;
-          *cp = v;
+          if (p.nsplit > 1) {
+            p.ws[(int64_t)blockIdx.z * p.M * p.N + gm + gn * p.M] = acc[t][s][e];
+          } else {
+            double* cp = p.C + gm + gn * p.ldc;
+            double v = p.alpha * acc[t][s][e];
+            if (p.beta != 0.0) v += p.beta * *cp;
+            *cp = v;
+          }
         }
       }
+}
+
+// C = alpha * sum_z ws[z] + beta * C, splits summed in a fixed order (deterministic).
+__global__ void dgemm_splitk_reduce(GemmParams p) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < p.M * p.N;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gm = o % p.M, gn = o / p.M;
+    if (tile_skipped(p, (gm / BM) * BM, (gn / BN) * BN)) continue;
+    double v = 0.0;
+    for (int z = 0; z < p.nsplit; ++z) v += p.ws[(int64_t)z * p.M * p.N + o];
+    double* cp = p.C + gm + gn * p.ldc;
+    v *= p.alpha;
+    if (p.beta != 0.0) v += p.beta * *cp;
+    *cp = v;
+  }
 }
 
 template <bool TA, bool TB>
@@ -153,16 +184,36 @@ void launch(cudaStream_t s, dim3 grid, const GemmParams& p) {
 
 void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, char opA, const double* B, int64_t ldb, char opB, double beta, double* C,
-           int64_t ldc, int flags, int64_t* launch_counter) {
+           int64_t ldc, int flags, int64_t* launch_counter, double* ws) {
   if (M <= 0 || N <= 0) return;
-  GemmParams p{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, flags};
+  GemmParams p{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, flags, 1, nullptr};
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
+  // small output, long K: split K so the launch fills the machine (the recursion's deep levels)
+  const int64_t tiles = (int64_t)grid.x * grid.y;
+  const int64_t ktiles = (K + BK - 1) / BK;
+  if (tiles < 74 && ktiles >= 8) {
+    int sp = (int)((148 + tiles - 1) / tiles);
+    if (sp > ktiles / 4) sp = (int)(ktiles / 4);
+    if (sp > 16) sp = 16;
+    if (sp > 1 && ws && (size_t)sp * M * N <= kSplitKWsDoubles) {
+      p.nsplit = sp;
+      p.ws = ws;
+      grid.z = sp;
+    }
+  }
   const bool ta = (opA == 'T'), tb = (opB == 'T');
   if (!ta && !tb) launch<false, false>(s, grid, p);
   else if (!ta && tb) launch<false, true>(s, grid, p);
   else if (ta && !tb) launch<true, false>(s, grid, p);
   else launch<true, true>(s, grid, p);
   if (launch_counter) ++*launch_counter;
+  if (p.nsplit > 1) {
+    const int64_t tot = M * N;
+    int64_t blocks = (tot + 255) / 256;
+    if (blocks > 1024) blocks = 1024;
+    dgemm_splitk_reduce<<<(unsigned)blocks, 256, 0, s>>>(p);
+    if (launch_counter) ++*launch_counter;
+  }
 }
 
 }  // namespace gls

@@ -53,9 +53,12 @@ enum GemmFlags : int {
   GEMM_LOWER_C = 8,    // only tiles intersecting the lower triangle of C
 };
 // C[M x N] = alpha * op(A) * op(B) + beta * C, column-major.  op = 'N' or 'T'.
+// ws (nullable, device, kSplitKWsDoubles doubles, private to the stream s): when given, GEMMs with
+// few output tiles and a long K are split over K (partial tiles in ws, then a fixed-order reduction).
+constexpr size_t kSplitKWsDoubles = (size_t)2 << 20;  // 16 MiB: (148 + 74) tiles x 128 x 64 doubles
 void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, char opA, const double* B, int64_t ldb, char opB, double beta, double* C,
-           int64_t ldc, int flags, int64_t* launch_counter);
+           int64_t ldc, int flags, int64_t* launch_counter, double* ws = nullptr);
 
 // ---------------------------------------------------------------- setup: Cholesky + inverse
 // In place: on return T (n x n, lower, ld) holds L^{-1} of M = L L^T; A (M on entry) is destroyed.

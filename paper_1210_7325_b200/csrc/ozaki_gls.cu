@@ -519,23 +519,31 @@ __global__ void oz_pack_kernel(const double* __restrict__ T, int64_t ld, int64_t
   while (i + 1 <= NBR && oz_tile_offset(i + 1) <= tile) ++i;
   const int c = (int)(tile - oz_tile_offset(i));
   int8_t* dst = T8 + tile * (int64_t)kOzTileBytes;
-  const int rr = threadIdx.x & 31;
-  const int64_t r = (int64_t)i * kR + rr;
-  const int e = (r < n) ? escale[r] : 0;
-  for (int k = threadIdx.x >> 5; k < kKC; k += blockDim.x >> 5) {
-    const int64_t j = (int64_t)c * kKC + k;
-    long long V = 0;
-    if (r < n && j <= r) V = llrint(ldexp(T[r + j * ld], e + 48));
-    int8_t d[kNSL];
+  // thread = (row rr of the block, 16 consecutive K): reads T column-major (a warp covers 32 rows of
+  // one column: coalesced), writes one 16-byte vector per digit
+  for (int u = threadIdx.x; u < kR * (kKC / 16); u += blockDim.x) {
+    const int rr = u & 31, kq = u >> 5;
+    const int64_t r = (int64_t)i * kR + rr;
+    const int e = (r < n) ? escale[r] : 0;
+    uint32_t d[kNSL][4];
 #pragma unroll
-    for (int s = kNSL - 1; s > 0; --s) {  // signed base-256 digits, least significant first
-      const int8_t lo = (int8_t)(V & 0xff);
-      d[s] = lo;
-      V = (V - lo) >> 8;
+    for (int s = 0; s < kNSL; ++s) d[s][0] = d[s][1] = d[s][2] = d[s][3] = 0;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const int64_t j = (int64_t)c * kKC + kq * 16 + kk;
+      long long V = 0;
+      if (r < n && j <= r) V = llrint(ldexp(T[r + j * ld], e + 48));
+#pragma unroll
+      for (int s = kNSL - 1; s > 0; --s) {  // signed base-256 digits, least significant first
+        const int8_t lo = (int8_t)(V & 0xff);
+        d[s][kk >> 2] |= (uint32_t)(uint8_t)lo << (8 * (kk & 3));
+        V = (V - lo) >> 8;
+      }
+      d[0][kk >> 2] |= (uint32_t)(uint8_t)(int8_t)V << (8 * (kk & 3));  // |top| <= 127
     }
-    d[0] = (int8_t)V;  // |top| <= 127 because |V| <= 127 * 2^48
 #pragma unroll
-    for (int s = 0; s < kNSL; ++s) dst[(s * kR + rr) * kKC + k] = d[s];  // TMA applies the swizzle
+    for (int s = 0; s < kNSL; ++s)
+      *(uint4*)(dst + (s * kR + rr) * kKC + kq * 16) = make_uint4(d[s][0], d[s][1], d[s][2], d[s][3]);
   }
 }
 
