@@ -146,6 +146,47 @@ int gls_solve_block_i8(gls_ctx* ctx, const int8_t* G, int64_t ldg, int64_t m_blk
 int gls_set_timing(gls_ctx* ctx, int32_t enable);
 int gls_read_timing(gls_ctx* ctx, double* ms_int8, double* ms_fp64, double* ms_conv, int64_t* launches);
 
+/* gls_get_dims -- n, pL, pR of a context (any state but NULL). */
+int gls_get_dims(const gls_ctx* ctx, int64_t* n, int32_t* pL, int32_t* pR);
+
+/* ---- Out-of-core from secondary storage (§4; NEXT-1 / NEXT-4 of SURVEY §8(f)).
+ * gls_solve_file streams the X_R of m problems from a file, in blocks of problems, and writes the b
+ * records (m x p doubles, record i at byte 8 p i) and optionally the int32 statuses to files.
+ *   xr_path, xr_offset : X_R as stored: m*pR columns of n elements, column-major from byte xr_offset;
+ *                        elem_bytes 8 = FP64 (gls_solve_block_ex), 1 = int8 genotype codes
+ *                        (gls_solve_block_i8)
+ *   block_groups       : problems per block (the paper's block size)
+ *   warmup_groups      : 0, or a smaller first block (§4.3: "initiate the computation with a small
+ *                        block size ... and increase it after a few iterations")
+ *   mode               : GLS_OOC_SYNC  -- Alg. 7, blocking read / solve / blocking write per block;
+ *                        GLS_OOC_ASYNC -- Alg. 8, two pinned host workspaces (fig:workspaces), a reader
+ *                        thread prefetching the next block and a writer thread storing the previous b,
+ *                        at most one read and one write in flight.
+ *   rep (nullable)     : wall, compute, read-wait and write-wait seconds measured at the algorithms' wait
+ *                        points (Alg. 8 lines 8 and 16; Alg. 7 lines 7 and 14), the first block's load,
+ *                        blocks and bytes moved.
+ * Results are bitwise identical between the two modes and to gls_solve_block on the same values (same
+ * kernels, block-partition independent).  Synchronous: returns when every b is on the file.
+ * Errors: GLS_ERR_ARG (bad argument, unreadable/short X_R file, failed write), GLS_ERR_DIM, GLS_ERR_OOM
+ * (pinned workspaces), and any error of the solve calls. */
+enum { GLS_OOC_SYNC = 0, GLS_OOC_ASYNC = 1 };
+typedef struct {
+  double wall_s, compute_s, read_wait_s, write_wait_s, first_load_s;
+  int64_t blocks, bytes_read, bytes_written;
+} gls_ooc_report;
+int gls_solve_file(gls_ctx* ctx, const char* xr_path, int64_t xr_offset, int32_t elem_bytes, int64_t m,
+                   const char* b_path, const char* status_path, int64_t block_groups, int64_t warmup_groups,
+                   int32_t mode, gls_ooc_report* rep);
+
+/* gls_select_block_size -- §4.3's block-size condition: the largest block (problems)
+ * whose two workspaces (X_R + b + status, elem_bytes per X_R element) fit in mem_limit_bytes, and
+ * *io_bound = 0 if at that size time(compute) >= 1.1 (time(load) + time(store)) with the given
+ * rates (compute in problems/s, I/O in bytes/s, io_latency_s per request), else *io_bound = 1.
+ * Returns -1 on bad arguments or when not even one problem fits. Pure host arithmetic. */
+int64_t gls_select_block_size(int64_t n, int32_t p, int32_t pR, int32_t elem_bytes, int64_t mem_limit_bytes,
+                              double compute_groups_per_s, double io_bytes_per_s, double io_latency_s,
+                              int32_t* io_bound);
+
 #ifdef __cplusplus
 }
 #endif

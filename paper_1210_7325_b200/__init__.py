@@ -3,4 +3,5 @@
 `gls` is the ctypes binding of libgls.so (C ABI in include/gls.h); `build` compiles the
 in-tree CUDA libraries for sm_100a.  See DESIGN.md.
 """
-from .gls import GLS_PATH_AUTO, GLS_PATH_FP64, Context, GLSError, gen_xr_device, load  # noqa: F401
+from .gls import (GLS_OOC_ASYNC, GLS_OOC_SYNC, GLS_PATH_AUTO, GLS_PATH_FP64, Context, GLSError,  # noqa: F401
+                  gen_xr_device, load, select_block_size)

@@ -916,6 +916,14 @@ int gls_path_counts(gls_ctx* c, int64_t* int8_launches, int64_t* fp64_launches) 
   return GLS_OK;
 }
 
+int gls_get_dims(const gls_ctx* c, int64_t* n, int32_t* pL, int32_t* pR) {
+  if (!c || !n || !pL || !pR) return GLS_ERR_ARG;
+  *n = c->n;
+  *pL = c->pL;
+  *pR = c->pR;
+  return GLS_OK;
+}
+
 int64_t gls_failed_pivot(const gls_ctx* c) { return c ? c->failed_pivot : -1; }
 
 const char* gls_last_error(const gls_ctx* c) { return c ? c->err.c_str() : ""; }

@@ -23,13 +23,25 @@ GLS_ERR_OOM = 5
 GLS_ERR_STATE = 6
 GLS_PATH_AUTO = 0
 GLS_PATH_FP64 = 1
+GLS_OOC_SYNC = 0
+GLS_OOC_ASYNC = 1
+
+
+class OocReport(ctypes.Structure):
+    """gls_ooc_report: wait times at the wait points of Alg. 7 / Alg. 8."""
+    _fields_ = [("wall_s", ctypes.c_double), ("compute_s", ctypes.c_double), ("read_wait_s", ctypes.c_double),
+                ("write_wait_s", ctypes.c_double), ("first_load_s", ctypes.c_double),
+                ("blocks", ctypes.c_int64), ("bytes_read", ctypes.c_int64), ("bytes_written", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 ABI_SYMBOLS = (
     "gls_create", "gls_solve_block", "gls_solve_block_ex", "gls_sync", "gls_set_stream",
     "gls_set_block_cols", "gls_destroy", "gls_failed_pivot", "gls_last_error",
     "gls_error_string", "gls_create_adopt", "gls_shared_view", "gls_commit_shared",
     "gls_kernel_launches", "gls_set_path", "gls_path_counts", "gls_solve_block_i8",
-    "gls_set_timing", "gls_read_timing",
+    "gls_set_timing", "gls_read_timing", "gls_get_dims", "gls_solve_file", "gls_select_block_size",
 )
 
 
@@ -94,6 +106,14 @@ def load(build_if_missing: bool = True):
     dpp = ctypes.POINTER(ctypes.c_double)
     L.gls_read_timing.argtypes = [vp, dpp, dpp, dpp, ctypes.POINTER(i64)]
     L.gls_read_timing.restype = ctypes.c_int
+    L.gls_get_dims.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    L.gls_get_dims.restype = ctypes.c_int
+    cp = ctypes.c_char_p
+    L.gls_solve_file.argtypes = [vp, cp, i64, i32, i64, cp, cp, i64, i64, i32, ctypes.POINTER(OocReport)]
+    L.gls_solve_file.restype = ctypes.c_int
+    L.gls_select_block_size.argtypes = [i64, i32, i32, i32, i64, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_double, ctypes.POINTER(i32)]
+    L.gls_select_block_size.restype = i64
     _lib = L
     return L
 
@@ -124,6 +144,15 @@ def _ptr(a, dtype: str = "float64"):
     import numpy as np
     assert isinstance(a, np.ndarray) and a.flags.c_contiguous and a.dtype == np.dtype(dtype)
     return a.ctypes.data
+
+
+def select_block_size(n: int, p: int, pR: int, elem_bytes: int, mem_limit_bytes: int,
+                      compute_groups_per_s: float, io_bytes_per_s: float, io_latency_s: float = 0.0):
+    """gls_select_block_size (§4.3): (block problems, io_bound)."""
+    flag = ctypes.c_int32()
+    k = load().gls_select_block_size(n, p, pR, elem_bytes, mem_limit_bytes, compute_groups_per_s,
+                                     io_bytes_per_s, io_latency_s, ctypes.byref(flag))
+    return int(k), bool(flag.value)
 
 
 def error_string(code: int) -> str:
@@ -167,6 +196,18 @@ class Context:
         ld = ldg if ldg is not None else int(G.shape[-1])
         self._check(self._lib.gls_solve_block_i8(self._h, _ptr(G, "int8"), ld, m_blk, _ptr(b_out),
                                                  _ptr(status_out, "int32"), 1 if async_ else 0))
+
+    def solve_file(self, xr_path: str, m: int, b_path: str, status_path: str | None = None, elem_bytes: int = 8,
+                   xr_offset: int = 0, block_groups: int = 65536, warmup_groups: int = 0,
+                   mode: int = GLS_OOC_ASYNC) -> dict:
+        """Out-of-core solve from a file (gls_solve_file; Alg. 7 when mode=GLS_OOC_SYNC, Alg. 8 when
+        GLS_OOC_ASYNC).  Returns the overlap report as a dict."""
+        rep = OocReport()
+        enc = lambda x: x.encode() if x is not None else None
+        self._check(self._lib.gls_solve_file(self._h, enc(xr_path), xr_offset, elem_bytes, m, enc(b_path),
+                                             enc(status_path), block_groups, warmup_groups, mode,
+                                             ctypes.byref(rep)))
+        return rep.as_dict()
 
     def set_timing(self, enable: bool = True):
         self._check(self._lib.gls_set_timing(self._h, 1 if enable else 0))

@@ -76,3 +76,27 @@ def test_null_handles_extensions(lib):
     assert lib.gls_set_timing(None, 1) == 1
     d = ctypes.c_double()
     assert lib.gls_read_timing(None, ctypes.byref(d), ctypes.byref(d), ctypes.byref(d), ctypes.byref(a)) == 1
+
+
+def test_select_block_size_condition():
+    """§4.3: time(compute) > time(load) + time(store); two workspaces in memory."""
+    from paper_1210_7325_b200 import select_block_size
+    n, p, pR = 10_000, 4, 1
+    per = pR * n * 8 + p * 8 + 4
+    # memory caps the block: two workspaces of k problems
+    k, io = select_block_size(n, p, pR, 8, 2 * per * 1000, compute_groups_per_s=3e5, io_bytes_per_s=55e9)
+    assert k == 1000
+    # FP64 X_R over 55 GB/s: 80 kB per problem = 1.45 us of PCIe vs 3.3 us of compute -> compute-bound
+    assert io is False
+    # int8 codes at 3 M problems/s are compute-bound at 55 GB/s (10 kB per problem = 0.18 us vs 0.33 us)
+    k8, io8 = select_block_size(n, p, pR, 1, 1 << 34, compute_groups_per_s=3e6, io_bytes_per_s=55e9)
+    assert io8 is False and k8 == (1 << 34) // (2 * (n + p * 8 + 4))
+    # FP64 X_R at 3 M problems/s over 55 GB/s is I/O-bound (the paper's n > 8 F / B condition fails)
+    _, iob = select_block_size(n, p, pR, 8, 1 << 34, compute_groups_per_s=3e6, io_bytes_per_s=55e9)
+    assert iob is True
+    # a per-request latency makes small blocks I/O-bound
+    _, iol = select_block_size(n, p, pR, 1, 2 * (n + 36) * 10, compute_groups_per_s=3e6, io_bytes_per_s=55e9,
+                               io_latency_s=1e-3)
+    assert iol is True
+    assert select_block_size(n, p, pR, 3, 1 << 30, 1.0, 1.0)[0] == -1
+    assert select_block_size(n, p, pR, 8, 10, 1.0, 1.0)[0] == -1

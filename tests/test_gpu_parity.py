@@ -441,3 +441,46 @@ def test_timing_hooks_and_counts(glsmod):
         t = ctx.read_timing()
         assert t["launches"] == 1 and t["fp64_ms"] > 0 and t["int8_ms"] == 0, t
         assert ctx.path_counts() == (1, 1)
+
+
+def test_solve_file_sync_and_async_bitwise(glsmod, tmp_path):
+    """Out-of-core from secondary storage (§4): Alg. 7 (sync) and Alg. 8 (double-buffered) over FP64
+    and int8-code X_R files, with a warm-up block (§4.3), give exactly the in-core bits; the report
+    accounts for every block and byte; bad files are GLS_ERR_ARG."""
+    n, pL, pR, m = 700, 3, 1, 3000
+    P = gen.make_problem(n, pL, pR, seed=25)
+    XR = gen.make_XR(25, n, 0, m)
+    hdr = np.arange(8, dtype=np.float64)  # 64-byte header before the stream
+    f64 = tmp_path / "xr_f64.bin"
+    with open(f64, "wb") as f:
+        f.write(hdr.tobytes())
+        f.write(XR.tobytes())
+    i8 = tmp_path / "xr_i8.bin"
+    XR.astype(np.int8).tofile(i8)
+    bpath, spath = str(tmp_path / "b.bin"), str(tmp_path / "st.bin")
+    with glsmod.Context(n, pL, pR, dev(P.M), dev(P.XL), dev(P.y)) as ctx:
+        ref = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+        ctx.solve_block(dev(XR), m, ref)
+        ref = ref.cpu().numpy()
+        b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR[:200], pR)
+        assert_parity(ref[:200], np.zeros(200, np.int32), b_or, st_or, label="file ref")
+        for mode in (glsmod.GLS_OOC_SYNC, glsmod.GLS_OOC_ASYNC):
+            for path, elem, off in ((str(f64), 8, 64), (str(i8), 1, 0)):
+                rep = ctx.solve_file(path, m, bpath, spath, elem_bytes=elem, xr_offset=off, block_groups=700,
+                                     warmup_groups=100, mode=mode)
+                b = np.fromfile(bpath).reshape(m, 4)
+                st = np.fromfile(spath, dtype=np.int32)
+                np.testing.assert_array_equal(b, ref)
+                assert st.shape == (m,) and not st.any()
+                assert rep["blocks"] == 1 + (m - 100 + 699) // 700
+                assert rep["bytes_read"] == m * n * elem and rep["bytes_written"] == m * 4 * 8
+                assert rep["wall_s"] >= rep["compute_s"] > 0 and rep["read_wait_s"] >= rep["first_load_s"] >= 0
+        with pytest.raises(glsmod.GLSError) as e:
+            ctx.solve_file(str(tmp_path / "missing.bin"), m, bpath)
+        assert e.value.code == 1
+        short = tmp_path / "short.bin"
+        XR[: m // 2].tofile(short)
+        for mode in (glsmod.GLS_OOC_SYNC, glsmod.GLS_OOC_ASYNC):
+            with pytest.raises(glsmod.GLSError) as e:
+                ctx.solve_file(str(short), m, bpath, block_groups=500, mode=mode)
+            assert e.value.code == 1
