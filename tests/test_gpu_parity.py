@@ -484,3 +484,18 @@ def test_solve_file_sync_and_async_bitwise(glsmod, tmp_path):
             with pytest.raises(glsmod.GLSError) as e:
                 ctx.solve_file(str(short), m, bpath, block_groups=500, mode=mode)
             assert e.value.code == 1
+
+
+def test_algorithm_ladder_agrees(glsmod):
+    """NEXT-2: seq-gls (Alg. 4: every problem's p columns whitened, FP64 path) and black-box (Alg. 3: a
+    factorization per problem) on the B200 kernels reproduce hp-gwas's b -- an
+    independent GPU-side check of the Fig. 1 partition."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "ladder", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "ladder.py"))
+    ladder = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(ladder)
+    out = ladder.run(300, 3, 1, 300, 6, seed=26)
+    dev_ = out["max_rel_dev_from_hp_gwas"]
+    assert dev_["seq-gls"] <= 1e-11 and dev_["black-box"] <= 1e-11, dev_
