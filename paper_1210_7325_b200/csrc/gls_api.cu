@@ -54,7 +54,7 @@ struct gls_ctx {
   cudaStream_t conv = nullptr;
   int64_t x8_cols = 0, ld8 = 0;
   int8_t* x8[2] = {nullptr, nullptr};
-  int* flags = nullptr;                  // 2 ints
+  int* flags = nullptr;                  // 2 ints, then (8-byte aligned) 2 work counters
   unsigned long long* ran = nullptr;     // [0] int8 kernel launches that ran, [1] FP64 ones
   cudaEvent_t ev_conv[2] = {}, ev_oz[2] = {}, ev_fb[2] = {};
   cudaStream_t fb = nullptr;  // gated FP64 fallback launches (off the int8 kernel's stream)
@@ -195,7 +195,7 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
   CK(c, dalloc(c, &c->Tpk, c->Tpk_bytes));
   CK(c, dalloc(c, &c->Wpk, c->Wpk_bytes));
   CK(c, dalloc(c, &c->G, c->G_bytes));
-  CK(c, dalloc(c, &c->flags, 2 * sizeof(int)));
+  CK(c, dalloc(c, &c->flags, 2 * sizeof(int) + 2 * sizeof(unsigned long long)));
   CK(c, dalloc(c, &c->ran, 2 * sizeof(unsigned long long)));
   CK(c, cudaMemsetAsync(c->ran, 0, 2 * sizeof(unsigned long long), c->own_stream));
   if (c->oz_ok) {
@@ -473,9 +473,11 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
     CK(c, cudaEventRecord(c->ev_oz[buf], c->stream));
     CK(c, cudaStreamWaitEvent(c->conv, c->ev_oz[buf], 0));
     CK(c, cudaStreamWaitEvent(c->conv, c->ev_fb[buf], 0));  // the fallback of chunk j-2 read flags[buf]
+    unsigned long long* work = (unsigned long long*)(c->flags + 2) + buf;
     CK(c, cudaMemsetAsync(c->flags + buf, 0, sizeof(int), c->conv));
+    CK(c, cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->conv));
     LaunchTimer lt(c, c->conv, 2);
-    oz_convert(c->conv, X + (size_t)g0 * pR * ldx, ldx, c->n, gc * pR, c->x8[buf], c->ld8, c->flags + buf,
+    oz_convert(c->conv, X + (size_t)g0 * pR * ldx, ldx, c->n, gc * pR, c->x8[buf], c->ld8, c->flags + buf, work,
                c->num_sms, &c->launches);
     CK(c, cudaGetLastError());
     CK(c, cudaEventRecord(c->ev_conv[buf], c->conv));
@@ -810,10 +812,17 @@ int gls_read_timing(gls_ctx* c, double* ms_int8, double* ms_fp64, double* ms_con
   int rc = sync_all(c);
   if (rc) return rc;
   double t[3] = {0, 0, 0};
+  static const bool trace = getenv("GLS_TRACE_LAUNCHES") != nullptr;  // diagnostics: the timeline
   for (auto& x : c->tl) {
     float ms = 0.f;
     CK(c, cudaEventElapsedTime(&ms, x.a, x.b));
     t[x.kind] += ms;
+    if (trace) {
+      float t0 = 0.f;
+      cudaEventElapsedTime(&t0, c->tl.front().a, x.a);
+      static const char* kinds[3] = {"int8", "fp64", "conv"};
+      fprintf(stderr, "[gls] launch %-4s start %9.3f ms  dur %8.3f ms\n", kinds[x.kind], t0, ms);
+    }
     c->ev_pool.push_back(x.a);
     c->ev_pool.push_back(x.b);
   }

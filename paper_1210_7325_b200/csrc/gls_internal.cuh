@@ -122,8 +122,9 @@ void oz_setup(cudaStream_t s, const double* T, int64_t ld, int64_t n, const doub
               int8_t* T8, double* aux, int* escale, const double* V, int8_t* V8, double* vscale,
               int64_t* launch_counter);
 // X (double) -> X8 (int8, ld8 % 16 == 0); *flag |= 1 if some value is not an integer in [-128,127].
+// work: a zeroed unsigned long long (the pass's work-stealing counter).
 void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t cols, int8_t* X8,
-                int64_t ld8, int* flag, int num_sms, int64_t* launch_counter);
+                int64_t ld8, int* flag, unsigned long long* work, int num_sms, int64_t* launch_counter);
 struct OzArgs {
   const int8_t* X8;     // column-major, ld8 (multiple of 16), device
   int64_t ld8;

@@ -639,37 +639,51 @@ __device__ __forceinline__ uint32_t to_i8_bits(double v, int& bad) {
 // int8 kernel, which leaves only a few thousand registers free per SM sub-partition, and it uses no
 // FP64 arithmetic, which would contend with that kernel's tensor-core work.  X rows start 16-byte
 // aligned (ldx even, base 16-byte aligned).
+// Work-stealing: blocks claim units of kConvCols columns from an atomic counter (work[0], zeroed with
+// the flag), so the few blocks that co-reside with the int8 kernel convert as much as they can and
+// the remainder finishes on the whole GPU the moment that kernel ends.
+constexpr int kConvCols = 16;
 __global__ void __launch_bounds__(64) oz_x_to_i8_kernel(const double* __restrict__ X, int64_t ldx, int64_t n,
                                                         int64_t cols, int8_t* __restrict__ X8, int64_t ld8,
-                                                        int* __restrict__ flag) {
+                                                        int* __restrict__ flag,
+                                                        unsigned long long* __restrict__ work) {
+  __shared__ unsigned long long unit;
   const int64_t per_col = (n + 7) >> 3;
-  const int64_t total = per_col * cols;
+  const int64_t nunits = (cols + kConvCols - 1) / kConvCols;
   int bad = 0;
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
-       o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t col = o / per_col;
-    const int64_t r0 = (o - col * per_col) << 3;
-    const double* src = X + col * ldx + r0;
-    uint32_t w0 = 0, w1 = 0;
-    if (r0 + 8 <= n) {
-      double2 v[4];
+  for (;;) {
+    if (threadIdx.x == 0) unit = atomicAdd(work, 1ull);
+    __syncthreads();
+    const int64_t u = (int64_t)unit;
+    __syncthreads();
+    if (u >= nunits) break;
+    const int64_t c0 = u * kConvCols;
+    const int64_t nc = (cols - c0 < kConvCols) ? cols - c0 : kConvCols;
+    for (int64_t o = threadIdx.x; o < per_col * nc; o += blockDim.x) {
+      const int64_t col = c0 + o / per_col;
+      const int64_t r0 = (o % per_col) << 3;
+      const double* src = X + col * ldx + r0;
+      uint32_t w0 = 0, w1 = 0;
+      if (r0 + 8 <= n) {
+        double2 v[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] = __ldcs((const double2*)src + k);
-      w0 = to_i8_bits(v[0].x, bad) | to_i8_bits(v[0].y, bad) << 8 | to_i8_bits(v[1].x, bad) << 16 |
-           to_i8_bits(v[1].y, bad) << 24;
-      w1 = to_i8_bits(v[2].x, bad) | to_i8_bits(v[2].y, bad) << 8 | to_i8_bits(v[3].x, bad) << 16 |
-           to_i8_bits(v[3].y, bad) << 24;
-    } else {
-      for (int k = 0; r0 + k < n; ++k) {
-        const uint32_t t = to_i8_bits(__ldcs(src + k), bad) << (8 * (k & 3));
-        if (k < 4) w0 |= t; else w1 |= t;
+        for (int k = 0; k < 4; ++k) v[k] = __ldcs((const double2*)src + k);
+        w0 = to_i8_bits(v[0].x, bad) | to_i8_bits(v[0].y, bad) << 8 | to_i8_bits(v[1].x, bad) << 16 |
+             to_i8_bits(v[1].y, bad) << 24;
+        w1 = to_i8_bits(v[2].x, bad) | to_i8_bits(v[2].y, bad) << 8 | to_i8_bits(v[3].x, bad) << 16 |
+             to_i8_bits(v[3].y, bad) << 24;
+      } else {
+        for (int k = 0; r0 + k < n; ++k) {
+          const uint32_t t = to_i8_bits(__ldcs(src + k), bad) << (8 * (k & 3));
+          if (k < 4) w0 |= t; else w1 |= t;
+        }
       }
-    }
-    int8_t* dst = X8 + col * ld8 + r0;
-    if (r0 + 8 <= ld8) {
-      *(uint2*)dst = make_uint2(w0, w1);
-    } else {
-      for (int k = 0; r0 + k < ld8; ++k) dst[k] = (int8_t)((k < 4 ? w0 : w1) >> (8 * (k & 3)));
+      int8_t* dst = X8 + col * ld8 + r0;
+      if (r0 + 8 <= ld8) {
+        *(uint2*)dst = make_uint2(w0, w1);
+      } else {
+        for (int k = 0; r0 + k < ld8; ++k) dst[k] = (int8_t)((k < 4 ? w0 : w1) >> (8 * (k & 3)));
+      }
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
@@ -742,12 +756,12 @@ void oz_setup(cudaStream_t s, const double* T, int64_t ld, int64_t n, const doub
 }
 
 void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t cols, int8_t* X8,
-                int64_t ld8, int* flag, int num_sms, int64_t* lc) {
-  const int64_t total = ((n + 7) >> 3) * cols;
-  int64_t blocks = (total + 63) / 64;
-  if (blocks > (int64_t)num_sms * 32) blocks = (int64_t)num_sms * 32;
+                int64_t ld8, int* flag, unsigned long long* work, int num_sms, int64_t* lc) {
+  const int64_t nunits = (cols + kConvCols - 1) / kConvCols;
+  int64_t blocks = (int64_t)num_sms * 32;
+  if (blocks > nunits) blocks = nunits;
   if (blocks < 1) blocks = 1;
-  oz_x_to_i8_kernel<<<(unsigned)blocks, 64, 0, s>>>(X, ldx, n, cols, X8, ld8, flag);
+  oz_x_to_i8_kernel<<<(unsigned)blocks, 64, 0, s>>>(X, ldx, n, cols, X8, ld8, flag, work);
   if (lc) ++*lc;
 }
 
