@@ -19,7 +19,7 @@
 namespace gls {
 namespace {
 
-constexpr int LEAF = 96;
+constexpr int LEAF = 64;
 constexpr int LEAF_THREADS = 1024;
 constexpr int LLD = LEAF + 1;
 
@@ -125,13 +125,21 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A,
   }
 }
 
+// Streams of the recursion: the main stream s (the context's, high priority) carries the critical
+// path; at each depth a low-priority "side" stream takes the part of the trailing update the next
+// leaf does not need yet (look-ahead) and an "aux" stream the Y = L21 T11 product.  Each stream has
+// its own split-K workspace.
+constexpr int kMaxDepth = 24;
+constexpr int64_t kLookaheadMin = 1024;  // smallest trailing node split for look-ahead
 struct RecCtx {
-  cudaStream_t s, aux;  // Y = L21 T11 runs on aux, overlapping the recursion on A22
+  cudaStream_t s;
+  cudaStream_t side[kMaxDepth], aux[kMaxDepth];
+  double* ws_main;
+  double* ws_side[kMaxDepth];
+  double* ws_aux[kMaxDepth];
   std::vector<cudaEvent_t>* events;
   CholStatus* st;
   int64_t* lc;
-  double* ws_main;  // split-K workspaces, one per stream
-  double* ws_aux;
 };
 
 cudaEvent_t new_event(RecCtx& rc) {
@@ -140,8 +148,22 @@ cudaEvent_t new_event(RecCtx& rc) {
   rc.events->push_back(e);
   return e;
 }
+cudaEvent_t record(RecCtx& rc, cudaStream_t st) {
+  cudaEvent_t e = new_event(rc);
+  cudaEventRecord(e, st);
+  return e;
+}
 
-void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64_t goff) {
+int64_t first_block(int64_t n) {  // size of the leading block of the split of an n x n node
+  const int64_t nblk = (n + LEAF - 1) / LEAF;
+  return LEAF * ((nblk + 1) / 2);
+}
+
+// Factor and invert the n x n node at A (T receives the inverse).  On entry the node's leading
+// first_block(n) x first_block(n) block is up to date in the order of the main stream; the rest of
+// the node (rows below it) is up to date once `rest_ready` has fired (nullptr: already).
+void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64_t goff, cudaEvent_t rest_ready,
+                  int depth) {
   cudaStream_t s = rc.s;
   if (n <= LEAF) {
     constexpr int kLeafSmem = 2 * LEAF * LLD * sizeof(double);
@@ -150,33 +172,52 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
       cudaFuncSetAttribute(chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
       attr = true;
     }
+    if (rest_ready) cudaStreamWaitEvent(s, rest_ready, 0);
     chol_inv_leaf<<<1, LEAF_THREADS, kLeafSmem, s>>>((int)n, A, T, ld, goff, rc.st);
     if (rc.lc) ++*rc.lc;
     return;
   }
-  const int64_t nblk = (n + LEAF - 1) / LEAF;
-  const int64_t h1 = LEAF * ((nblk + 1) / 2), h2 = n - h1;
+  const int d = depth < kMaxDepth ? depth : kMaxDepth - 1;
+  const int64_t h1 = first_block(n), h2 = n - h1;
   double* A11 = A;
   double* A21 = A + h1;
   double* A22 = A + h1 + h1 * ld;
   double* T11 = T;
-  double* T21 = T + h1;
+  double* T21 = T + h1;  // holds L21 until T21 is formed
   double* T22 = T + h1 + h1 * ld;
-  chol_inv_rec(rc, h1, A11, T11, ld, goff);
-  // L21 = A21 T11^T  -> stored in T21's (still unused) place
-  dgemm(s, h2, h1, h1, 1.0, A21, ld, 'N', T11, ld, 'T', 0.0, T21, ld, GEMM_KMAX_COL, rc.lc, rc.ws_main);
-  // A22 -= L21 L21^T (lower)
-  dgemm(s, h2, h2, h1, -1.0, T21, ld, 'N', T21, ld, 'T', 1.0, A22, ld, GEMM_LOWER_C, rc.lc, rc.ws_main);
-  // Y = L21 T11 -> A21's place, on the aux stream: it only needs L21 and T11, so it overlaps the
-  // (latency-bound) recursion on A22, which touches A22 and T22 only.
-  cudaEvent_t e1 = new_event(rc), e2 = new_event(rc);
-  cudaEventRecord(e1, s);
-  cudaStreamWaitEvent(rc.aux, e1, 0);
-  dgemm(rc.aux, h2, h1, h1, 1.0, T21, ld, 'N', T11, ld, 'N', 0.0, A21, ld, GEMM_KMIN_COL, rc.lc, rc.ws_aux);
-  cudaEventRecord(e2, rc.aux);
-  chol_inv_rec(rc, h2, A22, T22, ld, goff + h1);
-  // T21 = -T22 Y  (overwrites L21: Y must be complete)
-  cudaStreamWaitEvent(s, e2, 0);
+  chol_inv_rec(rc, h1, A11, T11, ld, goff, nullptr, depth + 1);
+  if (rest_ready) cudaStreamWaitEvent(s, rest_ready, 0);  // A21, A22 updated by the caller's side work
+  // L21 = A21 T11^T and A22 -= L21 L21^T, split at g = the leading block of the A22 node: its rows
+  // [0, g) on the main stream (all the next leaf needs), the rest on the side stream, overlapping
+  // the recursion into A22's leading block.
+  // (small nodes: no split -- the extra launches cost more than the overlap gains)
+  const int64_t g = h2 >= kLookaheadMin ? first_block(h2) : h2;
+  cudaEvent_t e_start = record(rc, s);
+  dgemm(s, g, h1, h1, 1.0, A21, ld, 'N', T11, ld, 'T', 0.0, T21, ld, GEMM_KMAX_COL, rc.lc, rc.ws_main);
+  cudaEvent_t e_top = record(rc, s);
+  dgemm(s, g, g, h1, -1.0, T21, ld, 'N', T21, ld, 'T', 1.0, A22, ld, GEMM_LOWER_C, rc.lc, rc.ws_main);
+  cudaEvent_t e_rest = nullptr;
+  cudaStream_t sd = rc.side[d];
+  if (h2 > g) {
+    cudaStreamWaitEvent(sd, e_start, 0);
+    dgemm(sd, h2 - g, h1, h1, 1.0, A21 + g, ld, 'N', T11, ld, 'T', 0.0, T21 + g, ld, GEMM_KMAX_COL, rc.lc,
+          rc.ws_side[d]);
+    cudaStreamWaitEvent(sd, e_top, 0);
+    // rows [g, h2) of the lower triangle: columns [0, g) full, [g, h2) lower
+    dgemm(sd, h2 - g, g, h1, -1.0, T21 + g, ld, 'N', T21, ld, 'T', 1.0, A22 + g, ld, 0, rc.lc, rc.ws_side[d]);
+    dgemm(sd, h2 - g, h2 - g, h1, -1.0, T21 + g, ld, 'N', T21 + g, ld, 'T', 1.0, A22 + g + g * ld, ld,
+          GEMM_LOWER_C, rc.lc, rc.ws_side[d]);
+    e_rest = record(rc, sd);
+  }
+  // Y = L21 T11 -> A21's place, on the aux stream (after every read of A21 and every write of L21)
+  cudaStream_t sa = rc.aux[d];
+  cudaStreamWaitEvent(sa, record(rc, s), 0);
+  if (e_rest) cudaStreamWaitEvent(sa, e_rest, 0);
+  dgemm(sa, h2, h1, h1, 1.0, T21, ld, 'N', T11, ld, 'N', 0.0, A21, ld, GEMM_KMIN_COL, rc.lc, rc.ws_aux[d]);
+  cudaEvent_t e_y = record(rc, sa);
+  chol_inv_rec(rc, h2, A22, T22, ld, goff + h1, e_rest, depth + 1);
+  // T21 = -T22 Y  (overwrites L21: Y, and with it every reader of L21, must be complete)
+  cudaStreamWaitEvent(s, e_y, 0);
   dgemm(s, h2, h1, h2, -1.0, T22, ld, 'N', A21, ld, 'N', 0.0, T21, ld, GEMM_KMAX_ROW, rc.lc, rc.ws_main);
 }
 
@@ -190,25 +231,48 @@ void chol_prepare(cudaStream_t s, int64_t n, const double* A, int64_t ld, CholSt
 
 void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholStatus* st,
               int64_t* lc) {
-  cudaStream_t aux;
-  cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least urgent
+  int depth = 1;
+  for (int64_t k = n; k > LEAF && depth < kMaxDepth; k = first_block(k)) ++depth;
+  RecCtx rc{};
+  rc.s = s;
   std::vector<cudaEvent_t> events;
-  double* ws = nullptr;  // split-K workspaces (main, aux) from the stream-ordered pool
-  if (cudaMallocAsync((void**)&ws, 2 * kSplitKWsDoubles * sizeof(double), s) != cudaSuccess) {
+  rc.events = &events;
+  rc.st = st;
+  rc.lc = lc;
+  // split-K workspaces (main + side and aux per depth) from the stream-ordered pool
+  double* ws = nullptr;
+  const size_t nws = 1 + 2 * (size_t)depth;
+  if (cudaMallocAsync((void**)&ws, nws * kSplitKWsDoubles * sizeof(double), s) != cudaSuccess) {
     cudaGetLastError();
     ws = nullptr;
   }
-  RecCtx rc{s, aux, &events, st, lc, ws, ws ? ws + kSplitKWsDoubles : nullptr};
-  chol_inv_rec(rc, n, A, T, ld, 0);
-  // join: everything issued on aux is ordered before later work on s
-  cudaEvent_t done;
-  cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
-  cudaEventRecord(done, aux);
-  cudaStreamWaitEvent(s, done, 0);
-  cudaEventDestroy(done);
-  if (ws) cudaFreeAsync(ws, s);  // after the join: the aux stream's last use precedes it
+  rc.ws_main = ws;
+  for (int d = 0; d < depth; ++d) {
+    cudaStreamCreateWithPriority(&rc.side[d], cudaStreamNonBlocking, lo);
+    cudaStreamCreateWithPriority(&rc.aux[d], cudaStreamNonBlocking, lo);
+    rc.ws_side[d] = ws ? ws + (1 + 2 * d) * kSplitKWsDoubles : nullptr;
+    rc.ws_aux[d] = ws ? ws + (2 + 2 * d) * kSplitKWsDoubles : nullptr;
+  }
+  // the side/aux streams see the workspace allocation through this event
+  cudaEvent_t e0 = record(rc, s);
+  for (int d = 0; d < depth; ++d) {
+    cudaStreamWaitEvent(rc.side[d], e0, 0);
+    cudaStreamWaitEvent(rc.aux[d], e0, 0);
+  }
+  chol_inv_rec(rc, n, A, T, ld, 0, nullptr, 0);
+  // join: everything issued on the side and aux streams is ordered before later work on s
+  for (int d = 0; d < depth; ++d) {
+    cudaStreamWaitEvent(s, record(rc, rc.side[d]), 0);
+    cudaStreamWaitEvent(s, record(rc, rc.aux[d]), 0);
+  }
+  if (ws) cudaFreeAsync(ws, s);  // after the join
   for (cudaEvent_t e : events) cudaEventDestroy(e);
-  cudaStreamDestroy(aux);
+  for (int d = 0; d < depth; ++d) {
+    cudaStreamDestroy(rc.side[d]);
+    cudaStreamDestroy(rc.aux[d]);
+  }
 }
 
 }  // namespace gls

@@ -167,7 +167,9 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
   c->NB = (n + kNB - 1) / kNB;
   CK(c, cudaGetDevice(&c->device));
   CK(c, cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
-  CK(c, cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;  // the context's stream is high priority: in gls_create it carries the
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);  // critical path of the factorisation
+  CK(c, cudaStreamCreateWithPriority(&c->own_stream, cudaStreamNonBlocking, prio_hi));
   CK(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->conv, cudaStreamNonBlocking));
