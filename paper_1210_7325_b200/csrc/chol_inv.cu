@@ -249,9 +249,16 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
     ws = nullptr;
   }
   rc.ws_main = ws;
+  // side/aux streams: created once per device and kept (stream creation would cost ~0.5 ms a call)
+  static cudaStream_t pool_side[64][kMaxDepth] = {}, pool_aux[64][kMaxDepth] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
   for (int d = 0; d < depth; ++d) {
-    cudaStreamCreateWithPriority(&rc.side[d], cudaStreamNonBlocking, lo);
-    cudaStreamCreateWithPriority(&rc.aux[d], cudaStreamNonBlocking, lo);
+    if (!pool_side[dev][d]) cudaStreamCreateWithPriority(&pool_side[dev][d], cudaStreamNonBlocking, lo);
+    if (!pool_aux[dev][d]) cudaStreamCreateWithPriority(&pool_aux[dev][d], cudaStreamNonBlocking, lo);
+    rc.side[d] = pool_side[dev][d];
+    rc.aux[d] = pool_aux[dev][d];
     rc.ws_side[d] = ws ? ws + (1 + 2 * d) * kSplitKWsDoubles : nullptr;
     rc.ws_aux[d] = ws ? ws + (2 + 2 * d) * kSplitKWsDoubles : nullptr;
   }
@@ -269,10 +276,6 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
   }
   if (ws) cudaFreeAsync(ws, s);  // after the join
   for (cudaEvent_t e : events) cudaEventDestroy(e);
-  for (int d = 0; d < depth; ++d) {
-    cudaStreamDestroy(rc.side[d]);
-    cudaStreamDestroy(rc.aux[d]);
-  }
 }
 
 }  // namespace gls
