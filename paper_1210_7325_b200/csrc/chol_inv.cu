@@ -167,11 +167,8 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
   cudaStream_t s = rc.s;
   if (n <= LEAF) {
     constexpr int kLeafSmem = 2 * LEAF * LLD * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    if (first_use_on_device((const void*)chol_inv_leaf))
       cudaFuncSetAttribute(chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
-      attr = true;
-    }
     if (rest_ready) cudaStreamWaitEvent(s, rest_ready, 0);
     chol_inv_leaf<<<1, LEAF_THREADS, kLeafSmem, s>>>((int)n, A, T, ld, goff, rc.st);
     if (rc.lc) ++*rc.lc;

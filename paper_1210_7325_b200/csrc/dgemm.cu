@@ -172,11 +172,8 @@ __global__ void dgemm_splitk_reduce(GemmParams p) {
 
 template <bool TA, bool TB>
 void launch(cudaStream_t s, dim3 grid, const GemmParams& p) {
-  static bool attr = false;
-  if (!attr) {
+  if (first_use_on_device((const void*)dgemm_kernel<TA, TB>))
     cudaFuncSetAttribute(dgemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    attr = true;
-  }
   dgemm_kernel<TA, TB><<<grid, THREADS, SMEM_BYTES, s>>>(p);
 }
 

@@ -497,12 +497,10 @@ PFN_encodeTiled get_encode() {
 template <int NW, bool FULL, bool ALIGNED>
 cudaError_t launch_variant(cudaStream_t s, const CUtensorMap& map, const KParams& kp, int num_sms) {
   using C = KCfg<NW, FULL>;
-  static bool attr_done = false;
-  if (!attr_done) {
+  if (first_use_on_device((const void*)fused_trsm_gls_kernel<NW, FULL, ALIGNED>)) {
     cudaError_t e = cudaFuncSetAttribute(fused_trsm_gls_kernel<NW, FULL, ALIGNED>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::bytes);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   const int64_t grid = kp.num_panels < num_sms ? kp.num_panels : num_sms;
   fused_trsm_gls_kernel<NW, FULL, ALIGNED><<<(unsigned)grid, kThreads, C::bytes, s>>>(map, kp);

@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -17,6 +19,17 @@
 #include "gls_internal.cuh"
 
 using namespace gls;
+
+namespace gls {
+bool first_use_on_device(const void* key) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  return done.insert({key, dev}).second;
+}
+}  // namespace gls
 
 namespace {
 enum CtxState { ST_OK = 0, ST_FAILED = 1, ST_ADOPT = 2 };

@@ -9,6 +9,10 @@
 
 namespace gls {
 
+// Per-device "done once" flags for kernel attribute setup (a process may drive several GPUs):
+// returns true the first time it is called for (key, current device).
+bool first_use_on_device(const void* key);
+
 // ---------------------------------------------------------------- hot-kernel tiling constants
 // Row block of T / z handled per epilogue ("nb" in DESIGN.md), K extent per pipeline stage.
 constexpr int kNB = 128;         // z rows per row block (4 warp slices x 32)

@@ -102,14 +102,16 @@ extern "C" int gls_solve_file(gls_ctx* ctx, const char* xr_path, int64_t xr_offs
   if (rc0) return rc0;
   const int32_t p = pL + pR;
   if (m < 1 || block_groups < 1 || warmup_groups < 0) return GLS_ERR_DIM;
-  const int fx = open(xr_path, O_RDONLY);
-  if (fx < 0) return GLS_ERR_ARG;
-  // Alg. 7 is synchronous I/O: no kernel readahead behind the computation; Alg. 8 streams
-  posix_fadvise(fx, 0, 0, mode == GLS_OOC_SYNC ? POSIX_FADV_RANDOM : POSIX_FADV_SEQUENTIAL);
+  // X_R is read with O_DIRECT when every block is 4 KiB-aligned in offset and length (no page cache,
+  // no kernel readahead: Alg. 7 is then really synchronous and Alg. 8's overlap is all ours), else
+  // buffered.  The pinned workspaces are page-aligned.
+  const int fx_buf = open(xr_path, O_RDONLY);
+  if (fx_buf < 0) return GLS_ERR_ARG;
+  int fx_direct = -1;
   const int fb = open(b_path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
   const int fs = status_path ? open(status_path, O_WRONLY | O_CREAT | O_TRUNC, 0644) : -1;
   if (fb < 0 || (status_path && fs < 0)) {
-    close(fx);
+    close(fx_buf);
     if (fb >= 0) close(fb);
     if (fs >= 0) close(fs);
     return GLS_ERR_ARG;
@@ -129,6 +131,14 @@ extern "C" int gls_solve_file(gls_ctx* ctx, const char* xr_path, int64_t xr_offs
     }
   }
   const std::vector<Block> blocks = plan(m, block_groups, warmup_groups);
+  {
+    bool aligned = xr_offset % 4096 == 0;
+    for (const Block& bk : blocks)
+      aligned = aligned && ((int64_t)bk.g0 * pR * (int64_t)col_bytes) % 4096 == 0 &&
+                (bk.g0 + bk.cnt == m || ((int64_t)bk.cnt * pR * (int64_t)col_bytes) % 4096 == 0);
+    if (aligned && xcap % 4096 == 0) fx_direct = open(xr_path, O_RDONLY | O_DIRECT);
+  }
+  const int fx = fx_direct >= 0 ? fx_direct : fx_buf;
   gls_ooc_report r;
   memset(&r, 0, sizeof r);
   r.blocks = (int64_t)blocks.size();
@@ -139,7 +149,19 @@ extern "C" int gls_solve_file(gls_ctx* ctx, const char* xr_path, int64_t xr_offs
   };
   auto do_read = [&](Workspace& w, const Block& bk) -> bool {
     const size_t bytes = (size_t)bk.cnt * pR * col_bytes;
-    return read_full(fx, w.x, bytes, (off_t)(xr_offset + (int64_t)bk.g0 * pR * (int64_t)col_bytes));
+    const off_t off = (off_t)(xr_offset + (int64_t)bk.g0 * pR * (int64_t)col_bytes);
+    if (fx != fx_direct || bytes % 4096 == 0) return read_full(fx, w.x, bytes, off);
+    // last block under O_DIRECT: read whole 4 KiB units (the file may end inside the last one)
+    const size_t up = (bytes + 4095) & ~(size_t)4095;
+    if (up > xcap) return read_full(fx_buf, w.x, bytes, off);
+    char* p = (char*)w.x;
+    size_t got = 0;
+    while (got < up) {
+      const ssize_t rr = pread(fx, p + got, up - got, off + (off_t)got);
+      if (rr <= 0) break;
+      got += (size_t)rr;
+    }
+    return got >= bytes;
   };
   auto do_write = [&](Workspace& w, const Block& bk) -> bool {
     bool ok = write_full(fb, w.b, (size_t)bk.cnt * p * sizeof(double), (off_t)(bk.g0 * p * (int64_t)sizeof(double)));
@@ -262,7 +284,8 @@ extern "C" int gls_solve_file(gls_ctx* ctx, const char* xr_path, int64_t xr_offs
     if (ws[k].b) cudaFreeHost(ws[k].b);
     if (ws[k].st) cudaFreeHost(ws[k].st);
   }
-  close(fx);
+  close(fx_buf);
+  if (fx_direct >= 0) close(fx_direct);
   close(fb);
   if (fs >= 0) close(fs);
   if (rep) *rep = r;

@@ -714,20 +714,24 @@ cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& xmap, const CUt
   static_assert(ST >= 4, "shared memory budget");
   constexpr int smem = ST * (kATile + kBHalf) + kFixed;
   auto kern = ozaki_trsm_gls_kernel<PL1C, NA, PR1, ST>;
-  static int max_pairs = -1;
-  if (max_pairs < 0) {
+  static int max_pairs_dev[64];  // per device: cluster occupancy of this variant
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (first_use_on_device((const void*)kern)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    max_pairs = num_sms / 2;
+    int mp = num_sms / 2;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * max_pairs));
+    cfg.gridDim = dim3((unsigned)(2 * mp));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     int nc = 0;
-    if (cudaOccupancyMaxActiveClusters(&nc, (void*)kern, &cfg) == cudaSuccess && nc > 0 && nc < max_pairs)
-      max_pairs = nc;
+    if (cudaOccupancyMaxActiveClusters(&nc, (void*)kern, &cfg) == cudaSuccess && nc > 0 && nc < mp) mp = nc;
     cudaGetLastError();
+    max_pairs_dev[dev] = mp;
   }
+  const int max_pairs = max_pairs_dev[dev] > 0 ? max_pairs_dev[dev] : num_sms / 2;
   const int need = (kp.num_tiles + 1) / 2;
   const int np = need < max_pairs ? need : max_pairs;
   kern<<<2 * np, kThreads, smem, s>>>(xmap, tmap, vmap, kp);
