@@ -20,7 +20,11 @@ namespace gls {
 namespace {
 
 constexpr int LEAF = 64;
-constexpr int LEAF_THREADS = 1024;
+#ifndef GLS_LEAF_THREADS
+#define GLS_LEAF_THREADS 512
+#endif
+constexpr int LEAF_THREADS = GLS_LEAF_THREADS;
+constexpr int LEAF_TY = LEAF_THREADS / 32;  // thread rows of the update phase
 constexpr int LLD = LEAF + 1;
 
 __global__ void maxdiag_kernel(int64_t n, const double* A, int64_t ld, CholStatus* st) {
@@ -42,9 +46,10 @@ __global__ void maxdiag_kernel(int64_t n, const double* A, int64_t ld, CholStatu
 // One CTA: Cholesky of the nb x nb diagonal block at A (lower read) and, in the same sweep, its
 // inverse by forward elimination on [L | I]: after column j of L is final, row j of T is
 // T[j,:] /= L_jj and every later row is updated T[i,:] -= L_ij T[j,:] (i > j), so that on exit
-// L T = I.  Two barriers per column: (A) every warp forms L_jj = sqrt(d_j) itself and the column
-// j of L / row j of T are scaled; (B) the rank-1 updates, with the operands of each thread's
-// (at most 3 x 3) items loaded into registers before the stores.  Writes L into A's lower
+// L T = I.  One barrier per column: every warp forms L_jj = sqrt(d_j) itself, the rank-1 updates
+// read column j of L / row j of T scaled on the fly (operands of each thread's at most 2 x 2 items
+// loaded into registers before the stores), and the scaled column / row is written back during
+// the next column's step.  Writes L into A's lower
 // triangle and T = L^{-1} (zeros above the diagonal).
 __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A, double* T, int64_t ld,
                                                      int64_t goff, CholStatus* st) {
@@ -62,11 +67,14 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A,
   __syncthreads();
   const double tol = st->tol;
   const int ty = tid >> 5, tx = tid & 31;
-  constexpr int R = LEAF / 32;  // items per thread per dimension
+  constexpr int RY = LEAF / LEAF_TY;  // rows per thread
+  constexpr int R = LEAF / 32;        // columns per thread
+  // One barrier per column: the scaling of column j of L and row j of T by 1 / L_jj is applied on
+  // the fly by every reader in step j, and written back in step j+1 (nothing reads them any more).
+  double ljj_prev = 0.0, rinv_prev = 0.0;
   for (int j = 0; j < nb; ++j) {
-    // (A) pivot (computed redundantly by every thread; thread 0 records failures) and scaling
-    // one lane per warp takes the square root and the reciprocal; shuffles broadcast them (the
-    // FP64 pipe is too slow for 1024 redundant sqrt/div per column)
+    // pivot (one lane per warp takes the square root and the reciprocal; shuffles broadcast them --
+    // the FP64 pipe is too slow for 1024 redundant sqrt/div per column)
     const double d = L[j * LLD + j];
     const bool bad = !(d > tol) || failed;
     double ljj = 0.0, rinv = 0.0;
@@ -76,35 +84,35 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A,
     }
     ljj = __shfl_sync(0xffffffffu, ljj, 0);
     rinv = __shfl_sync(0xffffffffu, rinv, 0);
-    const int r = nb - j - 1;
-    for (int idx = tid; idx < r + j + 1; idx += blockDim.x) {
-      if (idx < r) L[(j + 1 + idx) * LLD + j] *= rinv;
-      else Ti[j * LLD + (idx - r)] *= rinv;
+    if (tid == 0 && bad && !failed) {
+      atomicMin(&st->fail, (unsigned long long)(goff + j));
+      failed = 1;  // read by every thread after this step's barrier
     }
-    __syncthreads();
-    if (tid == 0) {
-      if (bad && !failed) {
-        atomicMin(&st->fail, (unsigned long long)(goff + j));
-        failed = 1;
+    // deferred write-back of step j-1: column j-1 of L (rows >= j-1) and row j-1 of T, scaled
+    if (j > 0) {
+      const int jp = j - 1, r = nb - jp - 1;
+      for (int idx = tid; idx < r + jp + 2; idx += blockDim.x) {
+        if (idx < r) L[(jp + 1 + idx) * LLD + jp] *= rinv_prev;
+        else if (idx < r + jp + 1) Ti[jp * LLD + (idx - r)] *= rinv_prev;
+        else L[jp * LLD + jp] = ljj_prev;
       }
-      L[j * LLD + j] = ljj;
     }
-    // (B) trailing lower triangle of L and rows below j of T (columns 0..j); 32 x 32 threads
+    // trailing lower triangle of L and rows below j of T (columns 0..j); 32 x 32 threads
 #pragma unroll
-    for (int a = 0; a < R; ++a) {
-      const int i = j + 1 + ty + 32 * a;
+    for (int a = 0; a < RY; ++a) {
+      const int i = j + 1 + ty + LEAF_TY * a;
       if (i < nb) {
-        const double lij = L[i * LLD + j];
+        const double lij = L[i * LLD + j] * rinv;
         double lk[R], li[R], tj[R], ti[R];
 #pragma unroll
         for (int c = 0; c < R; ++c) {
           const int k = j + 1 + tx + 32 * c;
           const bool v = k <= i;
-          lk[c] = v ? L[k * LLD + j] : 0.0;
+          lk[c] = v ? L[k * LLD + j] * rinv : 0.0;
           li[c] = v ? L[i * LLD + k] : 0.0;
           const int k2 = tx + 32 * c;
           const bool v2 = k2 <= j;
-          tj[c] = v2 ? Ti[j * LLD + k2] : 0.0;
+          tj[c] = v2 ? Ti[j * LLD + k2] * rinv : 0.0;
           ti[c] = v2 ? Ti[i * LLD + k2] : 0.0;
         }
 #pragma unroll
@@ -115,6 +123,16 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A,
           if (k2 <= j) Ti[i * LLD + k2] = ti[c] - lij * tj[c];
         }
       }
+    }
+    ljj_prev = ljj;
+    rinv_prev = rinv;
+    __syncthreads();
+  }
+  if (nb > 0) {  // write-back of the last column
+    const int jp = nb - 1;
+    for (int idx = tid; idx < jp + 2; idx += blockDim.x) {
+      if (idx < jp + 1) Ti[jp * LLD + idx] *= rinv_prev;
+      else L[jp * LLD + jp] = ljj_prev;
     }
     __syncthreads();
   }
@@ -127,7 +145,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A,
 
 // Streams of the recursion: the main stream s (the context's, high priority) carries the critical
 // path; at each depth a low-priority "side" stream takes the part of the trailing update the next
-// leaf does not need yet (look-ahead) and an "aux" stream the Y = L21 T11 product.  Each stream has
+// leaf does not need yet (look-ahead) and a high-priority "aux" stream the Y = L21 T11 product.  Each stream has
 // its own split-K workspace.
 constexpr int kMaxDepth = 24;
 constexpr int64_t kLookaheadMin = 1024;  // smallest trailing node split for look-ahead
@@ -141,6 +159,22 @@ struct RecCtx {
   CholStatus* st;
   int64_t* lc;
 };
+
+// GLS_TRACE_CHOL=1 (diagnostics): timing events on the main stream after every step, printed per
+// (depth, step) at the end of chol_inv.
+struct Mark {
+  cudaEvent_t e;
+  int depth;
+  const char* what;
+};
+std::vector<Mark>* g_marks = nullptr;
+void mark(cudaStream_t s, int depth, const char* what) {
+  if (!g_marks) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  g_marks->push_back({e, depth, what});
+}
 
 cudaEvent_t new_event(RecCtx& rc) {
   cudaEvent_t e;
@@ -170,8 +204,10 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
     if (first_use_on_device((const void*)chol_inv_leaf))
       cudaFuncSetAttribute(chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
     if (rest_ready) cudaStreamWaitEvent(s, rest_ready, 0);
+    mark(s, depth, "wait-rest");
     chol_inv_leaf<<<1, LEAF_THREADS, kLeafSmem, s>>>((int)n, A, T, ld, goff, rc.st);
     if (rc.lc) ++*rc.lc;
+    mark(s, depth, "leaf");
     return;
   }
   const int d = depth < kMaxDepth ? depth : kMaxDepth - 1;
@@ -184,6 +220,7 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
   double* T22 = T + h1 + h1 * ld;
   chol_inv_rec(rc, h1, A11, T11, ld, goff, nullptr, depth + 1);
   if (rest_ready) cudaStreamWaitEvent(s, rest_ready, 0);  // A21, A22 updated by the caller's side work
+  mark(s, depth, "wait-rest");
   // L21 = A21 T11^T and A22 -= L21 L21^T, split at g = the leading block of the A22 node: its rows
   // [0, g) on the main stream (all the next leaf needs), the rest on the side stream, overlapping
   // the recursion into A22's leading block.
@@ -191,8 +228,10 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
   const int64_t g = h2 >= kLookaheadMin ? first_block(h2) : h2;
   cudaEvent_t e_start = record(rc, s);
   dgemm(s, g, h1, h1, 1.0, A21, ld, 'N', T11, ld, 'T', 0.0, T21, ld, GEMM_KMAX_COL, rc.lc, rc.ws_main);
+  mark(s, depth, "L21top");
   cudaEvent_t e_top = record(rc, s);
   dgemm(s, g, g, h1, -1.0, T21, ld, 'N', T21, ld, 'T', 1.0, A22, ld, GEMM_LOWER_C, rc.lc, rc.ws_main);
+  mark(s, depth, "SYRK11");
   cudaEvent_t e_rest = nullptr;
   cudaStream_t sd = rc.side[d];
   if (h2 > g) {
@@ -215,7 +254,9 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
   chol_inv_rec(rc, h2, A22, T22, ld, goff + h1, e_rest, depth + 1);
   // T21 = -T22 Y  (overwrites L21: Y, and with it every reader of L21, must be complete)
   cudaStreamWaitEvent(s, e_y, 0);
+  mark(s, depth, "wait-Y");
   dgemm(s, h2, h1, h2, -1.0, T22, ld, 'N', A21, ld, 'N', 0.0, T21, ld, GEMM_KMAX_ROW, rc.lc, rc.ws_main);
+  mark(s, depth, "T21");
 }
 
 }  // namespace
@@ -253,7 +294,8 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
   if (dev < 0 || dev >= 64) dev = 0;
   for (int d = 0; d < depth; ++d) {
     if (!pool_side[dev][d]) cudaStreamCreateWithPriority(&pool_side[dev][d], cudaStreamNonBlocking, lo);
-    if (!pool_aux[dev][d]) cudaStreamCreateWithPriority(&pool_aux[dev][d], cudaStreamNonBlocking, lo);
+    // Y is on the critical path (the node's T21 waits for it): high priority, unlike the look-ahead
+    if (!pool_aux[dev][d]) cudaStreamCreateWithPriority(&pool_aux[dev][d], cudaStreamNonBlocking, hi);
     rc.side[d] = pool_side[dev][d];
     rc.aux[d] = pool_aux[dev][d];
     rc.ws_side[d] = ws ? ws + (1 + 2 * d) * kSplitKWsDoubles : nullptr;
@@ -265,7 +307,37 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
     cudaStreamWaitEvent(rc.side[d], e0, 0);
     cudaStreamWaitEvent(rc.aux[d], e0, 0);
   }
+  static const bool trace = getenv("GLS_TRACE_CHOL") != nullptr;
+  std::vector<Mark> marks;
+  if (trace) {
+    g_marks = &marks;
+    mark(s, -1, "start");
+  }
   chol_inv_rec(rc, n, A, T, ld, 0, nullptr, 0);
+  if (trace) {
+    cudaStreamSynchronize(s);
+    double agg[kMaxDepth][6] = {};
+    const char* names[6] = {"leaf", "wait-rest", "L21top", "SYRK11", "wait-Y", "T21"};
+    for (size_t k = 1; k < marks.size(); ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, marks[k - 1].e, marks[k].e);
+      const int dd = marks[k].depth < kMaxDepth ? marks[k].depth : kMaxDepth - 1;
+      for (int q = 0; q < 6; ++q)
+        if (strcmp(marks[k].what, names[q]) == 0) agg[dd][q] += ms;
+    }
+    float tot = 0.f;
+    cudaEventElapsedTime(&tot, marks.front().e, marks.back().e);
+    fprintf(stderr, "[chol] total %.3f ms on the main stream\n", tot);
+    for (int dd = 0; dd < kMaxDepth; ++dd) {
+      double sum = 0;
+      for (int q = 0; q < 6; ++q) sum += agg[dd][q];
+      if (sum > 0)
+        fprintf(stderr, "[chol] depth %2d: leaf %7.3f wait-rest %7.3f L21top %7.3f SYRK11 %7.3f wait-Y %7.3f T21 %7.3f\n",
+                dd, agg[dd][0], agg[dd][1], agg[dd][2], agg[dd][3], agg[dd][4], agg[dd][5]);
+    }
+    for (auto& m : marks) cudaEventDestroy(m.e);
+    g_marks = nullptr;
+  }
   // join: everything issued on the side and aux streams is ordered before later work on s
   for (int d = 0; d < depth; ++d) {
     cudaStreamWaitEvent(s, record(rc, rc.side[d]), 0);
