@@ -499,3 +499,67 @@ def test_algorithm_ladder_agrees(glsmod):
     out = ladder.run(300, 3, 1, 300, 6, seed=26)
     dev_ = out["max_rel_dev_from_hp_gwas"]
     assert dev_["seq-gls"] <= 1e-11 and dev_["black-box"] <= 1e-11, dev_
+
+
+def test_config3_full_size_sampled_parity(glsmod):
+    """Config 3 at full size (n=1e4, pL=16, pR=4, 5e5 groups = 2e6 columns, 160 GB of X_R in HBM; the
+    bench launch): oracle parity on sampled groups incl. tile / pair / wave edges, and the planted-beta
+    identity on every group."""
+    cfg = gen.CONFIGS[3]
+    torch.cuda.empty_cache()  # earlier tests' X_R buffers sit in torch's cache
+    free, _ = torch.cuda.mem_get_info()
+    if free < 175e9:
+        pytest.skip("needs ~170 GB of free device memory")
+    P = gen.config_problem(cfg)
+    cols = cfg.m * cfg.pR
+    Xd = torch.empty((cols, cfg.n), dtype=torch.float64, device="cuda")
+    for c in range(0, cols, 65536):
+        k = min(65536, cols - c)
+        glsmod.gen_xr_device(SEED, cfg.n, c, k, Xd[c:c + k])
+    b, st, _ = run_gpu(glsmod, P, Xd, cfg.m, cfg.pR)
+    assert np.all(st == 0)
+    tile_g = 32  # groups per 128-column tile at pR = 4
+    wave_g = 148 * tile_g
+    edges = [0, 7, 8, tile_g - 1, tile_g, 2 * tile_g - 1, 2 * tile_g, wave_g - 1, wave_g, cfg.m - 1]
+    sel = np.unique(np.concatenate([np.random.default_rng(4).choice(cfg.m, 8, replace=False), edges]))
+    XRs = np.concatenate([gen.make_XR(SEED, cfg.n, int(i) * cfg.pR, cfg.pR) for i in sel])
+    Lf = oracle.cholesky(P.M)
+    b_or, st_or = oracle.gls_sequence(Lf, P.XL, P.y, XRs, cfg.pR, sel=sel, xr_is_selected=True)
+    err = assert_parity(b[sel], st[sel], b_or, st_or, label="config3 full sample")
+    print("config3 full-size sampled guarded err %.3e" % err)
+    P0 = gen.config_problem(cfg, noise=0.0)
+    b0, st0, _ = run_gpu(glsmod, P0, Xd, cfg.m, cfg.pR)
+    del Xd
+    ref = np.concatenate([P0.beta_L, np.zeros(cfg.pR)])
+    assert np.all(st0 == 0)
+    assert np.max(np.abs(b0 - ref)) / np.max(np.abs(P0.beta_L)) <= 1e-10
+
+
+def test_config4_shape_host_stream_codes(glsmod, n1e4_factor):
+    """The out-of-core launch configuration at n = 1e4: 200k SNPs streamed from pinned host memory as
+    int8 codes in several host chunks (Alg. 8) equal the in-HBM run bit for bit, and match the oracle
+    on sampled SNPs at chunk edges."""
+    cfg = gen.CONFIGS[4]
+    P, Lf = n1e4_factor
+    m = 200_000
+    Xd = torch.empty((m, cfg.n), dtype=torch.float64, device="cuda")
+    for c in range(0, m, 65536):
+        k = min(65536, m - c)
+        glsmod.gen_xr_device(SEED, cfg.n, c, k, Xd[c:c + k])
+    Gh = torch.empty((m, cfg.n), dtype=torch.int8).pin_memory()
+    Gh.copy_(Xd.to(torch.int8))
+    with glsmod.Context(cfg.n, cfg.pL, cfg.pR, dev(P.M), dev(P.XL), dev(P.y)) as ctx:
+        bd = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+        ctx.solve_block(Xd, m, bd)
+        bd = bd.cpu().numpy()
+        bh = torch.empty((m, 4), dtype=torch.float64).pin_memory()
+        sh = torch.empty(m, dtype=torch.int32).pin_memory()
+        chunk = 148 * 128 * 4
+        ctx.solve_block_i8(Gh, m, bh, sh)
+        np.testing.assert_array_equal(bh.numpy(), bd)
+        assert not sh.numpy().any()
+    del Xd
+    sel = np.unique([0, chunk - 1, chunk, 2 * chunk - 1, 2 * chunk, m - 1, 12345, 99999])
+    XRs = np.concatenate([gen.make_XR(SEED, cfg.n, int(i), 1) for i in sel])
+    b_or, st_or = oracle.gls_sequence(Lf, P.XL, P.y, XRs, 1, sel=sel, xr_is_selected=True)
+    assert_parity(bd[sel], np.zeros(len(sel), np.int32), b_or, st_or, label="config4 stream sample")
