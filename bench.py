@@ -63,7 +63,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--m", type=int, default=0, help="SNPs per rank (default: the config's m)")
+    ap.add_argument("--m", "--snps", dest="m", type=int, default=0, help="SNPs per rank (default: the config m)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
