@@ -187,25 +187,6 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-// Bulk copy global -> the same smem offset in every CTA of `mask`, completing tx on each CTA's
-// barrier at the offset of `bar`.
-__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                            uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, "
-      "[%3], %4;\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-// Arrive (once each) on the barrier at the offset of `bar` in every CTA of `mask` when all prior
-// tcgen05.mma of this thread have completed.
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
 }  // namespace umma
 }  // namespace gls
 
@@ -281,11 +262,3 @@ __device__ __forceinline__ void mma_commit_pair_mc(uint64_t* bar, uint16_t mask)
 }  // namespace umma
 }  // namespace gls
 
-namespace gls {
-namespace umma {
-// Orders this thread's generic-proxy global writes before later async-proxy (TMA) accesses.
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;\n" ::: "memory");
-}
-}  // namespace umma
-}  // namespace gls
