@@ -875,8 +875,10 @@ int gls_set_block_cols(gls_ctx* c, int64_t cols) {
 void gls_destroy(gls_ctx* c) {
   if (!c) return;
   DeviceGuard g(c->device);
+  // every stream that may still read or write context buffers, before the stream-ordered frees
   if (c->h2d) cudaStreamSynchronize(c->h2d);
   if (c->conv) cudaStreamSynchronize(c->conv);
+  if (c->fb) cudaStreamSynchronize(c->fb);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->d2h) cudaStreamSynchronize(c->d2h);
   free_staging(c);
@@ -900,8 +902,6 @@ void gls_destroy(gls_ctx* c) {
     cudaEventDestroy(x.b);
   }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
-  if (c->conv) cudaStreamSynchronize(c->conv);
-  if (c->fb) cudaStreamSynchronize(c->fb);
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
   for (int k = 0; k < 2; ++k) {
     if (c->ev_h2d[k]) cudaEventDestroy(c->ev_h2d[k]);
