@@ -177,7 +177,90 @@ void launch(cudaStream_t s, dim3 grid, const GemmParams& p) {
   dgemm_kernel<TA, TB><<<grid, THREADS, SMEM_BYTES, s>>>(p);
 }
 
+// ---------------------------------------------------------------- skinny products with T
+// W = T B (T n x n lower triangular, B n x k, k <= 21): memory-bound (T read once).  Grid = row
+// blocks of 128 x K segments; thread = one row, reading T column-major (a warp reads 32 consecutive
+// rows of one column); partial sums per segment, reduced in a fixed order (deterministic).
+constexpr int kSkinnySeg = 32;
+__global__ void trmm_skinny_partial(int64_t n, int k, const double* __restrict__ T, int64_t ldt,
+                                    const double* __restrict__ B, int64_t ldb, double* __restrict__ part) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int seg = blockIdx.y;
+  const int64_t span = (n + kSkinnySeg - 1) / kSkinnySeg;
+  const int64_t j0 = seg * span, j1 = (j0 + span < n) ? j0 + span : n;
+  double acc[21];
+#pragma unroll
+  for (int w = 0; w < 21; ++w) acc[w] = 0.0;
+  if (i < n) {
+    const int64_t jend = (i + 1 < j1) ? i + 1 : j1;  // lower triangular: j <= i
+    for (int64_t j = j0; j < jend; ++j) {
+      const double t = T[i + j * ldt];
+#pragma unroll
+      for (int w = 0; w < 21; ++w)
+        if (w < k) acc[w] = fma(t, __ldg(B + j + w * ldb), acc[w]);
+    }
+#pragma unroll
+    for (int w = 0; w < 21; ++w)
+      if (w < k) part[((int64_t)seg * k + w) * n + i] = acc[w];
+  }
+}
+__global__ void trmm_skinny_reduce(int64_t n, int k, const double* __restrict__ part, double* __restrict__ W,
+                                   int64_t ldw) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n * k; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = o % n;
+    const int w = (int)(o / n);
+    double v = 0.0;
+    for (int seg = 0; seg < kSkinnySeg; ++seg) v += part[((int64_t)seg * k + w) * n + i];
+    W[i + w * ldw] = v;
+  }
+}
+// V = T^T W (V[j, w] = sum_{i >= j} T[i, j] W[i, w]): one warp per column j of T (contiguous),
+// lanes stride over i, fixed-order shuffle reduction.
+__global__ void trmm_t_skinny(int64_t n, int k, const double* __restrict__ T, int64_t ldt,
+                              const double* __restrict__ W, int64_t ldw, double* __restrict__ V, int64_t ldv) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n;
+       j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double acc[21];
+#pragma unroll
+    for (int w = 0; w < 21; ++w) acc[w] = 0.0;
+    for (int64_t i = j + lane; i < n; i += 32) {
+      const double t = T[i + j * ldt];
+#pragma unroll
+      for (int w = 0; w < 21; ++w)
+        if (w < k) acc[w] = fma(t, __ldg(W + i + w * ldw), acc[w]);
+    }
+#pragma unroll
+    for (int w = 0; w < 21; ++w) {
+      if (w < k) {
+        double v = acc[w];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) V[j + w * ldv] = v;
+      }
+    }
+  }
+}
+
 }  // namespace
+
+void trmm_lower_skinny(cudaStream_t s, int64_t n, int k, const double* T, int64_t ldt, const double* B,
+                       int64_t ldb, double* W, int64_t ldw, double* part, int64_t* lc) {
+  dim3 grid((unsigned)((n + 127) / 128), kSkinnySeg);
+  trmm_skinny_partial<<<grid, 128, 0, s>>>(n, k, T, ldt, B, ldb, part);
+  const int64_t tot = n * k;
+  trmm_skinny_reduce<<<(unsigned)((tot + 255) / 256 < 1024 ? (tot + 255) / 256 : 1024), 256, 0, s>>>(n, k, part, W,
+                                                                                                      ldw);
+  if (lc) *lc += 2;
+}
+
+void trmm_lower_t_skinny(cudaStream_t s, int64_t n, int k, const double* T, int64_t ldt, const double* W,
+                         int64_t ldw, double* V, int64_t ldv, int64_t* lc) {
+  int64_t blocks = (n * 32 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  trmm_t_skinny<<<(unsigned)blocks, 256, 0, s>>>(n, k, T, ldt, W, ldw, V, ldv);
+  if (lc) ++*lc;
+}
 
 void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, char opA, const double* B, int64_t ldb, char opB, double beta, double* C,

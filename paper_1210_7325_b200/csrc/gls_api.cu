@@ -306,14 +306,19 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   // B = [X_L | y];  W = T B = [X~_L | y~];  G = W^T W  (S_TL and b_T)
   if (pL > 0) CKS(cudaMemcpyAsync(B, X_L, (size_t)n * pL * sizeof(double), cudaMemcpyDefault, s));
   CKS(cudaMemcpyAsync(B + (size_t)n * pL, y, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
-  dgemm(s, n, pL + 1, n, 1.0, T, n, 'N', B, n, 'N', 0.0, W, n, GEMM_KMAX_ROW, &c->launches);
+  // W = T B: memory-bound skinny product (the dense A, free after chol_inv, holds its 32 (pL+1) n
+  // partial sums when n >= 32 (pL+1); small n takes the tiled GEMM)
+  if (n >= 32 * (int64_t)(pL + 1))
+    trmm_lower_skinny(s, n, pL + 1, T, n, B, n, W, n, A, &c->launches);
+  else
+    dgemm(s, n, pL + 1, n, 1.0, T, n, 'N', B, n, 'N', 0.0, W, n, GEMM_KMAX_ROW, &c->launches);
   dgemm(s, pL + 1, pL + 1, n, 1.0, W, n, 'T', W, n, 'N', 0.0, c->G, pL + 1, 0, &c->launches);
   mark("W,G");
   pack_T(s, T, n, n, c->NB, c->Tpk, &c->launches);
   pack_W(s, W, n, n, pL + 1, c->NB, c->NW, c->Wpk, &c->launches);
   if (c->oz_ok) {
     // V = T^T W = M^{-1} [X_L | y] into B (free again: W = T B is formed)
-    dgemm(s, n, pL + 1, n, 1.0, T, n, 'T', W, n, 'N', 0.0, B, n, 0, &c->launches);
+    trmm_lower_t_skinny(s, n, pL + 1, T, n, W, n, B, n, &c->launches);
     oz_setup(s, T, n, n, W, pL + 1, c->T8, c->aux, esc, B, c->V8, c->vscale, &c->launches);
   }
   CKS(cudaGetLastError());

@@ -64,6 +64,13 @@ void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const 
            int64_t lda, char opA, const double* B, int64_t ldb, char opB, double beta, double* C,
            int64_t ldc, int flags, int64_t* launch_counter, double* ws = nullptr);
 
+// Skinny products with a lower-triangular T (k <= 21 columns; memory-bound, deterministic):
+// W = T B (part: scratch of 32 * n * k doubles) and V = T^T W.
+void trmm_lower_skinny(cudaStream_t s, int64_t n, int k, const double* T, int64_t ldt, const double* B,
+                       int64_t ldb, double* W, int64_t ldw, double* part, int64_t* launch_counter);
+void trmm_lower_t_skinny(cudaStream_t s, int64_t n, int k, const double* T, int64_t ldt, const double* W,
+                         int64_t ldw, double* V, int64_t ldv, int64_t* launch_counter);
+
 // ---------------------------------------------------------------- setup: Cholesky + inverse
 // In place: on return T (n x n, lower, ld) holds L^{-1} of M = L L^T; A (M on entry) is destroyed.
 // T must be zero-initialised.  tol_fail: device {double tol; unsigned long long fail_pivot}.
