@@ -367,8 +367,9 @@ def main():
                "path": "C ABI gls_solve_block_i8: M, X_L, y (FP64) and X_R as int8 genotype codes in pinned "
                        "host memory -> double-buffered H2D stream; b and status back to pinned host memory",
                "bitwise_equal_to_device_run": same8}
-        # FP64 X_R from host (8 bytes per genotype over PCIe)
-        m_f = int(min(m, 0.6 * avail / local_world / (n * pR * 8)))
+        # FP64 X_R from host (8 bytes per genotype over PCIe), on at most 250k SNPs per rank (20 GB
+        # pinned per rank at n = 1e4: a secondary number, kept cheap for the multi-GPU runs)
+        m_f = int(min(m, 250_000, 0.6 * avail / local_world / (n * pR * 8)))
         m_f = max(m_f - m_f % 64, 64)
         Xh = torch.empty((m_f * pR, n), dtype=torch.float64, pin_memory=True)
         for c in range(0, m_f * pR, chunk):
