@@ -300,8 +300,11 @@ def main():
         fp64eq = flops_per_launch / (int8_ms / 1e3) / 1e12
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s (int8)",
                     "frac": achieved / peak, "traffic": traffic, "kernel": "ozaki_trsm_gls_kernel",
-                    "kernel_ms": int8_ms, "int8_conversion_ms": conv_ms, "fp64_fallback_ms": fp64_ms,
-                    "solve_block_ms": kern_avg_ms, "create_ms": statistics.mean(create_ms),
+                    "kernel_ms": int8_ms,
+                    "int8_conversion_ms_concurrent": conv_ms,
+                    "fp64_fallback_ms": fp64_ms if paths[1] > 0 else 0.0,
+                    "solve_block_ms": kern_avg_ms, "exposed_overhead_ms": kern_avg_ms - int8_ms,
+                    "create_ms": statistics.mean(create_ms),
                     "int8_ops_per_launch": ops, "peak_source": psrc,
                     "frac_of_sustained_peak": achieved / peak_sus,
                     "fp64_equivalent": {"achieved_tflops": fp64eq, "dmma_peak_tflops": FP64_DMMA_PEAK_SUSTAINED,
@@ -396,6 +399,10 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "arithmetic": ("FP64 results; the trsm as exact int8 x int8 -> int32 digit products on tcgen05 "
+                               "(T = L^-1 split into 7 base-256 digits, 55 bits per row; X_R integer) combined "
+                               "and reduced in FP64 (DESIGN.md reading A15)") if roofline["kernel"].startswith("ozaki")
+                              else "FP64 on the DMMA tensor pipe",
                 "config": {"workload": "config%d: n=%d pL=%d pR=%d, %d SNPs per GPU in HBM (rank r owns "
                                        "SNPs [r*m, (r+1)*m))" % (args.config, n, pL, pR, m),
                            "n": n, "pL": pL, "pR": pR, "m_per_rank": m, "seed": args.seed,
