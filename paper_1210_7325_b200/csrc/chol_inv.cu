@@ -78,9 +78,9 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A,
     const double d = L[j * LLD + j];
     const bool bad = !(d > tol) || failed;
     double ljj = 0.0, rinv = 0.0;
-    if ((tid & 31) == 0) {
-      ljj = bad ? __longlong_as_double(0x7ff8000000000000LL) : sqrt(d);  // NaN poisons the rest
-      rinv = 1.0 / ljj;
+    if ((tid & 31) == 0) {  // rsqrt and one multiply: a shorter FP64 chain than sqrt + divide
+      rinv = bad ? __longlong_as_double(0x7ff8000000000000LL) : rsqrt(d);  // NaN poisons the rest
+      ljj = d * rinv;
     }
     ljj = __shfl_sync(0xffffffffu, ljj, 0);
     rinv = __shfl_sync(0xffffffffu, rinv, 0);
