@@ -89,6 +89,9 @@ def test_config0_all_snps(glsmod):
     (515, 4, 5, 41, True),      # pR = 5
     (640, 3, 8, 33, True),      # pR = 8
     (771, 19, 1, 40, False),    # p = 20 with pL = 19 (3 W tiles)
+    (2, 0, 1, 50, False),       # smallest problem: n = 2, p = 1
+    (21, 19, 1, 33, False),     # p = 20 with n = p + 1
+    (160, 2, 16, 5, True),      # pR = 16: two groups per warp quadrant
 ])
 def test_ragged_shapes(glsmod, n, pL, pR, m, sex):
     """Both arithmetic paths (int8 digit split on tcgen05, FP64 DMMA) against the oracle."""
