@@ -301,7 +301,6 @@ def main():
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s (int8)",
                     "frac": achieved / peak, "traffic": traffic, "kernel": "ozaki_trsm_gls_kernel",
                     "kernel_ms": int8_ms,
-                    "int8_conversion_ms_concurrent": conv_ms,
                     "fp64_fallback_ms": fp64_ms if paths[1] > 0 else 0.0,
                     "solve_block_ms": kern_avg_ms, "exposed_overhead_ms": kern_avg_ms - int8_ms,
                     "create_ms": statistics.mean(create_ms),

@@ -465,17 +465,18 @@ int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* 
 }
 
 // One block of device-resident double X (column-major, ld = ldx, even, 16-byte aligned).
-// Path AUTO: chunks of 8 waves of int8 tiles; chunk j is converted to int8 on the conv stream
-// (flagging values that are not integers in [-128, 127]) while chunk j-1 is solved; then the int8
-// kernel and the FP64 kernel are both launched, each gated on the device by the chunk's flag, so
-// exactly one of them does the work and the host never waits.
+// Path AUTO: chunks of up to 8 waves of int8 tiles; chunk j is converted to int8 on the conv stream
+// (flagging values that are not integers in [-128, 127]), issued behind the solve of chunk j-1: its
+// blocks cannot share an SM with a solve CTA (measured: beside one they convert at ~1 GB/s per SM and
+// slow it), so they fill the SMs that kernel's tail frees and then stream at HBM speed on the whole
+// GPU.  Then the int8 kernel and the FP64 kernel are both launched, each gated on the device by the
+// chunk's flag, so exactly one of them does the work and the host never waits.
 int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt) {
   if (c->path == GLS_PATH_FP64 || !c->oz_ok) return run_fp64(c, X, ldx, groups, b, stt, nullptr);
   const int pR = c->pR, p = c->p;
   const int64_t cpt = 4 * (int64_t)((32 / pR) * pR);
-  // chunk j covers groups [bnd[j], bnd[j+1]) and holds min(j+1, 8) waves of tiles: only the first
-  // (short) conversion is exposed, and each later one -- slowed by the running int8 kernel, with
-  // which it shares HBM -- still finishes before the previous chunk's kernel does
+  // chunk j covers groups [bnd[j], bnd[j+1]) and holds min(j+1, 8) waves of tiles: the first
+  // conversion, which nothing can hide, is short
   const int64_t wave_groups = (int64_t)c->num_sms * cpt / pR;
   int64_t chunk_groups = 8 * wave_groups;
   if (chunk_groups > groups) chunk_groups = groups;

@@ -18,22 +18,24 @@
 // ~120x its FP64 DMMA rate.  The data-dependent guard: a block whose X_R is not all integers in
 // [-128, 127] is solved by the FP64 DMMA kernel instead (fused_trsm_gls.cu), decided on the device.
 //
-// Kernel layout (one CTA per SM, persistent over tiles of 128 SNP columns):
-//   warp 0      TMA producer: per stage the X tile (128 columns x 128 K, int8, 4 boxes of 32
-//               columns, 128B swizzle) and the packed T tile (7 digits x 32 z rows x 128 K, int8,
-//               pre-swizzled, one bulk copy), under full/empty mbarriers;
-//   warp 1      MMA issuer: D[128 cols x 224] += X^T[128 x 128] T^T[128 x 224] as 4
-//               tcgen05.mma.kind::i8 (M=128, N=224, K=32) per stage, D double-buffered in TMEM
-//               (2 x 224 of 512 columns); commits free the stage and hand D to the epilogue;
+// Kernel layout (CTA pairs, one CTA per SM, persistent over tiles of 256 SNP columns per pair):
+//   warp 0      TMA producer: per stage the X tile (128 columns x 128 K per CTA, int8, 4 boxes of 32
+//               columns, 128B swizzle) and this CTA's half of the packed digit tiles of TWO row blocks
+//               (a "step"), under full/empty mbarriers;
+//   warp 1      MMA issuer (leader): per stage and row block, 4 tcgen05.mma.cta_group::2.kind::i8
+//               (M=256, N=224, K=32) into that row block's accumulator region of TMEM ([0, 224) and
+//               [256, 480)), so each X chunk is staged once for two row blocks; commits free the stage
+//               and hand the regions to the epilogue;
 //   warps 2-9   epilogue: thread = one SNP column (TMEM lane), half h of the 32 z rows: combine
-//               the 7 digit products into z in FP64, then acc_W += z W~_row, acc_G += z z (Fig. 1
-//               S_BL, b_B, S_BR) -- X~_R never leaves registers.  After the last row block the two
-//               halves are summed in a fixed order and one lane per problem assembles S_i and
-//               solves it by Cholesky with the rank rule of reading A4 (Alg. 5 line 11).
+//               the 7 digit products into z in FP64 (exact int64 partial sums), release the region,
+//               then acc_G += z z over the group (Fig. 1 S_BR); S_BL and b_B come exactly from one
+//               extra MMA pass against the digits of V = M^-1 [X_L | y] (reading A17) -- X~_R never
+//               leaves registers.  After the last step the two halves are summed (through TMEM) in a
+//               fixed order and one lane per problem assembles S_i and solves it by Cholesky with the
+//               rank rule of reading A4 (Alg. 5 line 11).
 #include <cuda.h>
 
 #include <cstdio>
-#include <cstdlib>
 
 #include "gls_internal.cuh"
 #include "umma.cuh"
@@ -53,6 +55,8 @@ constexpr int kBHalf = kBTile / 2;       // 14 KiB staged per CTA of a pair
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = (2 + kEpiWarps) * 32;
 constexpr uint32_t kTmemCols = 512;
+// TMEM column pair of double w in the epilogue hand-over scratch: columns MMAs never write
+__device__ __forceinline__ uint32_t xcol(int w) { return w < 16 ? 224 + 2 * w : 480 + 2 * (w - 16); }
 constexpr uint32_t kIdesc = idesc_i8(256, kBN);  // CTA pair: M = 256
 static_assert(kOzTileBytes == kBTile, "packed T tile size");
 
@@ -146,17 +150,19 @@ __device__ __forceinline__ void timed_wait(uint64_t* bar, uint32_t ph, long long
   }
 }
 
-// K chunk order of row block i: forward on even, reverse on odd row blocks (zig-zag), so each pass
-// over the X panel starts where the previous one ended and re-reads hit L2.  The digit products are
+// K chunk order of step i: forward on even, reverse on odd steps (zig-zag), so each pass over the
+// X panel starts where the previous one ended and re-reads hit L2.  The digit products are
 // exact integers, so the order does not change any bit of the result.
 __device__ __forceinline__ int chunk_at(int i, int nc, int k) { return (i & 1) ? nc - 1 - k : k; }
 
-// One CTA pair (cluster of 2, one CTA per SM of a TPC) computes, per row block of 32 z rows and per
-// 128-row K chunk, D[256 SNP columns x 224] += X^T[256 x 128] T^T[128 x 224] as four
-// tcgen05.mma.cta_group::2.kind::i8 (M = 256, N = 224, K = 32) issued by the leader: each CTA stages
-// its own 128 X columns and half (112 rows) of the packed digit tile, so a stage is 30 KiB per SM and
-// the B operand is shared by the pair.  D lives in TMEM, double-buffered (2 x 224 of 512 columns):
-// CTA r's TMEM lanes hold its own 128 columns.
+// One CTA pair (cluster of 2, one CTA per SM of a TPC) computes, per step (row blocks 2t and 2t+1, 32
+// z rows each) and per 128-row K chunk, D_b[256 SNP columns x 224] += X^T[256 x 128] T_b^T[128 x 224]
+// for both row blocks b, as tcgen05.mma.cta_group::2.kind::i8 (M = 256, N = 224, K = 32) issued by
+// the leader: each CTA stages its own 128 X columns and half (112 rows) of both packed digit tiles,
+// so a stage is 44 KiB per SM and the B operands are shared by the pair.  The two D regions live in
+// TMEM ([0, 224) and [256, 480) of 512 columns; CTA r's lanes hold its own 128 columns) and are
+// released one by one: the next step's region-0 MMAs start as soon as region 0 is drained, its
+// region-1 MMAs are deferred (their stages held) until region 1 is.
 // PL1C: pL + 1 when fixed at compile time (0: runtime); NA: accumulators per column
 // (>= pL + 1 + pR); PR1: pR == 1 (Gram = z^2, no shuffles); ST: pipeline stages.
 template <int PL1C, int NA, bool PR1, int ST>
@@ -166,9 +172,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
-  uint8_t* sB = sA + ST * kATile;
-  double* red = (double*)(sB + ST * kBHalf);  // 128 columns x NA
-  uint64_t* bars = (uint64_t*)(red + 128 * NA);
+  uint8_t* sB = sA + ST * kATile;                  // per stage: two B halves (two row blocks)
+  uint64_t* bars = (uint64_t*)(sB + ST * 2 * kBHalf);
   uint64_t* full = bars;                 // used in the leader: all 60 KiB of a stage landed
   uint64_t* empty = bars + ST;           // both CTAs: the pair's MMAs released the stage
   uint64_t* tfull = bars + 2 * ST;       // both CTAs: accumulator buffer ready for the epilogue
@@ -201,11 +206,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int cpt = 4 * kp.cpw;  // columns per tile (per CTA)
   const Sched sc(kp.num_tiles, (int)rank);
 
+  // Steps: step t of a tile covers row blocks 2t and 2t+1 (the last one alone when NBR is odd); both
+  // have the same K extent, so each X chunk is loaded once and multiplied by both row blocks' digit
+  // tiles, into TMEM columns [0, 224) and [256, 480).  The step after the last is the V block.  The
+  // accumulator region is single-buffered: the next step's MMAs wait until both epilogues drained it.
+  const int nsteps = (kp.NBR + 1) / 2;
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       prefetch_tmap(&xmap);
       prefetch_tmap(&tmap);
+      prefetch_tmap(&vmap);
       int stage = 0;
       uint32_t ph = 0;
       long long tw = 0;
@@ -215,38 +226,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int r = 0; r < sc.rounds; ++r) {
         if (!sc.pair_active(r, kp.num_tiles)) break;
         const int col0 = sc.tile(r) * cpt;
-        for (int i = 0; i < kp.NBR; ++i) {
-          const int nc = (i >> 2) + 1;
-          const int trow0 = (int)(oz_tile_offset(i) * kBN) + (int)rank * (kBN / 2);
+        for (int t = 0; t <= nsteps; ++t) {
+          const bool vstep = t == nsteps;
+          const int i0 = 2 * t;
+          const int nrb = vstep ? 1 : (i0 + 1 < kp.NBR ? 2 : 1);
+          const int nc = vstep ? kp.NC : (i0 >> 2) + 1;
+          const uint32_t bbytes = vstep ? (uint32_t)kp.NV * (kKC / 2) : (uint32_t)nrb * kBHalf;
           for (int k = 0; k < nc; ++k) {
-            const int c = chunk_at(i, nc, k);
+            const int c = chunk_at(t, nc, k);
             timed_wait(&empty[stage], ph ^ 1, pw);
-            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kATile + kBHalf));
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kATile + bbytes));
             const uint32_t fb = full0 + stage * 8;
             const uint64_t pol = c < kp.cpin ? pol_keep : pol_stream;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               tma_2d_g2s_pair_hint(sA + stage * kATile + q * 4096, &xmap, c * kKC, col0 + q * kp.cpw, fb, pol);
-            tma_2d_g2s_pair(sB + stage * kBHalf, &tmap, 0, trow0 + c * kBN, fb);
+            uint8_t* sb = sB + stage * (2 * kBHalf);
+            if (vstep) {
+              tma_2d_g2s_pair(sb, &vmap, 0, c * kp.NV + (int)rank * (kp.NV / 2), fb);
+            } else {
+              for (int sl = 0; sl < nrb; ++sl) {
+                const int trow0 = (int)(oz_tile_offset(i0 + sl) * kBN) + (int)rank * (kBN / 2);
+                tma_2d_g2s_pair(sb + sl * kBHalf, &tmap, 0, trow0 + c * kBN, fb);
+              }
+            }
             if (++stage == ST) {
               stage = 0;
               ph ^= 1;
             }
-          }
-        }
-        // V block: all K chunks against the digits of V = M^{-1} [X_L | y] (-> S_BL, b_B)
-        for (int k = 0; k < kp.NC; ++k) {
-          const int c = chunk_at(kp.NBR, kp.NC, k);
-          timed_wait(&empty[stage], ph ^ 1, pw);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kATile + kp.NV * (kKC / 2)));
-          const uint32_t fb = full0 + stage * 8;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            tma_2d_g2s_pair(sA + stage * kATile + q * 4096, &xmap, c * kKC, col0 + q * kp.cpw, fb);
-          tma_2d_g2s_pair(sB + stage * kBHalf, &vmap, 0, c * kp.NV + (int)rank * (kp.NV / 2), fb);
-          if (++stage == ST) {
-            stage = 0;
-            ph ^= 1;
           }
         }
       }
@@ -257,58 +264,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (leader && lane == 0) {
       int stage = 0;
       uint32_t ph = 0;
-      uint32_t rbc = 0;
+      uint32_t u0 = 0, u1 = 0;  // uses of accumulator regions 0 and 1 so far (barrier phases)
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
       long long twf = 0, twt = 0;
       long long* pf = kp.prof ? &twf : nullptr;
       long long* pt = kp.prof ? &twt : nullptr;
       const long long tstart = clock64();
+      const uint32_t idv = idesc_i8(256, kp.NV);
+      // the 4 K=32 MMAs of stage st (K chunk k of the step) into accumulator region sl
+      auto issue = [&](int st, int k, int sl, uint32_t idesc) {
+        const uint64_t ad = sdesc_k128(a0 + st * kATile);
+        const uint64_t bd = sdesc_k128(b0 + st * (2 * kBHalf) + sl * kBHalf);
+#pragma unroll
+        for (int kk = 0; kk < kKC / 32; ++kk)
+          mma_i8_pair(tbase + sl * 256, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idesc, (k | kk) != 0);
+      };
       for (int r = 0; r < sc.rounds; ++r) {
         if (!sc.pair_active(r, kp.num_tiles)) break;
-        for (int i = 0; i < kp.NBR; ++i, ++rbc) {
-          const int nc = (i >> 2) + 1;
-          const uint32_t buf = rbc & 1, tph = (rbc >> 1) & 1;
-          timed_wait(&tempty[buf], tph ^ 1, pt);
+        for (int t = 0; t <= nsteps; ++t) {
+          const bool vstep = t == nsteps;
+          const int i0 = 2 * t;
+          const bool two = !vstep && i0 + 1 < kp.NBR;
+          const int nc = vstep ? kp.NC : (i0 >> 2) + 1;
+          const uint32_t idesc = vstep ? idv : kIdesc;
+          timed_wait(&tempty[0], (u0++ & 1) ^ 1, pt);
           tc_fence_after();
-          const uint32_t dt = tbase + buf * 256;
+          // Region 1 is drained after region 0 (the epilogue releases them one by one): until it is,
+          // its MMAs are deferred -- the stages stay held -- while region 0's go ahead.
+          bool r1 = !two;
+          int ndef = 0, dstage = 0, dk = 0;
           for (int k = 0; k < nc; ++k) {
             timed_wait(&full[stage], ph, pf);
             tc_fence_after();
-            const uint64_t ad = sdesc_k128(a0 + stage * kATile);
-            const uint64_t bd = sdesc_k128(b0 + stage * kBHalf);
-#pragma unroll
-            for (int kk = 0; kk < kKC / 32; ++kk)
-              mma_i8_pair(dt, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), kIdesc, (k | kk) != 0);
-            mma_commit_pair_mc(&empty[stage], 3);
+            issue(stage, k, 0, idesc);
+            if (r1) {
+              if (two) issue(stage, k, 1, idesc);
+              mma_commit_pair_mc(&empty[stage], 3);
+            } else {
+              if (ndef++ == 0) {
+                dstage = stage;
+                dk = k;
+              }
+              if (ndef == ST - 1 || k == nc - 1 || mbar_test(&tempty[1], (u1 & 1) ^ 1)) {
+                timed_wait(&tempty[1], (u1++ & 1) ^ 1, pt);
+                tc_fence_after();
+                r1 = true;
+                for (int d = 0, s2 = dstage; d < ndef; ++d, s2 = s2 + 1 == ST ? 0 : s2 + 1) {
+                  issue(s2, dk + d, 1, idesc);
+                  mma_commit_pair_mc(&empty[s2], 3);
+                }
+                ndef = 0;
+              }
+            }
             if (++stage == ST) {
               stage = 0;
               ph ^= 1;
             }
           }
-          mma_commit_pair_mc(&tfull[buf], 3);
-        }
-        {  // V block: N = NV
-          const uint32_t buf = rbc & 1, tph = (rbc >> 1) & 1;
-          ++rbc;
-          timed_wait(&tempty[buf], tph ^ 1, pt);
-          tc_fence_after();
-          const uint32_t dt = tbase + buf * 256;
-          const uint32_t idv = idesc_i8(256, kp.NV);
-          for (int k = 0; k < kp.NC; ++k) {
-            timed_wait(&full[stage], ph, pf);
-            tc_fence_after();
-            const uint64_t ad = sdesc_k128(a0 + stage * kATile);
-            const uint64_t bd = sdesc_k128(b0 + stage * kBHalf);
-#pragma unroll
-            for (int kk = 0; kk < kKC / 32; ++kk)
-              mma_i8_pair(dt, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idv, (k | kk) != 0);
-            mma_commit_pair_mc(&empty[stage], 3);
-            if (++stage == ST) {
-              stage = 0;
-              ph ^= 1;
-            }
-          }
-          mma_commit_pair_mc(&tfull[buf], 3);
+          mma_commit_pair_mc(&tfull[0], 3);
         }
       }
       if (kp.prof) {
@@ -321,101 +334,114 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int ew = warp - 2;
     const int q = warp & 3;      // TMEM lane quadrant this warp may access
-    const int h = ew >> 2;       // which 16 of the 32 z rows
-    const int tc = q * 32 + lane;  // column of the CTA's tile held by this thread (TMEM lane)
+    const int h = ew >> 2;       // which 16 of a row block's 32 z rows
     const int pl1 = PL1C > 0 ? PL1C : kp.pL + 1;
     const int as = pl1 + 1;        // aux row stride
     const int a_in = PR1 ? 0 : lane % kp.pR;  // position inside the group
-    const uint32_t trow = tbase + ((uint32_t)(q * 32) << 16) + h * 16;
-    const uint32_t tempty0 = mapa_shared(smem_u32(tempty), 0);  // leader's tempty[0]
+    const uint32_t tlane = tbase + ((uint32_t)(q * 32) << 16);
+    const uint32_t tempty0 = mapa_shared(smem_u32(tempty), 0);  // leader's tempty[0] (tempty[1]: + 8)
     double acc[NA];
     zero_acc(acc);
-    uint32_t rbc = 0;
+    uint32_t stc = 0;
     long long twe = 0, prof_drain = 0, prof_busy = 0;
     long long* pe = (kp.prof && ew == 0 && lane == 0) ? &twe : nullptr;
+    auto release = [&](int sl) {  // this warp is done reading accumulator region sl
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&tempty[sl]);
+        else
+          mbar_arrive_cluster(tempty0 + 8 * sl);
+      }
+    };
+    // z rows 16 h .. 16 h + 15 of the row block in TMEM region `sl`: the 7 digit sums combined exactly
+    // in int64 (two partial sums), then one FP64 rounding each
+    auto drain = [&](int sl, double (&z)[16]) {
+      const uint32_t tr = tlane + sl * 256 + h * 16;
+      long long hi[16], lo[16];
+      int32_t v[16];
+      tmem_ld16(tr, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) hi[r] = (long long)v[r] * 16777216LL;
+      tmem_ld16(tr + 1 * kR, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) hi[r] += (long long)v[r] * 65536LL;
+      tmem_ld16(tr + 2 * kR, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) hi[r] += (long long)v[r] * 256LL;
+      tmem_ld16(tr + 3 * kR, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) hi[r] += (long long)v[r];
+      tmem_ld16(tr + 4 * kR, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) lo[r] = (long long)v[r] * 65536LL;
+      tmem_ld16(tr + 5 * kR, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) lo[r] += (long long)v[r] * 256LL;
+      tmem_ld16(tr + 6 * kR, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) lo[r] += (long long)v[r];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) z[r] = fma((double)hi[r], 16777216.0, (double)lo[r]);
+    };
+    // Gram of z rows of row block i: acc[pl1 + b] += zr z_b over the group's columns (S_BR)
+    auto reduce = [&](int i, const double (&z)[16]) {
+      const double* arow = kp.aux + (int64_t)(i * kR + h * 16) * as;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const double zr = z[r] * __ldg(arow + r * as);
+#pragma unroll
+        for (int w = 0; w < NA; ++w) {
+          if (w < pl1) {
+          } else if (PR1) {
+            if (w == pl1) acc[w] = fma(zr, zr, acc[w]);
+          } else if (w - pl1 < kp.pR) {
+            acc[w] = fma(zr, __shfl_sync(0xffffffffu, zr, lane - a_in + (w - pl1)), acc[w]);
+          }
+        }
+      }
+    };
     for (int rr = 0; rr < sc.rounds; ++rr) {
       if (!sc.pair_active(rr, kp.num_tiles)) break;
       const int tile = sc.tile(rr);
-      for (int i = 0; i < kp.NBR; ++i, ++rbc) {
-        const uint32_t buf = rbc & 1, tph = (rbc >> 1) & 1;
-        timed_wait(&tfull[buf], tph, pe);
+      for (int t = 0; t < nsteps; ++t, ++stc) {
+        const int i0 = 2 * t;
+        const bool two = i0 + 1 < kp.NBR;
+        timed_wait(&tfull[0], stc & 1, pe);
         const long long tw0 = pe ? clock64() : 0;
         tc_fence_after();
-        // z = sum_s 256^(6-s) D_s: digit sums 0..3 and 4..6 combined exactly in int64 (IMAD.WIDE),
-        // then one rounding each into FP64 -- 2 conversions + 1 FMA per z instead of 7 + 6
-        long long hi[16], lo[16];
-        {
-          int32_t v[16];
-          tmem_ld16(trow + buf * 256, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int r = 0; r < 16; ++r) hi[r] = (long long)v[r] * 16777216LL;
-          tmem_ld16(trow + buf * 256 + 1 * kR, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int r = 0; r < 16; ++r) hi[r] += (long long)v[r] * 65536LL;
-          tmem_ld16(trow + buf * 256 + 2 * kR, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int r = 0; r < 16; ++r) hi[r] += (long long)v[r] * 256LL;
-          tmem_ld16(trow + buf * 256 + 3 * kR, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int r = 0; r < 16; ++r) hi[r] += (long long)v[r];
-          tmem_ld16(trow + buf * 256 + 4 * kR, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int r = 0; r < 16; ++r) lo[r] = (long long)v[r] * 65536LL;
-          tmem_ld16(trow + buf * 256 + 5 * kR, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int r = 0; r < 16; ++r) lo[r] += (long long)v[r] * 256LL;
-          tmem_ld16(trow + buf * 256 + 6 * kR, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int r = 0; r < 16; ++r) lo[r] += (long long)v[r];
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader)
-            mbar_arrive(&tempty[buf]);
-          else
-            mbar_arrive_cluster(tempty0 + buf * 8);
-        }
+        // one z block live at a time (fewer registers than draining both first, and measured faster):
+        // region 0's release lets the next step's MMAs start while region 1 is still being read
+        double z[16];
+        drain(0, z);
+        release(0);
         if (pe) prof_drain += clock64() - tw0;
-        const double* arow = kp.aux + (int64_t)(i * kR + h * 16) * as;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const double* a = arow + r * as;
-          const double z = fma((double)hi[r], 16777216.0, (double)lo[r]);
-          const double zr = z * __ldg(a);
-          // Gram only: acc[pl1 + b] += zr * z_b over the group's columns (S_BR); S_BL and b_B come
-          // from the V block.  Static indices only, so acc stays in registers.
-#pragma unroll
-          for (int w = 0; w < NA; ++w) {
-            if (w < pl1) {
-            } else if (PR1) {
-              if (w == pl1) acc[w] = fma(zr, zr, acc[w]);
-            } else if (w - pl1 < kp.pR) {
-              acc[w] = fma(zr, __shfl_sync(0xffffffffu, zr, lane - a_in + (w - pl1)), acc[w]);
-            }
-          }
+        reduce(i0, z);
+        if (two) {
+          drain(1, z);
+          release(1);
+          reduce(i0 + 1, z);
         }
         if (pe) prof_busy += clock64() - tw0;
       }
       {  // V block: S_BL[w] (w < pL) and b_B (w = pL) of this column = 2^-(e_w+48) sum_s 256^(6-s) D[8w+s]
-        const uint32_t buf = rbc & 1, tph = (rbc >> 1) & 1;
-        ++rbc;
-        timed_wait(&tfull[buf], tph, pe);
+        timed_wait(&tfull[0], stc & 1, pe);
+        ++stc;
         tc_fence_after();
         if (h == 0) {
-          const uint32_t tv = tbase + ((uint32_t)(q * 32) << 16) + buf * 256;
 #pragma unroll
           for (int w = 0; w < NA; ++w) {
             if (w < pl1) {
               int32_t v[8];
-              tmem_ld8(tv + 8 * w, v);
+              tmem_ld8(tlane + 8 * w, v);
               tmem_wait_ld();
               const long long vh = (long long)v[0] * 16777216LL + (long long)v[1] * 65536LL +
                                    (long long)v[2] * 256LL + (long long)v[3];
@@ -424,47 +450,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader)
-            mbar_arrive(&tempty[buf]);
-          else
-            mbar_arrive_cluster(tempty0 + buf * 8);
-        }
+        release(0);
       }
-      // ---- per-tile finalisation: sum the two row halves, assemble S_i, posv
+      // ---- per-tile finalisation: sum the two row halves, assemble S_i, posv.  The h = 1 warps hand
+      // their sums over through TMEM columns no MMA writes ([224, 256) and [480, 512)), same lanes.
       named_bar_sync(1, kEpiWarps * 32);
       if (h == 1) {
 #pragma unroll
-        for (int w = 0; w < NA; ++w) red[tc * NA + w] = acc[w];
+        for (int w = 0; w < NA; ++w) tmem_st_f64(tlane + xcol(w), acc[w]);
+        tmem_wait_st();
+        tc_fence_before();
       }
       named_bar_sync(2, kEpiWarps * 32);
       if (h == 0) {
+        tc_fence_after();
 #pragma unroll
-        for (int w = 0; w < NA; ++w) red[tc * NA + w] = acc[w] + red[tc * NA + w];
-        __syncwarp();
+        for (int w = 0; w < NA; ++w) acc[w] += tmem_ld_f64(tlane + xcol(w));
         const int64_t col = (int64_t)tile * cpt + q * kp.cpw + lane;
-        if (lane < kp.cpw && a_in == 0 && col < kp.cols) {
-          const int64_t g = col / kp.pR;
-          const int p = kp.p, pL = kp.pL, pR = kp.pR;
-          double S[400];
-          double rhs[20];
+        const bool owner = lane < kp.cpw && a_in == 0 && col < kp.cols;
+        const int p = kp.p, pL = kp.pL, pR = kp.pR;
+        double S[400];
+        double rhs[20];
+        if (owner) {
           for (int a2 = 0; a2 < pL; ++a2) {
             for (int b2 = 0; b2 < pL; ++b2) S[a2 + b2 * 20] = __ldg(kp.G + a2 + b2 * pl1);
             rhs[a2] = __ldg(kp.G + a2 + pL * pl1);
           }
-          for (int a2 = 0; a2 < pR; ++a2) {
-            const double* rr2 = red + (tc + a2) * NA;
-            for (int k = 0; k < pL; ++k) {
-              S[(pL + a2) + k * 20] = rr2[k];
-              S[k + (pL + a2) * 20] = rr2[k];
-            }
-            rhs[pL + a2] = rr2[pL];
-            for (int b2 = 0; b2 < pR; ++b2) S[(pL + a2) + (pL + b2) * 20] = rr2[pl1 + b2];
-          }
-          posv_store(S, rhs, p, kp.b_out + g * p, kp.status_out ? kp.status_out + g : nullptr);
         }
+        // the group's columns are lanes lane .. lane + pR - 1 of this warp (groups never straddle warps)
+#pragma unroll
+        for (int a2 = 0; a2 < (PR1 ? 1 : 20); ++a2) {
+          if (a2 < pR) {
+#pragma unroll
+            for (int w = 0; w < NA; ++w) {
+              const double v = PR1 ? acc[w] : __shfl_sync(0xffffffffu, acc[w], lane + a2);
+              if (owner) {
+                if (w < pL) {
+                  S[(pL + a2) + w * 20] = v;
+                  S[w + (pL + a2) * 20] = v;
+                }
+                if (w == pL) rhs[pL + a2] = v;
+                if (w >= pl1 && w - pl1 < pR) S[(pL + a2) + (pL + w - pl1) * 20] = v;
+              }
+            }
+          }
+        }
+        if (owner) posv_store(S, rhs, p, kp.b_out + (col / pR) * p, kp.status_out ? kp.status_out + col / pR : nullptr);
       }
       zero_acc(acc);
     }
@@ -634,22 +665,27 @@ __device__ __forceinline__ uint32_t to_i8_bits(double v, int& bad) {
 }
 
 // X (double, column-major, ld = ldx) -> X8 (int8, column-major, ld = ld8), flagging any value that
-// is not an integer in [-128, 127] (NaN included).  One thread per 8 rows of one column (a warp
-// reads 2 KiB contiguous).  Small blocks and few registers on purpose: the pass runs beside the
-// int8 kernel, which leaves only a few thousand registers free per SM sub-partition, and it uses no
-// FP64 arithmetic, which would contend with that kernel's tensor-core work.  X rows start 16-byte
-// aligned (ldx even, base 16-byte aligned).
-// Work-stealing: blocks claim units of kConvCols columns from an atomic counter (work[0], zeroed with
-// the flag), so the few blocks that co-reside with the int8 kernel convert as much as they can and
-// the remainder finishes on the whole GPU the moment that kernel ends.
+// is not an integer in [-128, 127] (NaN included); X8's padding rows [n, ld8) are not written (the
+// solve kernel's TMA reads rows < n only).  Integer bit tests only, no FP64 arithmetic.
+// A warp converts pieces of 256 rows of one column: lane l holds rows 2l, 2l+1 (+64 k, k < 4), so
+// every load instruction reads 512 contiguous bytes and every store writes 64; kInflight pieces are
+// in flight per warp.  X columns start 16-byte aligned (ldx even, base 16-byte aligned).
+// Work-stealing: blocks claim units of kConvCols columns from an atomic counter (work[0], zeroed
+// with the flag).
 constexpr int kConvCols = 16;
-__global__ void __launch_bounds__(64) oz_x_to_i8_kernel(const double* __restrict__ X, int64_t ldx, int64_t n,
-                                                        int64_t cols, int8_t* __restrict__ X8, int64_t ld8,
-                                                        int* __restrict__ flag,
-                                                        unsigned long long* __restrict__ work) {
+constexpr int kConvThreads = 256;
+constexpr int kInflight = 2;  // 256-row pieces in flight per warp
+constexpr int kConvSmem = 8192;
+
+__global__ void __launch_bounds__(kConvThreads, 4) oz_x_to_i8_kernel(const double* __restrict__ X, int64_t ldx,
+                                                                     int64_t n, int64_t cols, int8_t* __restrict__ X8,
+                                                                     int64_t ld8, int* __restrict__ flag,
+                                                                     unsigned long long* __restrict__ work) {
   __shared__ unsigned long long unit;
-  const int64_t per_col = (n + 7) >> 3;
   const int64_t nunits = (cols + kConvCols - 1) / kConvCols;
+  const uint32_t per_col = (uint32_t)((n + 255) >> 8);  // 256-row pieces per column
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = kConvThreads / 32;
   int bad = 0;
   for (;;) {
     if (threadIdx.x == 0) unit = atomicAdd(work, 1ull);
@@ -658,37 +694,42 @@ __global__ void __launch_bounds__(64) oz_x_to_i8_kernel(const double* __restrict
     __syncthreads();
     if (u >= nunits) break;
     const int64_t c0 = u * kConvCols;
-    const int64_t nc = (cols - c0 < kConvCols) ? cols - c0 : kConvCols;
-    for (int64_t o = threadIdx.x; o < per_col * nc; o += blockDim.x) {
-      const int64_t col = c0 + o / per_col;
-      const int64_t r0 = (o % per_col) << 3;
-      const double* src = X + col * ldx + r0;
-      uint32_t w0 = 0, w1 = 0;
-      if (r0 + 8 <= n) {
-        double2 v[4];
+    const uint32_t nc = (cols - c0 < kConvCols) ? (uint32_t)(cols - c0) : (uint32_t)kConvCols;
+    const uint32_t total = per_col * nc;
+    for (uint32_t q0 = warp; q0 < total; q0 += kInflight * kWarps) {
+      double2 v[kInflight][4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = __ldcs((const double2*)src + k);
-        w0 = to_i8_bits(v[0].x, bad) | to_i8_bits(v[0].y, bad) << 8 | to_i8_bits(v[1].x, bad) << 16 |
-             to_i8_bits(v[1].y, bad) << 24;
-        w1 = to_i8_bits(v[2].x, bad) | to_i8_bits(v[2].y, bad) << 8 | to_i8_bits(v[3].x, bad) << 16 |
-             to_i8_bits(v[3].y, bad) << 24;
-      } else {
-        for (int k = 0; r0 + k < n; ++k) {
-          const uint32_t t = to_i8_bits(__ldcs(src + k), bad) << (8 * (k & 3));
-          if (k < 4) w0 |= t; else w1 |= t;
+      for (int j = 0; j < kInflight; ++j) {
+        const uint32_t q = q0 + j * kWarps;
+        const uint32_t c = q / per_col;
+        const int64_t r = (int64_t)(q - c * per_col) * 256;
+        if (q < total && r + 256 <= n) {
+          const double2* src = (const double2*)(X + (c0 + c) * ldx + r) + lane;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[j][k] = __ldcs(src + 32 * k);
         }
       }
-      int8_t* dst = X8 + col * ld8 + r0;
-      if (r0 + 8 <= ld8) {
-        *(uint2*)dst = make_uint2(w0, w1);
-      } else {
-        for (int k = 0; r0 + k < ld8; ++k) dst[k] = (int8_t)((k < 4 ? w0 : w1) >> (8 * (k & 3)));
+#pragma unroll
+      for (int j = 0; j < kInflight; ++j) {
+        const uint32_t q = q0 + j * kWarps;
+        if (q >= total) continue;
+        const uint32_t c = q / per_col;
+        const int64_t r = (int64_t)(q - c * per_col) * 256;
+        const double* src = X + (c0 + c) * ldx + r;
+        int8_t* dst = X8 + (c0 + c) * ld8 + r;
+        if (r + 256 <= n) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            *(uint16_t*)(dst + 2 * lane + 64 * k) =
+                (uint16_t)(to_i8_bits(v[j][k].x, bad) | to_i8_bits(v[j][k].y, bad) << 8);
+        } else {  // the ragged end of the column
+          for (int64_t e = lane; r + e < n; e += 32) dst[e] = (int8_t)to_i8_bits(__ldcs(src + e), bad);
+        }
       }
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
-
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                     const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -709,10 +750,11 @@ PFN_encodeTiled get_encode() {
 template <int PL1C, int NA, bool PR1>
 cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& xmap, const CUtensorMap& tmap,
                               const CUtensorMap& vmap, const OzParams& kp, int num_sms) {
-  constexpr int kFixed = 128 * NA * 8 + 1024 + 512;  // reduction scratch, alignment, barriers
-  constexpr int ST = (232448 - kFixed) / (kATile + kBHalf) < 8 ? (232448 - kFixed) / (kATile + kBHalf) : 8;
+  constexpr int kFixed = 1024 + 512;  // alignment, barriers
+  constexpr int kStage = kATile + 2 * kBHalf;  // X chunk + the digit halves of two row blocks
+  constexpr int ST = (232448 - kFixed) / kStage < 8 ? (232448 - kFixed) / kStage : 8;
   static_assert(ST >= 4, "shared memory budget");
-  constexpr int smem = ST * (kATile + kBHalf) + kFixed;
+  constexpr int smem = ST * kStage + kFixed;
   auto kern = ozaki_trsm_gls_kernel<PL1C, NA, PR1, ST>;
   static int max_pairs_dev[64];  // per device: cluster occupancy of this variant
   int dev = 0;
@@ -762,10 +804,13 @@ void oz_setup(cudaStream_t s, const double* T, int64_t ld, int64_t n, const doub
 void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t cols, int8_t* X8,
                 int64_t ld8, int* flag, unsigned long long* work, int num_sms, int64_t* lc) {
   const int64_t nunits = (cols + kConvCols - 1) / kConvCols;
-  int64_t blocks = (int64_t)num_sms * 32;
+  int64_t blocks = (int64_t)num_sms * 4;
   if (blocks > nunits) blocks = nunits;
   if (blocks < 1) blocks = 1;
-  oz_x_to_i8_kernel<<<(unsigned)blocks, 64, 0, s>>>(X, ldx, n, cols, X8, ld8, flag, work);
+  // kConvSmem of (unused) dynamic shared memory keeps these blocks off SMs that hold an int8 solve
+  // CTA: placed beside one they would convert at ~1 GB/s per SM and slow it down, while on the
+  // whole GPU (the tail of each solve kernel onwards) the pass streams at HBM speed
+  oz_x_to_i8_kernel<<<(unsigned)blocks, kConvThreads, kConvSmem, s>>>(X, ldx, n, cols, X8, ld8, flag, work);
   if (lc) ++*lc;
 }
 

@@ -1,5 +1,5 @@
 """A/B timing of the config-2 solve with a given libgls.so (diagnostics): only symbols every round-1
-build exports.  usage: python tools/ab_solve.py LIB [m]"""
+build exports.  usage: python tools/ab_solve.py LIB [m] [config]"""
 import ctypes, os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -17,22 +17,23 @@ lib.gls_set_timing.argtypes = [vp, i32]
 dpp = ctypes.POINTER(ctypes.c_double)
 lib.gls_read_timing.argtypes = [vp, dpp, dpp, dpp, ctypes.POINTER(i64)]
 lib.gls_destroy.argtypes = [vp]
-cfg = gen.CONFIGS[2]
+cfg = gen.CONFIGS[int(sys.argv[3]) if len(sys.argv) > 3 else 2]
 n = cfg.n
 P = gen.config_problem(cfg)
 d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
 Md, XLd, yd = d(P.M), d(P.XL), d(P.y)
-X = torch.empty((m, n), dtype=torch.float64, device="cuda")
-for c in range(0, m, 65536):
-    k = min(65536, m - c)
+pL, pR = cfg.pL, cfg.pR
+X = torch.empty((m * pR, n), dtype=torch.float64, device="cuda")
+for c in range(0, m * pR, 65536):
+    k = min(65536, m * pR - c)
     g.gen_xr_device(gen.DEFAULT_SEED, n, c, k, X[c:c + k])
-b = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+b = torch.empty((m, pL + pR), dtype=torch.float64, device="cuda")
 s = torch.cuda.Stream()
 for rep in range(4):
     h = vp()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    assert lib.gls_create(n, 3, 1, Md.data_ptr(), XLd.data_ptr(), yd.data_ptr(), ctypes.byref(h)) == 0
+    assert lib.gls_create(n, pL, pR, Md.data_ptr(), XLd.data_ptr(), yd.data_ptr(), ctypes.byref(h)) == 0
     t1 = time.perf_counter()
     lib.gls_set_stream(h, s.cuda_stream)
     lib.gls_set_timing(h, 1)
