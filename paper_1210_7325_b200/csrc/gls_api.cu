@@ -74,6 +74,7 @@ struct gls_ctx {
   uint64_t oseq = 0;
   // host int8 staging (gls_solve_block_i8 with a host or unaligned source)
   int8_t* stage8[2] = {nullptr, nullptr};
+  int8_t* raw8[2] = {nullptr, nullptr};  // when ld8 != n: rows of n bytes as they arrive, repacked to ld8
   int64_t stage8_cols = 0;
   // optional per-launch timing of the hot kernels (gls_set_timing): event pairs on the launch stream
   bool timing = false;
@@ -583,10 +584,15 @@ int ensure_stage8(gls_ctx* c, int64_t cols) {
   const int64_t ld8 = (c->n + 15) & ~(int64_t)15;
   if (c->stage8_cols >= cols && c->ld8 == ld8) return GLS_OK;
   CK(c, cudaDeviceSynchronize());
-  dfree(c, c->stage8[0]);
-  dfree(c, c->stage8[1]);
+  for (int k = 0; k < 2; ++k) {
+    dfree(c, c->stage8[k]);
+    dfree(c, c->raw8[k]);
+  }
   c->stage8_cols = 0;
-  for (int k = 0; k < 2; ++k) CK(c, dalloc(c, &c->stage8[k], (size_t)ld8 * cols));
+  for (int k = 0; k < 2; ++k) {
+    CK(c, dalloc(c, &c->stage8[k], (size_t)ld8 * cols));
+    if (ld8 != c->n) CK(c, dalloc(c, &c->raw8[k], (size_t)c->n * cols));
+  }
   CK(c, cudaStreamSynchronize(c->own_stream));
   c->stage8_cols = cols;
   c->ld8 = ld8;
@@ -622,11 +628,22 @@ int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, d
     const int64_t gc = (m_blk - g0 < chunk_groups) ? m_blk - g0 : chunk_groups;
     const int buf = (int)(c->seq++ & 1);
     CK(c, cudaStreamWaitEvent(c->h2d, c->ev_comp[buf], 0));
-    CK(c, cudaMemcpy2DAsync(c->stage8[buf], c->ld8, G + (size_t)g0 * pR * ldg, ldg, n, gc * pR,
-                            cudaMemcpyDefault, c->h2d));
+    // contiguous rows whose length is not a multiple of 16 bytes (the TMA row pitch): one linear copy
+    // (a pitched copy of short rows runs at a fraction of the link rate), repacked on the device
+    const bool repack = ldg == n && c->ld8 != n;
+    if (repack)
+      CK(c, cudaMemcpyAsync(c->raw8[buf], G + (size_t)g0 * pR * ldg, (size_t)gc * pR * n, cudaMemcpyDefault,
+                            c->h2d));
+    else
+      CK(c, cudaMemcpy2DAsync(c->stage8[buf], c->ld8, G + (size_t)g0 * pR * ldg, ldg, n, gc * pR,
+                              cudaMemcpyDefault, c->h2d));
     CK(c, cudaEventRecord(c->ev_h2d[buf], c->h2d));
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d[buf], 0));
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_d2h[buf], 0));
+    if (repack) {
+      oz_repack_rows(c->stream, c->raw8[buf], n, gc * pR, c->stage8[buf], c->ld8, &c->launches);
+      CK(c, cudaGetLastError());
+    }
     double* bdst = b_dev ? b_out + (size_t)g0 * p : c->bstage[buf];
     int32_t* sdst = status_out ? (s_dev ? status_out + g0 : c->sstage[buf]) : nullptr;
     rc = run_int8(c, c->stage8[buf], c->ld8, gc, bdst, sdst, nullptr);
@@ -901,8 +918,10 @@ void gls_destroy(gls_ctx* c) {
   dfree(c, c->x8[1]);
   dfree(c, c->flags);
   dfree(c, c->ran);
-  dfree(c, c->stage8[0]);
-  dfree(c, c->stage8[1]);
+  for (int k = 0; k < 2; ++k) {
+    dfree(c, c->stage8[k]);
+    dfree(c, c->raw8[k]);
+  }
   for (auto& x : c->tl) {
     cudaEventDestroy(x.a);
     cudaEventDestroy(x.b);

@@ -152,6 +152,9 @@ struct OzArgs {
   double* b_out;
   int32_t* status_out;
 };
+// rows of n int8 codes packed back to back -> the same rows at pitch ld8 (>= n); padding untouched
+void oz_repack_rows(cudaStream_t s, const int8_t* src, int64_t n, int64_t rows, int8_t* dst, int64_t ld8,
+                    int64_t* launch_counter);
 cudaError_t launch_ozaki_gls(cudaStream_t s, const OzArgs& a, int num_sms, std::string* msg,
                              int64_t* launch_counter);
 

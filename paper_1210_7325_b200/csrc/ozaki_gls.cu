@@ -780,6 +780,12 @@ cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& xmap, const CUt
   return cudaGetLastError();
 }
 
+__global__ void __launch_bounds__(256) oz_repack_kernel(const int8_t* __restrict__ src, int64_t n, int64_t rows,
+                                                        int8_t* __restrict__ dst, int64_t ld8) {
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x)
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) dst[r * ld8 + j] = src[r * n + j];
+}
+
 }  // namespace
 
 int64_t oz_total_tiles(int64_t NBR) { return oz_tile_offset(NBR); }
@@ -799,6 +805,14 @@ void oz_setup(cudaStream_t s, const double* T, int64_t ld, int64_t n, const doub
   oz_vscale_kernel<<<pl1, 256, 0, s>>>(V, n, escale, vscale);
   oz_vpack_kernel<<<(unsigned)oz_nchunks(n), 256, 0, s>>>(V, n, pl1, escale, oz_nv(pl1), V8);
   if (lc) *lc += 5;
+}
+
+void oz_repack_rows(cudaStream_t s, const int8_t* src, int64_t n, int64_t rows, int8_t* dst, int64_t ld8,
+                    int64_t* lc) {
+  if (rows <= 0) return;
+  const int64_t blocks = rows < 148 * 16 ? rows : 148 * 16;
+  oz_repack_kernel<<<(unsigned)blocks, 256, 0, s>>>(src, n, rows, dst, ld8);
+  if (lc) ++*lc;
 }
 
 void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t cols, int8_t* X8,
