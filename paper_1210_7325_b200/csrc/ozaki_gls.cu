@@ -646,22 +646,18 @@ __global__ void oz_aux_w_kernel(const double* __restrict__ W, int64_t ldw, int64
 // x -> int8 bits for an integer-valued double in [-128, 127], by integer operations on its bits only
 // (FP64 arithmetic contends with the tensor core on this part); bad |= any other value.
 __device__ __forceinline__ uint32_t to_i8_bits(double v, int& bad) {
-  const long long b = __double_as_longlong(v);
-  const long long a = b & 0x7fffffffffffffffLL;
-  const int e = (int)(a >> 52);  // biased exponent
-  uint32_t mag = 0;
-  if (a != 0) {
-    if (e >= 1023 && e <= 1030) {
-      const int sh = 52 - (e - 1023);  // 45 .. 52
-      const long long mant = (a & 0xfffffffffffffLL) | (1LL << 52);
-      bad |= (mant & ((1LL << sh) - 1)) != 0;  // a fractional part
-      mag = (uint32_t)(mant >> sh);           // 1 .. 255
-      bad |= mag > (b < 0 ? 128u : 127u);
-    } else {
-      bad = 1;  // 0 < |v| < 1, |v| >= 256, inf, NaN
-    }
-  }
-  return (b < 0 ? (0u - mag) : mag) & 0xffu;
+  // 32-bit integer tests on the two words of v: an integer 1 <= |v| <= 255 has biased exponent
+  // 1023 + k (k <= 7), its integer part in the top k of the high word's 20 mantissa bits and nothing
+  // below (the low word and the high word's low 20 - k bits are zero)
+  const uint32_t hi = (uint32_t)__double2hiint(v), lo = (uint32_t)__double2loint(v);
+  const uint32_t a = hi & 0x7fffffffu;
+  const uint32_t k = (a >> 20) - 1023u;  // wraps for |v| < 1
+  const bool zero = (a | lo) == 0u;
+  const bool ok = k <= 7u && lo == 0u && (a & ((0x100000u >> (k & 7u)) - 1u)) == 0u;
+  const uint32_t mag = ((a & 0xfffffu) | 0x100000u) >> (20u - (k & 7u));  // 1 .. 255 when ok
+  const bool neg = (hi >> 31) != 0u;
+  bad |= !zero && (!ok || mag > (neg ? 128u : 127u));  // 0 < |v| < 1, fractions, |v| >= 128/256, inf, NaN
+  return zero ? 0u : ((neg ? (0u - mag) : mag) & 0xffu);
 }
 
 // X (double, column-major, ld = ldx) -> X8 (int8, column-major, ld = ld8), flagging any value that
