@@ -211,6 +211,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // tiles, into TMEM columns [0, 224) and [256, 480).  The step after the last is the V block.  The
   // accumulator region is single-buffered: the next step's MMAs wait until both epilogues drained it.
   const int nsteps = (kp.NBR + 1) / 2;
+  // Split completion (light epilogues): region 0 gets its own tfull commit and the MMAs of region 1's
+  // last ST-1 stages are deferred on purpose, so region 0's drain overlaps region 1's tail MMAs and the
+  // next step's region-0 MMAs queue behind that tail.  Measured +1 % on config 2; the heavy-epilogue
+  // variants (NA = 21) lose 1 % with it and keep one commit per step.
+  constexpr bool kSplit = NA <= 8;
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
@@ -290,14 +295,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           timed_wait(&tempty[0], (u0++ & 1) ^ 1, pt);
           tc_fence_after();
           // Region 1 is drained after region 0 (the epilogue releases them one by one): until it is,
-          // its MMAs are deferred -- the stages stay held -- while region 0's go ahead.
+          // its MMAs are deferred -- the stages stay held -- while region 0's go ahead (and, with
+          // kSplit, again over the step's last ST-1 stages).
           bool r1 = !two;
           int ndef = 0, dstage = 0, dk = 0;
           for (int k = 0; k < nc; ++k) {
             timed_wait(&full[stage], ph, pf);
             tc_fence_after();
             issue(stage, k, 0, idesc);
-            if (r1) {
+            if (k == nc - 1 && (kSplit || !two)) mma_commit_pair_mc(&tfull[0], 3);  // region 0 complete
+            const bool hold = two && (!r1 || (kSplit && k >= nc - (ST - 1)));
+            if (!hold) {
               if (two) issue(stage, k, 1, idesc);
               mma_commit_pair_mc(&empty[stage], 3);
             } else {
@@ -305,10 +313,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 dstage = stage;
                 dk = k;
               }
-              if (ndef == ST - 1 || k == nc - 1 || mbar_test(&tempty[1], (u1 & 1) ^ 1)) {
-                timed_wait(&tempty[1], (u1++ & 1) ^ 1, pt);
-                tc_fence_after();
-                r1 = true;
+              const bool late = kSplit && k >= nc - (ST - 1);  // the tail: flush only when forced
+              if (ndef == ST - 1 || k == nc - 1 || (!late && mbar_test(&tempty[1], (u1 & 1) ^ 1))) {
+                if (!r1) {
+                  timed_wait(&tempty[1], (u1++ & 1) ^ 1, pt);
+                  tc_fence_after();
+                  r1 = true;
+                }
                 for (int d = 0, s2 = dstage; d < ndef; ++d, s2 = s2 + 1 == ST ? 0 : s2 + 1) {
                   issue(s2, dk + d, 1, idesc);
                   mma_commit_pair_mc(&empty[s2], 3);
@@ -321,7 +332,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               ph ^= 1;
             }
           }
-          mma_commit_pair_mc(&tfull[0], 3);
+          if (two) mma_commit_pair_mc(&tfull[kSplit ? 1 : 0], 3);  // region 1 (and, unsplit, 0) complete
         }
       }
       if (kp.prof) {
@@ -342,7 +353,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty), 0);  // leader's tempty[0] (tempty[1]: + 8)
     double acc[NA];
     zero_acc(acc);
-    uint32_t stc = 0;
+    uint32_t f0 = 0, f1 = 0;  // completions of tfull[0] / tfull[1] consumed (barrier phases)
     long long twe = 0, prof_drain = 0, prof_busy = 0;
     long long* pe = (kp.prof && ew == 0 && lane == 0) ? &twe : nullptr;
     auto release = [&](int sl) {  // this warp is done reading accumulator region sl
@@ -412,20 +423,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int rr = 0; rr < sc.rounds; ++rr) {
       if (!sc.pair_active(rr, kp.num_tiles)) break;
       const int tile = sc.tile(rr);
-      for (int t = 0; t < nsteps; ++t, ++stc) {
+      for (int t = 0; t < nsteps; ++t) {
         const int i0 = 2 * t;
         const bool two = i0 + 1 < kp.NBR;
-        timed_wait(&tfull[0], stc & 1, pe);
+        timed_wait(&tfull[0], f0++ & 1, pe);
         const long long tw0 = pe ? clock64() : 0;
         tc_fence_after();
-        // one z block live at a time (fewer registers than draining both first, and measured faster):
-        // region 0's release lets the next step's MMAs start while region 1 is still being read
+        // one z block live at a time; each region is waited for, drained and released on its own:
+        // region 0 completes first and its release lets the next step's MMAs start while region 1's
+        // last MMAs still run
         double z[16];
         drain(0, z);
         release(0);
         if (pe) prof_drain += clock64() - tw0;
         reduce(i0, z);
         if (two) {
+          if (kSplit) {
+            timed_wait(&tfull[1], f1++ & 1, pe);
+            tc_fence_after();
+          }
           drain(1, z);
           release(1);
           reduce(i0 + 1, z);
@@ -433,8 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (pe) prof_busy += clock64() - tw0;
       }
       {  // V block: S_BL[w] (w < pL) and b_B (w = pL) of this column = 2^-(e_w+48) sum_s 256^(6-s) D[8w+s]
-        timed_wait(&tfull[0], stc & 1, pe);
-        ++stc;
+        timed_wait(&tfull[0], f0++ & 1, pe);
         tc_fence_after();
         if (h == 0) {
 #pragma unroll
