@@ -403,19 +403,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int r = 0; r < 16; ++r) z[r] = fma((double)hi[r], 16777216.0, (double)lo[r]);
     };
-    // Gram of z rows of row block i: acc[pl1 + b] += zr z_b over the group's columns (S_BR)
+    // acc layout: the Gram row at the bottom, acc[b] (b < pR), the V block's outputs at the top,
+    // acc[NA - 1 - w] (w < pL + 1): static register indices for both whatever pL and pR are.
+    // Gram of z rows of row block i: acc[b] += zr z_b over the group's columns (S_BR, row a_in)
     auto reduce = [&](int i, const double (&z)[16]) {
       const double* arow = kp.aux + (int64_t)(i * kR + h * 16) * as;
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const double zr = z[r] * __ldg(arow + r * as);
+        if (PR1) {
+          acc[0] = fma(zr, zr, acc[0]);
+        } else {
 #pragma unroll
-        for (int w = 0; w < NA; ++w) {
-          if (w < pl1) {
-          } else if (PR1) {
-            if (w == pl1) acc[w] = fma(zr, zr, acc[w]);
-          } else if (w - pl1 < kp.pR) {
-            acc[w] = fma(zr, __shfl_sync(0xffffffffu, zr, lane - a_in + (w - pl1)), acc[w]);
+          for (int b = 0; b < NA; ++b) {
+            if (b >= kp.pR) break;  // uniform
+            acc[b] = fma(zr, __shfl_sync(0xffffffffu, zr, lane - a_in + b), acc[b]);
           }
         }
       }
@@ -461,7 +463,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const long long vh = (long long)v[0] * 16777216LL + (long long)v[1] * 65536LL +
                                    (long long)v[2] * 256LL + (long long)v[3];
               const long long vl = (long long)v[4] * 65536LL + (long long)v[5] * 256LL + (long long)v[6];
-              acc[w] = fma((double)vh, 16777216.0, (double)vl) * __ldg(kp.vscale + w);
+              acc[NA - 1 - w] = fma((double)vh, 16777216.0, (double)vl) * __ldg(kp.vscale + w);
             }
           }
         }
@@ -500,12 +502,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int w = 0; w < NA; ++w) {
               const double v = PR1 ? acc[w] : __shfl_sync(0xffffffffu, acc[w], lane + a2);
               if (owner) {
-                if (w < pL) {
-                  S[(pL + a2) + w * 20] = v;
-                  S[w + (pL + a2) * 20] = v;
+                if (w < pR) S[(pL + a2) + (pL + w) * 20] = v;  // S_BR
+                const int wv = NA - 1 - w;                      // V output wv: S_BL (wv < pL), b_B
+                if (wv < pL) {
+                  S[(pL + a2) + wv * 20] = v;
+                  S[wv + (pL + a2) * 20] = v;
                 }
-                if (w == pL) rhs[pL + a2] = v;
-                if (w >= pl1 && w - pl1 < pR) S[(pL + a2) + (pL + w - pl1) * 20] = v;
+                if (wv == pL) rhs[pL + a2] = v;
               }
             }
           }
