@@ -396,19 +396,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // acc layout: the Gram row at the bottom, acc[b] (b < pR), the V block's outputs at the top,
     // acc[NA - 1 - w] (w < pL + 1): static register indices for both whatever pL and pR are.
     // Gram of z rows of row block i: acc[b] += zr z_b over the group's columns (S_BR, row a_in)
-    auto reduce = [&](int i, const double (&z)[16]) {
-      const double* arow = kp.aux + (int64_t)(i * kR + h * 16) * as;
+    // sigma of the warp's 16 rows of row block i, lane r holding row r: loaded before the step's
+    // TMEM wait (a global load from an SM running this kernel takes microseconds), broadcast below
+    auto load_sigma = [&](int i) -> double {
+      return lane < 16 ? __ldg(kp.aux + (int64_t)(i * kR + h * 16 + lane) * as) : 0.0;
+    };
+    auto reduce = [&](double sig, double (&z)[16]) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const double zr = z[r] * __ldg(arow + r * as);
-        if (PR1) {
-          acc[0] = fma(zr, zr, acc[0]);
-        } else {
+      for (int r = 0; r < 16; ++r) z[r] *= __shfl_sync(0xffffffffu, sig, r);
+      if (PR1) {
 #pragma unroll
-          for (int b = 0; b < NA; ++b) {
-            if (b >= kp.pR) break;  // uniform
-            acc[b] = fma(zr, __shfl_sync(0xffffffffu, zr, lane - a_in + b), acc[b]);
-          }
+        for (int r = 0; r < 16; ++r) acc[0] = fma(z[r], z[r], acc[0]);
+      } else {
+        // b outside, rows inside: 16 independent shuffle + FMA chains per b (the rows' order per
+        // accumulator is unchanged)
+#pragma unroll
+        for (int b = 0; b < NA; ++b) {
+          if (b >= kp.pR) break;  // uniform
+#pragma unroll
+          for (int r = 0; r < 16; ++r)
+            acc[b] = fma(z[r], __shfl_sync(0xffffffffu, z[r], lane - a_in + b), acc[b]);
         }
       }
     };
@@ -418,6 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int t = 0; t < nsteps; ++t) {
         const int i0 = 2 * t;
         const bool two = i0 + 1 < kp.NBR;
+        const double sig0 = load_sigma(i0), sig1 = two ? load_sigma(i0 + 1) : 0.0;
         timed_wait(&tfull[0], f0++ & 1, pe);
         const long long tw0 = pe ? clock64() : 0;
         tc_fence_after();
@@ -428,7 +436,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         drain(0, z);
         release(0);
         if (pe) prof_drain += clock64() - tw0;
-        reduce(i0, z);
+        reduce(sig0, z);
         if (two) {
           if (kSplit) {
             timed_wait(&tfull[1], f1++ & 1, pe);
@@ -436,7 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           drain(1, z);
           release(1);
-          reduce(i0 + 1, z);
+          reduce(sig1, z);
         }
         if (pe) prof_busy += clock64() - tw0;
       }
