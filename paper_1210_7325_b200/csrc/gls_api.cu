@@ -66,6 +66,8 @@ struct gls_ctx {
   // int8 conversion workspaces (two, swapping roles) and their rejection flags
   cudaStream_t conv = nullptr;
   int64_t x8_cols = 0, ld8 = 0;
+  double* sws = nullptr;     // per-problem records for the separate posv of large p (OzArgs::s_ws)
+  int64_t sws_groups = 0;
   int8_t* x8[2] = {nullptr, nullptr};
   int* flags = nullptr;                  // 2 ints, then (8-byte aligned) 2 work counters
   unsigned long long* ran = nullptr;     // [0] int8 kernel launches that ran, [1] FP64 ones
@@ -438,6 +440,14 @@ int ensure_x8(gls_ctx* c, int64_t cols) {
 
 int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* b, int32_t* stt,
              const int* gate) {
+  if (c->p > kOzPosvInKernelMaxP && c->sws_groups < groups) {
+    CK(c, cudaDeviceSynchronize());
+    dfree(c, c->sws);
+    c->sws_groups = 0;
+    CK(c, dalloc(c, &c->sws, (size_t)groups * c->pR * (c->p + 1) * sizeof(double)));
+    CK(c, cudaStreamSynchronize(c->own_stream));
+    c->sws_groups = groups;
+  }
   LaunchTimer lt(c, c->stream, 0);
   OzArgs a;
   a.X8 = X8;
@@ -455,6 +465,7 @@ int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* 
   a.vscale = c->vscale;
   a.b_out = b;
   a.status_out = stt;
+  a.s_ws = c->p > kOzPosvInKernelMaxP ? c->sws : nullptr;
   std::string msg;
   cudaError_t e = launch_ozaki_gls(c->stream, a, c->num_sms, &msg, &c->launches);
   if (e != cudaSuccess) {
@@ -916,6 +927,7 @@ void gls_destroy(gls_ctx* c) {
   dfree(c, c->vscale);
   dfree(c, c->x8[0]);
   dfree(c, c->x8[1]);
+  dfree(c, c->sws);
   dfree(c, c->flags);
   dfree(c, c->ran);
   for (int k = 0; k < 2; ++k) {

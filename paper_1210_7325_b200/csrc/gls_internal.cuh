@@ -151,7 +151,10 @@ struct OzArgs {
   const double* vscale;
   double* b_out;
   int32_t* status_out;
+  double* s_ws;         // nullable: m_blk records of pR (pL + pR + 1) doubles; when set, the kernel
+                        // stores S_BL, S_BR, b_B there and a batched posv kernel solves (large p)
 };
+constexpr int kOzPosvInKernelMaxP = 8;  // p above this: posv in a separate kernel (oz s_ws)
 // rows of n int8 codes packed back to back -> the same rows at pitch ld8 (>= n); padding untouched
 void oz_repack_rows(cudaStream_t s, const int8_t* src, int64_t n, int64_t rows, int8_t* dst, int64_t ld8,
                     int64_t* launch_counter);

@@ -80,6 +80,7 @@ struct OzParams {
   int cpin;             // X chunks c < cpin are loaded L2::evict_last (they are re-read by every row
                         // block of the tile), the others evict_first
   const double* vscale; // pL+1 column scales 2^-(e_w+48) of V = M^{-1} [X_L | y]
+  double* s_ws;         // nullable: per problem S_BL (pR x pL), S_BR (pR x pR), b_B (pR) for oz_posv_kernel
 };
 
 template <int NA>
@@ -486,7 +487,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int p = kp.p, pL = kp.pL, pR = kp.pR;
         double S[400];
         double rhs[20];
-        if (owner) {
+        // large p: the record goes to global memory and oz_posv_kernel solves after this kernel (a
+        // 20 x 20 Cholesky in local memory here would stall the next tile's first step)
+        double* rec = kp.s_ws ? kp.s_ws + (col / pR) * (int64_t)(pR * (pL + pR + 1)) : nullptr;
+        if (owner && !rec) {
           for (int a2 = 0; a2 < pL; ++a2) {
             for (int b2 = 0; b2 < pL; ++b2) S[a2 + b2 * 20] = __ldg(kp.G + a2 + b2 * pl1);
             rhs[a2] = __ldg(kp.G + a2 + pL * pl1);
@@ -499,7 +503,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int w = 0; w < NA; ++w) {
               const double v = PR1 ? acc[w] : __shfl_sync(0xffffffffu, acc[w], lane + a2);
-              if (owner) {
+              if (owner && rec) {
+                if (w < pR) rec[pR * pL + a2 * pR + w] = v;
+                const int wv = NA - 1 - w;
+                if (wv < pL) rec[a2 * pL + wv] = v;
+                if (wv == pL) rec[pR * pL + pR * pR + a2] = v;
+              } else if (owner) {
                 if (w < pR) S[(pL + a2) + (pL + w) * 20] = v;  // S_BR
                 const int wv = NA - 1 - w;                      // V output wv: S_BL (wv < pL), b_B
                 if (wv < pL) {
@@ -511,7 +520,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (owner) posv_store(S, rhs, p, kp.b_out + (col / pR) * p, kp.status_out ? kp.status_out + col / pR : nullptr);
+        if (owner && !rec)
+          posv_store(S, rhs, p, kp.b_out + (col / pR) * p, kp.status_out ? kp.status_out + col / pR : nullptr);
       }
       zero_acc(acc);
     }
@@ -792,6 +802,34 @@ cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& xmap, const CUt
   return cudaGetLastError();
 }
 
+// Alg. 5 line 11 for the records the int8 kernel left in s_ws (large p): S_i = [[S_TL, S_BL^T],
+// [S_BL, S_BR]], [b_T; b_B] with S_TL, b_T from G, then the same posv_store as in the kernel.
+__global__ void __launch_bounds__(128) oz_posv_kernel(const double* __restrict__ rec, const double* __restrict__ G,
+                                                      int pL, int pR, int64_t m_blk, const int* gate,
+                                                      double* __restrict__ b_out, int32_t* __restrict__ st) {
+  if (gate && *(volatile const int*)gate != 0) return;
+  const int p = pL + pR, pl1 = pL + 1;
+  const int64_t rs = (int64_t)pR * (pL + pR + 1);
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < m_blk; g += (int64_t)gridDim.x * blockDim.x) {
+    double S[400];
+    double rhs[20];
+    for (int a2 = 0; a2 < pL; ++a2) {
+      for (int b2 = 0; b2 < pL; ++b2) S[a2 + b2 * 20] = G[a2 + b2 * pl1];
+      rhs[a2] = G[a2 + pL * pl1];
+    }
+    const double* r = rec + g * rs;
+    for (int a2 = 0; a2 < pR; ++a2) {
+      for (int w = 0; w < pL; ++w) {
+        S[(pL + a2) + w * 20] = r[a2 * pL + w];
+        S[w + (pL + a2) * 20] = r[a2 * pL + w];
+      }
+      for (int b2 = 0; b2 < pR; ++b2) S[(pL + a2) + (pL + b2) * 20] = r[pR * pL + a2 * pR + b2];
+      rhs[pL + a2] = r[pR * pL + pR * pR + a2];
+    }
+    posv_store(S, rhs, p, b_out + g * p, st ? st + g : nullptr);
+  }
+}
+
 __global__ void __launch_bounds__(256) oz_repack_kernel(const int8_t* __restrict__ src, int64_t n, int64_t rows,
                                                         int8_t* __restrict__ dst, int64_t ld8) {
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x)
@@ -882,6 +920,7 @@ cudaError_t launch_ozaki_gls(cudaStream_t s, const OzArgs& a, int num_sms, std::
   }
   kp.b_out = a.b_out;
   kp.status_out = a.status_out;
+  kp.s_ws = a.s_ws;
   kp.cols = cols;
   kp.m_blk = a.m_blk;
   const int64_t cpt = 4 * (int64_t)cpw;
@@ -936,6 +975,13 @@ cudaError_t launch_ozaki_gls(cudaStream_t s, const OzArgs& a, int num_sms, std::
   else
     e = launch_oz_variant<0, 21, false>(s, map, tmap, vmap, kp, num_sms);
   if (lc) ++*lc;
+  if (e == cudaSuccess && a.s_ws) {
+    const int64_t blocks = (a.m_blk + 127) / 128 < 4 * num_sms ? (a.m_blk + 127) / 128 : 4 * num_sms;
+    oz_posv_kernel<<<(unsigned)blocks, 128, 0, s>>>(a.s_ws, a.G, a.pL, a.pR, a.m_blk, a.gate, a.b_out,
+                                                    a.status_out);
+    e = cudaGetLastError();
+    if (lc) ++*lc;
+  }
   if (e != cudaSuccess && msg) *msg = std::string("ozaki_trsm_gls launch: ") + cudaGetErrorString(e);
   if (prof_on && e == cudaSuccess) {
     long long h[8 * 1024];
