@@ -141,7 +141,9 @@ bool is_device_ptr(const void* p) {
 
 // Device memory comes from the device's stream-ordered pool (cudaMallocAsync on the context's own
 // stream); freed blocks stay cached in the pool (release threshold GLS_POOL_KEEP_BYTES, default
-// 8 GiB) so a create/destroy cycle does not pay cudaMalloc/cudaFree page mapping every time.
+// 32 GiB -- the two FP64 host staging buffers alone are 12 GB at n = 1e4) so a create/destroy cycle
+// does not pay page unmapping and remapping every time (measured: with 8 GiB, destroying a context
+// after a FP64 host-input solve took 0.3-3.6 s and the next solve's first touch ~0.7 s more).
 void configure_pool(int device) {
   static bool done = false;
   if (done) return;
@@ -151,7 +153,7 @@ void configure_pool(int device) {
     cudaGetLastError();
     return;
   }
-  uint64_t keep = 8ull << 30;
+  uint64_t keep = 32ull << 30;
   if (const char* e = getenv("GLS_POOL_KEEP_BYTES")) keep = strtoull(e, nullptr, 10);
   cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   cudaGetLastError();
