@@ -149,6 +149,12 @@ int gls_read_timing(gls_ctx* ctx, double* ms_int8, double* ms_fp64, double* ms_c
 /* gls_get_dims -- n, pL, pR of a context (any state but NULL). */
 int gls_get_dims(const gls_ctx* ctx, int64_t* n, int32_t* pL, int32_t* pR);
 
+/* gls_release_cached_memory -- return the device memory that destroyed contexts left cached in the
+ * current device's stream-ordered pool (up to GLS_POOL_KEEP_BYTES, default 32 GiB, is kept so that
+ * create/destroy cycles do not remap pages) to the driver, e.g. before a large allocation by another
+ * allocator.  Synchronises the device.  Returns GLS_OK or GLS_ERR_CUDA. */
+int gls_release_cached_memory(void);
+
 /* ---- Out-of-core from secondary storage (§4; NEXT-1 / NEXT-4 of SURVEY §8(f)).
  * gls_solve_file streams the X_R of m problems from a file, in blocks of problems, and writes the b
  * records (m x p doubles, record i at byte 8 p i) and optionally the int32 statuses to files.

@@ -4,4 +4,4 @@
 in-tree CUDA libraries for sm_100a.  See DESIGN.md.
 """
 from .gls import (GLS_OOC_ASYNC, GLS_OOC_SYNC, GLS_PATH_AUTO, GLS_PATH_FP64, Context, GLSError,  # noqa: F401
-                  gen_xr_device, load, select_block_size)
+                  gen_xr_device, load, release_cached_memory, select_block_size)

@@ -908,6 +908,17 @@ int gls_set_block_cols(gls_ctx* c, int64_t cols) {
   return GLS_OK;
 }
 
+int gls_release_cached_memory(void) {
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+      cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess || cudaMemPoolTrimTo(pool, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return GLS_ERR_CUDA;
+  }
+  return GLS_OK;
+}
+
 void gls_destroy(gls_ctx* c) {
   if (!c) return;
   DeviceGuard g(c->device);

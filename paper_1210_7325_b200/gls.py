@@ -42,6 +42,7 @@ ABI_SYMBOLS = (
     "gls_error_string", "gls_create_adopt", "gls_shared_view", "gls_commit_shared",
     "gls_kernel_launches", "gls_set_path", "gls_path_counts", "gls_solve_block_i8",
     "gls_set_timing", "gls_read_timing", "gls_get_dims", "gls_solve_file", "gls_select_block_size",
+    "gls_release_cached_memory",
 )
 
 
@@ -114,6 +115,8 @@ def load(build_if_missing: bool = True):
     L.gls_select_block_size.argtypes = [i64, i32, i32, i32, i64, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_double, ctypes.POINTER(i32)]
     L.gls_select_block_size.restype = i64
+    L.gls_release_cached_memory.argtypes = []
+    L.gls_release_cached_memory.restype = ctypes.c_int
     _lib = L
     return L
 
@@ -153,6 +156,13 @@ def select_block_size(n: int, p: int, pR: int, elem_bytes: int, mem_limit_bytes:
     k = load().gls_select_block_size(n, p, pR, elem_bytes, mem_limit_bytes, compute_groups_per_s,
                                      io_bytes_per_s, io_latency_s, ctypes.byref(flag))
     return int(k), bool(flag.value)
+
+
+def release_cached_memory() -> None:
+    """gls_release_cached_memory: hand the pool memory cached by destroyed contexts back to the driver."""
+    rc = load().gls_release_cached_memory()
+    if rc:
+        raise GLSError(rc, error_string(rc))
 
 
 def error_string(code: int) -> str:
