@@ -70,6 +70,8 @@ struct gls_ctx {
   int64_t sws_groups = 0;
   int8_t* x8[2] = {nullptr, nullptr};
   int* flags = nullptr;                  // 2 ints, then (8-byte aligned) 2 work counters
+  int* cflags = nullptr;                 // per conversion chunk of a block: "not int8" flags
+  int64_t cflags_cap = 0;
   unsigned long long* ran = nullptr;     // [0] int8 kernel launches that ran, [1] FP64 ones
   cudaEvent_t ev_conv[2] = {}, ev_oz[2] = {}, ev_fb[2] = {};
   cudaStream_t fb = nullptr;  // gated FP64 fallback launches (off the int8 kernel's stream)
@@ -441,7 +443,8 @@ int ensure_x8(gls_ctx* c, int64_t cols) {
 }
 
 int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* b, int32_t* stt,
-             const int* gate) {
+             const int* gate, const double* cv_X = nullptr, int64_t cv_ldx = 0, int64_t cv_cols = 0,
+             int8_t* cv_X8 = nullptr, int* cv_flag = nullptr) {
   if (c->p > kOzPosvInKernelMaxP && c->sws_groups < groups) {
     CK(c, cudaDeviceSynchronize());
     dfree(c, c->sws);
@@ -468,6 +471,12 @@ int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* 
   a.b_out = b;
   a.status_out = stt;
   a.s_ws = c->p > kOzPosvInKernelMaxP ? c->sws : nullptr;
+  a.cv_X = cv_X;
+  a.cv_ldx = cv_ldx;
+  a.cv_cols = cv_cols;
+  a.cv_X8 = cv_X8;
+  a.cv_ld8 = ld8;
+  a.cv_flag = cv_flag;
   std::string msg;
   cudaError_t e = launch_ozaki_gls(c->stream, a, c->num_sms, &msg, &c->launches);
   if (e != cudaSuccess) {
@@ -479,18 +488,16 @@ int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* 
 }
 
 // One block of device-resident double X (column-major, ld = ldx, even, 16-byte aligned).
-// Path AUTO: chunks of up to 8 waves of int8 tiles; chunk j is converted to int8 on the conv stream
-// (flagging values that are not integers in [-128, 127]), issued behind the solve of chunk j-1: its
-// blocks cannot share an SM with a solve CTA (measured: beside one they convert at ~1 GB/s per SM and
-// slow it), so they fill the SMs that kernel's tail frees and then stream at HBM speed on the whole
-// GPU.  Then the int8 kernel and the FP64 kernel are both launched, each gated on the device by the
-// chunk's flag, so exactly one of them does the work and the host never waits.
+// Path AUTO: chunks of up to 8 waves of int8 tiles (1, 2, .. 8, 8, ..).  Chunk 0 is converted to int8
+// by a standalone pass; every later chunk j+1 is converted by the convert-ahead warps of the int8
+// kernel of chunk j, concurrently with its tensor-core work, into the other of the two int8
+// workspaces (flagging values that are not integers in [-128, 127] in cflags[j+1]).  For each chunk
+// the int8 kernel and the FP64 kernel are both launched, each gated on the device by the chunk's
+// flag, so exactly one of them does the work and the host never waits.
 int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt) {
   if (c->path == GLS_PATH_FP64 || !c->oz_ok) return run_fp64(c, X, ldx, groups, b, stt, nullptr);
   const int pR = c->pR, p = c->p;
   const int64_t cpt = 4 * (int64_t)((32 / pR) * pR);
-  // chunk j covers groups [bnd[j], bnd[j+1]) and holds min(j+1, 8) waves of tiles: the first
-  // conversion, which nothing can hide, is short
   const int64_t wave_groups = (int64_t)c->num_sms * cpt / pR;
   int64_t chunk_groups = 8 * wave_groups;
   if (chunk_groups > groups) chunk_groups = groups;
@@ -500,47 +507,48 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
   for (int64_t j = 1; bnd.back() < groups; ++j)
     bnd.push_back(std::min(groups, bnd.back() + std::min<int64_t>(j, 8) * wave_groups));
   const int64_t nchunks = (int64_t)bnd.size() - 1;
-  auto issue_conv = [&](int64_t j) -> int {
-    const int buf = (int)((c->oseq + j) & 1);
-    const int64_t g0 = bnd[j], gc = bnd[j + 1] - bnd[j];
-    // ev_oz[buf] is recorded on the compute stream before the kernels of chunk j-1, i.e. after those
-    // of chunk j-2 (the previous users of x8[buf] and flags[buf]) and after whatever produced X.
-    CK(c, cudaEventRecord(c->ev_oz[buf], c->stream));
-    CK(c, cudaStreamWaitEvent(c->conv, c->ev_oz[buf], 0));
-    CK(c, cudaStreamWaitEvent(c->conv, c->ev_fb[buf], 0));  // the fallback of chunk j-2 read flags[buf]
-    unsigned long long* work = (unsigned long long*)(c->flags + 2) + buf;
-    CK(c, cudaMemsetAsync(c->flags + buf, 0, sizeof(int), c->conv));
-    CK(c, cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->conv));
-    LaunchTimer lt(c, c->conv, 2);
-    oz_convert(c->conv, X + (size_t)g0 * pR * ldx, ldx, c->n, gc * pR, c->x8[buf], c->ld8, c->flags + buf, work,
-               c->num_sms, &c->launches);
+  if (c->cflags_cap < nchunks) {
+    CK(c, cudaDeviceSynchronize());
+    dfree(c, c->cflags);
+    c->cflags_cap = 0;
+    const int64_t cap = std::max<int64_t>(nchunks, 256);
+    CK(c, dalloc(c, &c->cflags, (size_t)cap * sizeof(int)));
+    CK(c, cudaStreamSynchronize(c->own_stream));
+    c->cflags_cap = cap;
+  }
+  // the flags of the previous block were last read by its FP64 launches, which the compute stream
+  // waited for at the end of that block
+  CK(c, cudaMemsetAsync(c->cflags, 0, (size_t)nchunks * sizeof(int), c->stream));
+  unsigned long long* work = (unsigned long long*)(c->flags + 2);
+  CK(c, cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->stream));
+  {
+    LaunchTimer lt(c, c->stream, 2);
+    oz_convert(c->stream, X, ldx, c->n, (bnd[1] - bnd[0]) * pR, c->x8[0], c->ld8, c->cflags, work, c->num_sms,
+               &c->launches);
     CK(c, cudaGetLastError());
-    CK(c, cudaEventRecord(c->ev_conv[buf], c->conv));
-    return GLS_OK;
-  };
-  rc = issue_conv(0);
-  if (rc) return rc;
+  }
   for (int64_t j = 0; j < nchunks; ++j) {
-    const int buf = (int)((c->oseq + j) & 1);
+    const int buf = (int)(j & 1);
     const int64_t g0 = bnd[j], gc = bnd[j + 1] - bnd[j];
-    CK(c, cudaStreamWaitEvent(c->stream, c->ev_conv[buf], 0));
-    if (j + 1 < nchunks) {
-      rc = issue_conv(j + 1);
-      if (rc) return rc;
-    }
+    // cflags[j] is final here (written by chunk j-1's kernel or the standalone pass)
+    CK(c, cudaEventRecord(c->ev_oz[buf], c->stream));
+    CK(c, cudaStreamWaitEvent(c->fb, c->ev_oz[buf], 0));
     double* bj = b + (size_t)g0 * p;
     int32_t* sj = stt ? stt + g0 : nullptr;
-    rc = run_int8(c, c->x8[buf], c->ld8, gc, bj, sj, c->flags + buf);
+    if (j + 1 < nchunks)
+      rc = run_int8(c, c->x8[buf], c->ld8, gc, bj, sj, c->cflags + j, X + (size_t)bnd[j + 1] * pR * ldx, ldx,
+                    (bnd[j + 2] - bnd[j + 1]) * pR, c->x8[buf ^ 1], c->cflags + j + 1);
+    else
+      rc = run_int8(c, c->x8[buf], c->ld8, gc, bj, sj, c->cflags + j);
     if (rc) return rc;
     // the gated FP64 kernel runs on its own stream, so when it has nothing to do its launch never
-    // holds back the next int8 kernel (it would queue behind the running conversion pass)
-    CK(c, cudaStreamWaitEvent(c->fb, c->ev_conv[buf], 0));
-    rc = run_fp64(c, X + (size_t)g0 * pR * ldx, ldx, gc, bj, sj, c->flags + buf, c->fb);
+    // holds back the next int8 kernel
+    rc = run_fp64(c, X + (size_t)g0 * pR * ldx, ldx, gc, bj, sj, c->cflags + j, c->fb);
     if (rc) return rc;
-    CK(c, cudaEventRecord(c->ev_fb[buf], c->fb));
   }
   // the block is complete on the compute stream only when its fallback launches are
-  for (int k = 0; k < 2; ++k) CK(c, cudaStreamWaitEvent(c->stream, c->ev_fb[k], 0));
+  CK(c, cudaEventRecord(c->ev_fb[0], c->fb));
+  CK(c, cudaStreamWaitEvent(c->stream, c->ev_fb[0], 0));
   c->oseq += nchunks;
   return GLS_OK;
 }
@@ -942,6 +950,7 @@ void gls_destroy(gls_ctx* c) {
   dfree(c, c->x8[1]);
   dfree(c, c->sws);
   dfree(c, c->flags);
+  dfree(c, c->cflags);
   dfree(c, c->ran);
   for (int k = 0; k < 2; ++k) {
     dfree(c, c->stage8[k]);

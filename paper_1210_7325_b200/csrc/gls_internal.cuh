@@ -153,6 +153,13 @@ struct OzArgs {
   int32_t* status_out;
   double* s_ws;         // nullable: m_blk records of pR (pL + pR + 1) doubles; when set, the kernel
                         // stores S_BL, S_BR, b_B there and a batched posv kernel solves (large p)
+  // nullable convert-ahead job run by the kernel's conv warps (also when gated): FP64 X (ld cv_ldx,
+  // even, 16-byte aligned, cv_cols columns of n) -> int8 cv_X8 (ld cv_ld8); non-integers set *cv_flag
+  const double* cv_X = nullptr;
+  int64_t cv_ldx = 0, cv_cols = 0;
+  int8_t* cv_X8 = nullptr;
+  int64_t cv_ld8 = 0;
+  int* cv_flag = nullptr;
 };
 constexpr int kOzPosvInKernelMaxP = 8;  // p above this: posv in a separate kernel (oz s_ws)
 // rows of n int8 codes packed back to back -> the same rows at pitch ld8 (>= n); padding untouched

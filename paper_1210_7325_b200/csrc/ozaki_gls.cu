@@ -53,7 +53,10 @@ constexpr int kATile = 128 * kKC;        // 16 KiB
 constexpr int kBTile = kBN * kKC;        // 28 KiB (whole packed digit tile)
 constexpr int kBHalf = kBTile / 2;       // 14 KiB staged per CTA of a pair
 constexpr int kEpiWarps = 8;
-constexpr int kThreads = (2 + kEpiWarps) * 32;
+constexpr int kConvWarps = 2;  // convert-ahead warps: FP64 -> int8 of the NEXT chunk (see the kernel)
+constexpr int kThreads = (2 + kEpiWarps + kConvWarps) * 32;
+constexpr int kCvBuf = 8192;          // bytes per convert-ahead staging buffer (two per conv warp)
+constexpr int kCvRows = kCvBuf / 8;   // X rows per piece
 constexpr uint32_t kTmemCols = 512;
 // TMEM column pair of double w in the epilogue hand-over scratch: columns MMAs never write
 __device__ __forceinline__ uint32_t xcol(int w) { return w < 16 ? 224 + 2 * w : 480 + 2 * (w - 16); }
@@ -81,7 +84,31 @@ struct OzParams {
                         // block of the tile), the others evict_first
   const double* vscale; // pL+1 column scales 2^-(e_w+48) of V = M^{-1} [X_L | y]
   double* s_ws;         // nullable: per problem S_BL (pR x pL), S_BR (pR x pR), b_B (pR) for oz_posv_kernel
+  // convert-ahead job (nullable cv_X): FP64 X of the next chunk -> int8 cv_X8, any non-integer or
+  // out-of-range value sets *cv_flag
+  int64_t n;            // rows of X / T
+  const double* cv_X;
+  int64_t cv_ldx, cv_cols;
+  int8_t* cv_X8;
+  int64_t cv_ld8;
+  int* cv_flag;
 };
+
+// FP64 value -> int8 code, flagging (bad = 1) anything that is not an integer in [-128, 127]
+__device__ __forceinline__ uint32_t to_i8_bits(double v, int& bad) {
+  // 32-bit integer tests on the two words of v: an integer 1 <= |v| <= 255 has biased exponent
+  // 1023 + k (k <= 7), its integer part in the top k of the high word's 20 mantissa bits and nothing
+  // below (the low word and the high word's low 20 - k bits are zero)
+  const uint32_t hi = (uint32_t)__double2hiint(v), lo = (uint32_t)__double2loint(v);
+  const uint32_t a = hi & 0x7fffffffu;
+  const uint32_t k = (a >> 20) - 1023u;  // wraps for |v| < 1
+  const bool zero = (a | lo) == 0u;
+  const bool ok = k <= 7u && lo == 0u && (a & ((0x100000u >> (k & 7u)) - 1u)) == 0u;
+  const uint32_t mag = ((a & 0xfffffu) | 0x100000u) >> (20u - (k & 7u));  // 1 .. 255 when ok
+  const bool neg = (hi >> 31) != 0u;
+  bad |= !zero && (!ok || mag > (neg ? 128u : 127u));  // 0 < |v| < 1, fractions, |v| >= 128/256, inf, NaN
+  return zero ? 0u : ((neg ? (0u - mag) : mag) & 0xffu);
+}
 
 template <int NA>
 __device__ __forceinline__ void zero_acc(double (&acc)[NA]) {
@@ -179,10 +206,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* empty = bars + ST;           // both CTAs: the pair's MMAs released the stage
   uint64_t* tfull = bars + 2 * ST;       // both CTAs: accumulator buffer ready for the epilogue
   uint64_t* tempty = bars + 2 * ST + 2;  // used in the leader: both epilogues drained the buffer
-  uint32_t* tslot = (uint32_t*)(bars + 2 * ST + 4);
+  uint64_t* cvbar = bars + 2 * ST + 4;   // 2 per conv warp: its staging buffers landed
+  uint32_t* tslot = (uint32_t*)(cvbar + 2 * kConvWarps);
+  uint8_t* cvbuf = (uint8_t*)(tslot + 4);  // 2 x kCvBuf per conv warp (16-byte aligned)
 
-  if (kp.gate && *(volatile const int*)kp.gate != 0) return;  // uniform across the grid
-  if (kp.ran && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(kp.ran, 1ull);
+  // A gated launch (this chunk is not integer: the FP64 kernel solves it) still runs its
+  // convert-ahead job -- the next chunk depends on it -- but no tile.
+  const bool gated = kp.gate && *(volatile const int*)kp.gate != 0;  // uniform across the grid
+  if (!gated && kp.ran && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(kp.ran, 1ull);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -196,6 +227,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 2 * kEpiWarps);
     }
+    for (int b = 0; b < 2 * kConvWarps; ++b) mbar_init(&cvbar[b], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_pair(tslot, kTmemCols);
@@ -205,7 +237,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tslot;
   const int cpt = 4 * kp.cpw;  // columns per tile (per CTA)
-  const Sched sc(kp.num_tiles, (int)rank);
+  const Sched sc(gated ? 0 : kp.num_tiles, (int)rank);
 
   // Steps: step t of a tile covers row blocks 2t and 2t+1 (the last one alone when NBR is odd); both
   // have the same K extent, so each X chunk is loaded once and multiplied by both row blocks' digit
@@ -342,7 +374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         kp.prof[blockIdx.x * 8 + 3] = clock64() - tstart;
       }
     }
-  } else {
+  } else if (warp < 2 + kEpiWarps) {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int ew = warp - 2;
     const int q = warp & 3;      // TMEM lane quadrant this warp may access
@@ -530,6 +562,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       kp.prof[blockIdx.x * 8 + 5] = prof_drain;
       kp.prof[blockIdx.x * 8 + 6] = prof_busy;
     }
+  } else if (kp.cv_X) {
+    // ------------------------------------------------------------ convert-ahead (both CTAs)
+    // FP64 X of the next chunk -> int8, piece by piece (kCvRows rows of one column): a bulk copy
+    // into shared memory (bytes in flight without registers: plain loads from an SM running this
+    // kernel take microseconds), integer bit tests, 2-byte stores.  Pieces are dealt round-robin
+    // over all conv warps of the grid; two buffers per warp keep one copy in flight while the other
+    // piece is converted.
+    const int cw = warp - (2 + kEpiWarps);
+    const int64_t gw = (int64_t)blockIdx.x * kConvWarps + cw, nw = (int64_t)gridDim.x * kConvWarps;
+    const int64_t n = kp.n, ppc = (n + kCvRows - 1) / kCvRows;
+    const int64_t units = kp.cv_cols * ppc;
+    uint8_t* const buf0 = cvbuf + (size_t)cw * 2 * kCvBuf;
+    uint64_t* const bar0 = cvbar + 2 * cw;
+    auto piece = [&](int64_t u, int64_t& c, int64_t& r0, int& rows) {
+      c = u / ppc;
+      r0 = (u - c * ppc) * kCvRows;
+      rows = (int)(n - r0 < kCvRows ? n - r0 : kCvRows);
+    };
+    auto issue = [&](int64_t u, int b) {
+      int64_t c, r0;
+      int rows;
+      piece(u, c, r0, rows);
+      const uint32_t bytes = (uint32_t)(rows * 8) & ~15u;  // an odd last row is read directly
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&bar0[b], bytes);
+        bulk_g2s(buf0 + b * kCvBuf, kp.cv_X + c * kp.cv_ldx + r0, bytes, &bar0[b]);
+      }
+    };
+    int bad = 0;
+    uint32_t ph0 = 0, ph1 = 0;
+    if (gw < units) issue(gw, 0);
+    if (gw + nw < units) issue(gw + nw, 1);
+    int b = 0;
+    for (int64_t u = gw; u < units; u += nw, b ^= 1) {
+      mbar_wait(&bar0[b], b ? ph1 : ph0);
+      if (b) ph1 ^= 1; else ph0 ^= 1;
+      int64_t c, r0;
+      int rows;
+      piece(u, c, r0, rows);
+      const double* sv = (const double*)(buf0 + b * kCvBuf);
+      int8_t* dst = kp.cv_X8 + c * kp.cv_ld8 + r0;
+#pragma unroll 4
+      for (int k = 0; k < kCvRows / 64; ++k) {  // lane holds rows 2 lane + 64 k, +1
+        const int r = 2 * lane + 64 * k;
+        if (r + 2 <= rows) {
+          const double2 v = *(const double2*)(sv + r);
+          *(uint16_t*)(dst + r) = (uint16_t)(to_i8_bits(v.x, bad) | to_i8_bits(v.y, bad) << 8);
+        } else if (r < rows) {  // the column's odd last row: not in the bulk copy
+          dst[r] = (int8_t)to_i8_bits(__ldg(kp.cv_X + c * kp.cv_ldx + r0 + r), bad);
+        }
+      }
+      __syncwarp();
+      fence_proxy_async();  // this warp's reads of the buffer before the copy that overwrites it
+      if (u + 2 * nw < units) issue(u + 2 * nw, b);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(kp.cv_flag, 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -671,20 +759,6 @@ __global__ void oz_aux_w_kernel(const double* __restrict__ W, int64_t ldw, int64
 
 // x -> int8 bits for an integer-valued double in [-128, 127], by integer operations on its bits only
 // (FP64 arithmetic contends with the tensor core on this part); bad |= any other value.
-__device__ __forceinline__ uint32_t to_i8_bits(double v, int& bad) {
-  // 32-bit integer tests on the two words of v: an integer 1 <= |v| <= 255 has biased exponent
-  // 1023 + k (k <= 7), its integer part in the top k of the high word's 20 mantissa bits and nothing
-  // below (the low word and the high word's low 20 - k bits are zero)
-  const uint32_t hi = (uint32_t)__double2hiint(v), lo = (uint32_t)__double2loint(v);
-  const uint32_t a = hi & 0x7fffffffu;
-  const uint32_t k = (a >> 20) - 1023u;  // wraps for |v| < 1
-  const bool zero = (a | lo) == 0u;
-  const bool ok = k <= 7u && lo == 0u && (a & ((0x100000u >> (k & 7u)) - 1u)) == 0u;
-  const uint32_t mag = ((a & 0xfffffu) | 0x100000u) >> (20u - (k & 7u));  // 1 .. 255 when ok
-  const bool neg = (hi >> 31) != 0u;
-  bad |= !zero && (!ok || mag > (neg ? 128u : 127u));  // 0 < |v| < 1, fractions, |v| >= 128/256, inf, NaN
-  return zero ? 0u : ((neg ? (0u - mag) : mag) & 0xffu);
-}
 
 // X (double, column-major, ld = ldx) -> X8 (int8, column-major, ld = ld8), flagging any value that
 // is not an integer in [-128, 127] (NaN included); X8's padding rows [n, ld8) are not written (the
@@ -772,7 +846,7 @@ PFN_encodeTiled get_encode() {
 template <int PL1C, int NA, bool PR1>
 cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& xmap, const CUtensorMap& tmap,
                               const CUtensorMap& vmap, const OzParams& kp, int num_sms) {
-  constexpr int kFixed = 1024 + 512;  // alignment, barriers
+  constexpr int kFixed = 1024 + 512 + 2 * kConvWarps * kCvBuf;  // alignment, barriers, conv staging
   constexpr int kStage = kATile + 2 * kBHalf;  // X chunk + the digit halves of two row blocks
   constexpr int ST = (232448 - kFixed) / kStage < 8 ? (232448 - kFixed) / kStage : 8;
   static_assert(ST >= 4, "shared memory budget");
@@ -871,9 +945,9 @@ void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t
   int64_t blocks = (int64_t)num_sms * 4;
   if (blocks > nunits) blocks = nunits;
   if (blocks < 1) blocks = 1;
-  // kConvSmem of (unused) dynamic shared memory keeps these blocks off SMs that hold an int8 solve
-  // CTA: placed beside one they would convert at ~1 GB/s per SM and slow it down, while on the
-  // whole GPU (the tail of each solve kernel onwards) the pass streams at HBM speed
+  // Used for the first chunk of a block (later chunks are converted by the solve kernel's
+  // convert-ahead warps).  kConvSmem of (unused) dynamic shared memory keeps these blocks off SMs
+  // that hold an int8 solve CTA: placed beside one, plain loads convert at ~1 GB/s per SM.
   oz_x_to_i8_kernel<<<(unsigned)blocks, kConvThreads, kConvSmem, s>>>(X, ldx, n, cols, X8, ld8, flag, work);
   if (lc) ++*lc;
 }
@@ -921,6 +995,13 @@ cudaError_t launch_ozaki_gls(cudaStream_t s, const OzArgs& a, int num_sms, std::
   kp.b_out = a.b_out;
   kp.status_out = a.status_out;
   kp.s_ws = a.s_ws;
+  kp.n = a.n;
+  kp.cv_X = a.cv_X;
+  kp.cv_ldx = a.cv_ldx;
+  kp.cv_cols = a.cv_cols;
+  kp.cv_X8 = a.cv_X8;
+  kp.cv_ld8 = a.cv_ld8;
+  kp.cv_flag = a.cv_flag;
   kp.cols = cols;
   kp.m_blk = a.m_blk;
   const int64_t cpt = 4 * (int64_t)cpw;
