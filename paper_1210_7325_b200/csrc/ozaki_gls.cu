@@ -32,7 +32,9 @@
 //               extra MMA pass against the digits of V = M^-1 [X_L | y] (reading A17) -- X~_R never
 //               leaves registers.  After the last step the two halves are summed (through TMEM) in a
 //               fixed order and one lane per problem assembles S_i and solves it by Cholesky with the
-//               rank rule of reading A4 (Alg. 5 line 11).
+//               rank rule of reading A4 (Alg. 5 line 11; for p > 8 a separate batched kernel does).
+//   warps 10-11 convert-ahead: FP64 -> int8 of the NEXT chunk's X_R through bulk copies into
+//               shared memory, concurrently with the tensor-core work.
 #include <cuda.h>
 
 #include <cstdio>
