@@ -527,15 +527,26 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
                &c->launches);
     CK(c, cudaGetLastError());
   }
+  // convert-ahead needs the kernel's tensor work per column (~n^2) to cover the conversion of the
+  // next chunk's column (8n bytes): at small n the convert-ahead warps would become the bottleneck
+  // (n = 1500: kernel 1.8 -> 3.5 ms), and each chunk gets a standalone pass instead
+  const bool ahead = c->n >= kConvertAheadMinN;
   for (int64_t j = 0; j < nchunks; ++j) {
     const int buf = (int)(j & 1);
     const int64_t g0 = bnd[j], gc = bnd[j + 1] - bnd[j];
-    // cflags[j] is final here (written by chunk j-1's kernel or the standalone pass)
+    if (!ahead && j > 0) {
+      CK(c, cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->stream));
+      LaunchTimer lt(c, c->stream, 2);
+      oz_convert(c->stream, X + (size_t)g0 * pR * ldx, ldx, c->n, gc * pR, c->x8[buf], c->ld8, c->cflags + j,
+                 work, c->num_sms, &c->launches);
+      CK(c, cudaGetLastError());
+    }
+    // cflags[j] is final here (written by chunk j-1's kernel or a standalone pass)
     CK(c, cudaEventRecord(c->ev_oz[buf], c->stream));
     CK(c, cudaStreamWaitEvent(c->fb, c->ev_oz[buf], 0));
     double* bj = b + (size_t)g0 * p;
     int32_t* sj = stt ? stt + g0 : nullptr;
-    if (j + 1 < nchunks)
+    if (ahead && j + 1 < nchunks)
       rc = run_int8(c, c->x8[buf], c->ld8, gc, bj, sj, c->cflags + j, X + (size_t)bnd[j + 1] * pR * ldx, ldx,
                     (bnd[j + 2] - bnd[j + 1]) * pR, c->x8[buf ^ 1], c->cflags + j + 1);
     else

@@ -588,8 +588,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       piece(u, c, r0, rows);
       const uint32_t bytes = (uint32_t)(rows * 8) & ~15u;  // an odd last row is read directly
       if (lane == 0) {
-        mbar_arrive_expect_tx(&bar0[b], bytes);
-        bulk_g2s(buf0 + b * kCvBuf, kp.cv_X + c * kp.cv_ldx + r0, bytes, &bar0[b]);
+        if (bytes) {
+          mbar_arrive_expect_tx(&bar0[b], bytes);
+          bulk_g2s(buf0 + b * kCvBuf, kp.cv_X + c * kp.cv_ldx + r0, bytes, &bar0[b]);
+        } else {
+          mbar_arrive(&bar0[b]);  // a one-row piece: nothing to copy
+        }
       }
     };
     int bad = 0;

@@ -149,6 +149,42 @@ def test_mixed_chunks_pick_paths_independently(glsmod):
     assert_parity(b, st, b_or, st_or, label="mixed chunks")
 
 
+@pytest.mark.parametrize("n", [4096, 4097])
+def test_convert_ahead_chunks(glsmod, n):
+    """n >= 4096: every chunk of a block after the first is converted to int8 by the convert-ahead
+    warps of the previous chunk's kernel (also when that kernel is gated off).  n = 4096 takes the
+    in-place device path; odd n = 4097 the staged one (blocks of 4 waves, ld = n + 1) and leaves a
+    one-row piece at the end of every column (read directly, not by bulk copy).  A non-integer value
+    in the last row of a column in chunk 1 or 2 of a block (1, 2, 1 waves) sends exactly that chunk
+    to the FP64 kernel; all rows agree with the FP64 path, and sampled SNPs with the oracle."""
+    pL, pR = 2, 1
+    w = 148 * 128                       # SNPs per wave of tiles (pR = 1)
+    m = 6 * w - 777                     # several chunks, ragged last one
+    P = gen.make_problem(n, pL, pR, seed=41)
+    Xd = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    for c in range(0, m, 16384):
+        k = min(16384, m - c)
+        glsmod.gen_xr_device(41, n, c, k, Xd[c:c + k])
+    counts0 = []
+    b, st, _ = run_gpu(glsmod, P, Xd, m, pR, counts=counts0)
+    assert counts0[1] == 0 and counts0[0] >= 3, counts0
+    b64, st64, _ = run_gpu(glsmod, P, Xd, m, pR, path=glsmod.GLS_PATH_FP64)
+    assert_parity(b, st, b64, st64, label="int8 vs FP64 path")
+    for col, value in ((w + 1234, 0.5), (3 * w + 1234, 128.0)):  # chunk 1 and chunk 2 of the first block
+        Xd2 = Xd.clone()
+        Xd2[col, n - 1] = value
+        counts = []
+        b2, st2, _ = run_gpu(glsmod, P, Xd2, m, pR, counts=counts)
+        assert counts == [counts0[0] - 1, 1], (col, value, counts, counts0)
+        b64, st64, _ = run_gpu(glsmod, P, Xd2, m, pR, path=glsmod.GLS_PATH_FP64)
+        assert_parity(b2, st2, b64, st64, label="int8 vs FP64 path, value %g" % value)
+        del Xd2
+    # oracle on SNPs around the chunk boundaries and the ragged end
+    pick = sorted({0, 1, m - 1, m - 2} | {x + d for x in (w, 3 * w, 4 * w, 5 * w) for d in (-1, 0)})
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, Xd[pick].cpu().numpy(), pR)
+    assert_parity(b[pick], st[pick], b_or, st_or, label="convert-ahead vs oracle")
+
+
 def test_host_stream_equals_device_bitwise(glsmod):
     """Host-resident X_R (Alg. 8 double-buffered stream) gives the same bits as device X_R,
     for several block sizes (block-partition independence)."""
