@@ -1,5 +1,5 @@
 #!/bin/bash
-CMD="python bench.py --m 681984 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --m 833536 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
 timeout 600 $CMD > gpurun_out/p2_plain.log 2>&1; rc=$?; echo "plain_rc=$rc"
 if [ $rc -eq 0 ]; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/p2_launches.csv $CMD > /dev/null 2>&1; echo "ncu_launch_rc=$?"
