@@ -499,14 +499,27 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
   const int pR = c->pR, p = c->p;
   const int64_t cpt = 4 * (int64_t)((32 / pR) * pR);
   const int64_t wave_groups = (int64_t)c->num_sms * cpt / pR;
-  int64_t chunk_groups = 8 * wave_groups;
-  if (chunk_groups > groups) chunk_groups = groups;
+  // convert-ahead needs the kernel's tensor work per column (~n^2) to cover the conversion of the
+  // next chunk's column (8n bytes): at small n the convert-ahead warps would become the bottleneck
+  // (n = 1500: kernel 1.8 -> 3.5 ms), and the conversion runs as standalone passes instead
+  const bool ahead = c->n >= kConvertAheadMinN;
+  std::vector<int64_t> bnd{0};
+  if (ahead) {
+    for (int64_t j = 1; bnd.back() < groups; ++j)
+      bnd.push_back(std::min(groups, bnd.back() + std::min<int64_t>(j, 8) * wave_groups));
+  } else {
+    // nothing to hide the passes behind: chunks of 8 waves (one pass and one solve launch each; the
+    // int8/FP64 path is decided per chunk) within the workspace budget
+    const int64_t ld8 = (c->n + 15) & ~(int64_t)15;
+    int64_t cap = std::min<int64_t>(8 * wave_groups, kSerialChunkBytes / (ld8 * pR)) / wave_groups * wave_groups;
+    if (cap < wave_groups) cap = wave_groups;
+    for (int64_t g = 0; g < groups; g += cap) bnd.push_back(std::min(groups, g + cap));
+  }
+  const int64_t nchunks = (int64_t)bnd.size() - 1;
+  int64_t chunk_groups = 0;
+  for (int64_t j = 0; j < nchunks; ++j) chunk_groups = std::max(chunk_groups, bnd[j + 1] - bnd[j]);
   int rc = ensure_x8(c, chunk_groups * pR);
   if (rc) return rc;
-  std::vector<int64_t> bnd{0};
-  for (int64_t j = 1; bnd.back() < groups; ++j)
-    bnd.push_back(std::min(groups, bnd.back() + std::min<int64_t>(j, 8) * wave_groups));
-  const int64_t nchunks = (int64_t)bnd.size() - 1;
   if (c->cflags_cap < nchunks) {
     CK(c, cudaDeviceSynchronize());
     dfree(c, c->cflags);
@@ -527,10 +540,6 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
                &c->launches);
     CK(c, cudaGetLastError());
   }
-  // convert-ahead needs the kernel's tensor work per column (~n^2) to cover the conversion of the
-  // next chunk's column (8n bytes): at small n the convert-ahead warps would become the bottleneck
-  // (n = 1500: kernel 1.8 -> 3.5 ms), and each chunk gets a standalone pass instead
-  const bool ahead = c->n >= kConvertAheadMinN;
   for (int64_t j = 0; j < nchunks; ++j) {
     const int buf = (int)(j & 1);
     const int64_t g0 = bnd[j], gc = bnd[j + 1] - bnd[j];

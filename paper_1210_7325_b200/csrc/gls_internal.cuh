@@ -163,6 +163,7 @@ struct OzArgs {
 };
 constexpr int kOzPosvInKernelMaxP = 8;  // p above this: posv in a separate kernel (oz s_ws)
 constexpr int64_t kConvertAheadMinN = 4096;  // n below this: standalone FP64 -> int8 pass per chunk
+constexpr int64_t kSerialChunkBytes = 1ll << 30;  // int8 workspace per chunk when the passes are standalone
 // rows of n int8 codes packed back to back -> the same rows at pitch ld8 (>= n); padding untouched
 void oz_repack_rows(cudaStream_t s, const int8_t* src, int64_t n, int64_t rows, int8_t* dst, int64_t ld8,
                     int64_t* launch_counter);
