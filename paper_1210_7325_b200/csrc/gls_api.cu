@@ -319,7 +319,10 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
     trmm_lower_skinny(s, n, pL + 1, T, n, B, n, W, n, A, &c->launches);
   else
     dgemm(s, n, pL + 1, n, 1.0, T, n, 'N', B, n, 'N', 0.0, W, n, GEMM_KMAX_ROW, &c->launches);
-  dgemm(s, pL + 1, pL + 1, n, 1.0, W, n, 'T', W, n, 'N', 0.0, c->G, pL + 1, 0, &c->launches);
+  // G: a (pL+1)^2 output with K = n -- split K over the machine, partial tiles in A (free again once
+  // W is formed; it holds the at most 16 (pL+1)^2 partials whenever n^2 does)
+  dgemm(s, pL + 1, pL + 1, n, 1.0, W, n, 'T', W, n, 'N', 0.0, c->G, pL + 1, 0, &c->launches,
+        n * n >= 16 * (int64_t)(pL + 1) * (pL + 1) ? A : nullptr);
   mark("W,G");
   pack_T(s, T, n, n, c->NB, c->Tpk, &c->launches);
   pack_W(s, W, n, n, pL + 1, c->NB, c->NW, c->Wpk, &c->launches);
