@@ -193,6 +193,7 @@ __global__ void trmm_skinny_partial(int64_t n, int k, const double* __restrict__
   for (int w = 0; w < 21; ++w) acc[w] = 0.0;
   if (i < n) {
     const int64_t jend = (i + 1 < j1) ? i + 1 : j1;  // lower triangular: j <= i
+#pragma unroll 8
     for (int64_t j = j0; j < jend; ++j) {
       const double t = T[i + j * ldt];
 #pragma unroll
@@ -224,6 +225,7 @@ __global__ void trmm_t_skinny(int64_t n, int k, const double* __restrict__ T, in
     double acc[21];
 #pragma unroll
     for (int w = 0; w < 21; ++w) acc[w] = 0.0;
+#pragma unroll 8
     for (int64_t i = j + lane; i < n; i += 32) {
       const double t = T[i + j * ldt];
 #pragma unroll

@@ -640,8 +640,10 @@ __global__ void oz_rowscale_kernel(const double* __restrict__ T, int64_t ld, int
   const int rl = threadIdx.x & 31, strand = threadIdx.x >> 5;
   const int64_t r = (int64_t)blockIdx.x * 32 + rl;
   double mx = 0.0;
-  if (r < n)
+  if (r < n) {
+#pragma unroll 8
     for (int64_t j = strand; j <= r; j += 8) mx = fmax(mx, fabs(T[r + j * ld]));
+  }
   sm[strand][rl] = mx;
   __syncthreads();
   if (strand == 0) {
