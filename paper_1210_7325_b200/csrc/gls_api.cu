@@ -64,7 +64,6 @@ struct gls_ctx {
   int path = GLS_PATH_AUTO;
   bool oz_ok = false;  // n small enough for exact int32 digit products
   // int8 conversion workspaces (two, swapping roles) and their rejection flags
-  cudaStream_t conv = nullptr;
   int64_t x8_cols = 0, ld8 = 0;
   double* sws = nullptr;     // per-problem records for the separate posv of large p (OzArgs::s_ws)
   int64_t sws_groups = 0;
@@ -73,9 +72,8 @@ struct gls_ctx {
   int* cflags = nullptr;                 // per conversion chunk of a block: "not int8" flags
   int64_t cflags_cap = 0;
   unsigned long long* ran = nullptr;     // [0] int8 kernel launches that ran, [1] FP64 ones
-  cudaEvent_t ev_conv[2] = {}, ev_oz[2] = {}, ev_fb[2] = {};
+  cudaEvent_t ev_oz[2] = {}, ev_fb[2] = {};
   cudaStream_t fb = nullptr;  // gated FP64 fallback launches (off the int8 kernel's stream)
-  uint64_t oseq = 0;
   // host int8 staging (gls_solve_block_i8 with a host or unaligned source)
   int8_t* stage8[2] = {nullptr, nullptr};
   int8_t* raw8[2] = {nullptr, nullptr};  // when ld8 != n: rows of n bytes as they arrive, repacked to ld8
@@ -192,11 +190,9 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
   CK(c, cudaStreamCreateWithPriority(&c->own_stream, cudaStreamNonBlocking, prio_hi));
   CK(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
-  CK(c, cudaStreamCreateWithFlags(&c->conv, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->fb, cudaStreamNonBlocking));
   c->stream = c->own_stream;
   for (int k = 0; k < 2; ++k) {
-    CK(c, cudaEventCreateWithFlags(&c->ev_conv[k], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_oz[k], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_fb[k], cudaEventDisableTiming));
     CK(c, cudaEventRecord(c->ev_fb[k], c->own_stream));
@@ -572,7 +568,6 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
   // the block is complete on the compute stream only when its fallback launches are
   CK(c, cudaEventRecord(c->ev_fb[0], c->fb));
   CK(c, cudaStreamWaitEvent(c->stream, c->ev_fb[0], 0));
-  c->oseq += nchunks;
   return GLS_OK;
 }
 
@@ -709,7 +704,6 @@ int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, d
 
 int sync_all(gls_ctx* c) {
   CK(c, cudaStreamSynchronize(c->h2d));
-  CK(c, cudaStreamSynchronize(c->conv));
   CK(c, cudaStreamSynchronize(c->fb));
   CK(c, cudaStreamSynchronize(c->stream));
   CK(c, cudaStreamSynchronize(c->d2h));
@@ -955,7 +949,6 @@ void gls_destroy(gls_ctx* c) {
   DeviceGuard g(c->device);
   // every stream that may still read or write context buffers, before the stream-ordered frees
   if (c->h2d) cudaStreamSynchronize(c->h2d);
-  if (c->conv) cudaStreamSynchronize(c->conv);
   if (c->fb) cudaStreamSynchronize(c->fb);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->d2h) cudaStreamSynchronize(c->d2h);
@@ -989,11 +982,9 @@ void gls_destroy(gls_ctx* c) {
     if (c->ev_h2d[k]) cudaEventDestroy(c->ev_h2d[k]);
     if (c->ev_comp[k]) cudaEventDestroy(c->ev_comp[k]);
     if (c->ev_d2h[k]) cudaEventDestroy(c->ev_d2h[k]);
-    if (c->ev_conv[k]) cudaEventDestroy(c->ev_conv[k]);
     if (c->ev_oz[k]) cudaEventDestroy(c->ev_oz[k]);
     if (c->ev_fb[k]) cudaEventDestroy(c->ev_fb[k]);
   }
-  if (c->conv) cudaStreamDestroy(c->conv);
   if (c->fb) cudaStreamDestroy(c->fb);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   if (c->h2d) cudaStreamDestroy(c->h2d);
