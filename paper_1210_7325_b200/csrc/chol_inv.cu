@@ -51,21 +51,12 @@ __global__ void maxdiag_kernel(int64_t n, const double* A, int64_t ld, CholStatu
 // loaded into registers before the stores), and the scaled column / row is written back during
 // the next column's step.  Writes L into A's lower
 // triangle and T = L^{-1} (zeros above the diagonal).
-__global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A, double* T, int64_t ld,
-                                                     int64_t goff, CholStatus* st) {
-  extern __shared__ double leaf_smem[];
-  double* L = leaf_smem;
-  double* Ti = leaf_smem + LEAF * LLD;
-  __shared__ int failed;
+// The column sweep of a leaf on shared-memory copies: L (lower nb x nb, zeros above) becomes L_jj's
+// Cholesky factor and Ti (= I on entry) its inverse.  Every thread of the block must call it; it ends
+// with a barrier.
+__device__ void leaf_sweep(int nb, double* L, double* Ti, double tol, int64_t goff, CholStatus* st,
+                           int* failed) {
   const int tid = threadIdx.x;
-  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-    const int i = idx % nb, j = idx / nb;
-    L[i * LLD + j] = (i >= j) ? A[i + (int64_t)j * ld] : 0.0;
-    Ti[i * LLD + j] = (i == j) ? 1.0 : 0.0;
-  }
-  if (tid == 0) failed = 0;
-  __syncthreads();
-  const double tol = st->tol;
   const int ty = tid >> 5, tx = tid & 31;
   constexpr int RY = LEAF / LEAF_TY;  // rows per thread
   constexpr int R = LEAF / 32;        // columns per thread
@@ -76,7 +67,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A,
     // pivot (one lane per warp takes the square root and the reciprocal; shuffles broadcast them --
     // the FP64 pipe is too slow for 1024 redundant sqrt/div per column)
     const double d = L[j * LLD + j];
-    const bool bad = !(d > tol) || failed;
+    const bool bad = !(d > tol) || *(volatile int*)failed;
     double ljj = 0.0, rinv = 0.0;
     if ((tid & 31) == 0) {  // rsqrt and one multiply: a shorter FP64 chain than sqrt + divide
       rinv = bad ? __longlong_as_double(0x7ff8000000000000LL) : rsqrt(d);  // NaN poisons the rest
@@ -84,9 +75,9 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A,
     }
     ljj = __shfl_sync(0xffffffffu, ljj, 0);
     rinv = __shfl_sync(0xffffffffu, rinv, 0);
-    if (tid == 0 && bad && !failed) {
+    if (tid == 0 && bad && !*failed) {
       atomicMin(&st->fail, (unsigned long long)(goff + j));
-      failed = 1;  // read by every thread after this step's barrier
+      *failed = 1;  // read by every thread after this step's barrier
     }
     // deferred write-back of step j-1: column j-1 of L (rows >= j-1) and row j-1 of T, scaled
     if (j > 0) {
@@ -136,10 +127,124 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A,
     }
     __syncthreads();
   }
+}
+
+// One CTA: Cholesky of the nb x nb diagonal block at A (lower read) and, in the same sweep, its
+// inverse by forward elimination on [L | I]: after column j of L is final, row j of T is
+// T[j,:] /= L_jj and every later row is updated T[i,:] -= L_ij T[j,:] (i > j), so that on exit
+// L T = I.  One barrier per column: every warp forms L_jj = sqrt(d_j) itself, the rank-1 updates
+// read column j of L / row j of T scaled on the fly (operands of each thread's at most 2 x 2 items
+// loaded into registers before the stores), and the scaled column / row is written back during
+// the next column's step.  Writes L into A's lower
+// triangle and T = L^{-1} (zeros above the diagonal).
+__global__ void __launch_bounds__(LEAF_THREADS) chol_inv_leaf(int nb, double* A, double* T, int64_t ld,
+                                                     int64_t goff, CholStatus* st) {
+  extern __shared__ double leaf_smem[];
+  double* L = leaf_smem;
+  double* Ti = leaf_smem + LEAF * LLD;
+  __shared__ int failed;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+    const int i = idx % nb, j = idx / nb;
+    L[i * LLD + j] = (i >= j) ? A[i + (int64_t)j * ld] : 0.0;
+    Ti[i * LLD + j] = (i == j) ? 1.0 : 0.0;
+  }
+  if (tid == 0) failed = 0;
+  __syncthreads();
+  leaf_sweep(nb, L, Ti, st->tol, goff, st, &failed);
   for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
     const int i = idx % nb, j = idx / nb;
     if (i >= j) A[i + (int64_t)j * ld] = L[i * LLD + j];
     T[i + (int64_t)j * ld] = (i >= j) ? Ti[i * LLD + j] : 0.0;
+  }
+}
+
+// 64 x 64 product on shared-memory blocks (row stride LLD), 512 threads, 8 outputs per thread
+// (rows ty + 16 a, columns tx + 32 b): out[i][k] = sum_m A(i, m) B(m, k) with the operand accessors
+// given; OP receives (i, k, value).
+template <class FA, class FB, class OP>
+__device__ __forceinline__ void smem_gemm64(FA fa, FB fb, OP op) {
+  const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+  double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll 4
+  for (int m = 0; m < LEAF; ++m) {
+    double a[4], bv[2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = fa(ty + 16 * u, m);
+#pragma unroll
+    for (int v = 0; v < 2; ++v) bv[v] = fb(m, tx + 32 * v);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) acc[u][v] = fma(a[u], bv[v], acc[u][v]);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) op(ty + 16 * u, tx + 32 * v, acc[u][v]);
+}
+
+// A node of n = 64 + h2 (0 < h2 <= 64) rows in one CTA: the recursion's two leaves and its four
+// small products (L21 = A21 T11^T, A22 -= L21 L21^T, Y = L21 T11, T21 = -T22 Y) on shared-memory
+// blocks -- one launch instead of two leaves, three main-stream GEMMs and an aux-stream GEMM.
+__global__ void __launch_bounds__(LEAF_THREADS) chol_inv_node128(int n, double* A, double* T, int64_t ld,
+                                                        int64_t goff, CholStatus* st) {
+  extern __shared__ double leaf_smem[];
+  constexpr int B = LEAF * LLD;
+  double* L1 = leaf_smem;       // A11 -> L11
+  double* T1 = L1 + B;          // I -> T11
+  double* P = T1 + B;           // A21, later Y
+  double* Q = P + B;            // L21
+  double* L2 = Q + B;           // A22 -> L22
+  double* T2 = L2 + B;          // I -> T22
+  __shared__ int failed;
+  const int tid = threadIdx.x;
+  const int h2 = n - LEAF;
+  double* A21 = A + LEAF;
+  double* A22 = A + LEAF + (int64_t)LEAF * ld;
+  for (int idx = tid; idx < LEAF * LEAF; idx += blockDim.x) {
+    const int i = idx % LEAF, j = idx / LEAF;
+    L1[i * LLD + j] = (i >= j) ? A[i + (int64_t)j * ld] : 0.0;
+    T1[i * LLD + j] = (i == j) ? 1.0 : 0.0;
+    P[i * LLD + j] = (i < h2) ? A21[i + (int64_t)j * ld] : 0.0;
+    L2[i * LLD + j] = (i < h2 && j <= i) ? A22[i + (int64_t)j * ld] : 0.0;
+    T2[i * LLD + j] = (i == j && i < h2) ? 1.0 : 0.0;
+  }
+  if (tid == 0) failed = 0;
+  __syncthreads();
+  const double tol = st->tol;
+  leaf_sweep(LEAF, L1, T1, tol, goff, st, &failed);
+  // L21 = A21 T11^T  (T11 is zero above its diagonal)
+  smem_gemm64([&](int i, int m) { return P[i * LLD + m]; }, [&](int m, int k) { return T1[k * LLD + m]; },
+              [&](int i, int k, double v) { Q[i * LLD + k] = v; });
+  __syncthreads();
+  // A22 -= L21 L21^T (lower triangle)
+  smem_gemm64([&](int i, int m) { return Q[i * LLD + m]; }, [&](int m, int k) { return Q[k * LLD + m]; },
+              [&](int i, int k, double v) {
+                if (k <= i) L2[i * LLD + k] -= v;
+              });
+  __syncthreads();
+  leaf_sweep(h2, L2, T2, tol, goff + LEAF, st, &failed);
+  // Y = L21 T11 (into P: A21 is no longer needed)
+  smem_gemm64([&](int i, int m) { return Q[i * LLD + m]; }, [&](int m, int k) { return T1[m * LLD + k]; },
+              [&](int i, int k, double v) { P[i * LLD + k] = v; });
+  __syncthreads();
+  // T21 = -T22 Y, straight to global memory
+  smem_gemm64([&](int i, int m) { return T2[i * LLD + m]; }, [&](int m, int k) { return P[m * LLD + k]; },
+              [&](int i, int k, double v) {
+                if (i < h2) T[LEAF + i + (int64_t)k * ld] = -v;
+              });
+  for (int idx = tid; idx < LEAF * LEAF; idx += blockDim.x) {
+    const int i = idx % LEAF, j = idx / LEAF;
+    if (i >= j) A[i + (int64_t)j * ld] = L1[i * LLD + j];
+    T[i + (int64_t)j * ld] = (i >= j) ? T1[i * LLD + j] : 0.0;
+    if (i < h2) {
+      A21[i + (int64_t)j * ld] = Q[i * LLD + j];
+      if (j < h2) {
+        if (i >= j) A22[i + (int64_t)j * ld] = L2[i * LLD + j];
+        T[LEAF + i + (int64_t)(LEAF + j) * ld] = (i >= j) ? T2[i * LLD + j] : 0.0;
+      }
+    }
   }
 }
 
@@ -206,6 +311,17 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
     if (rest_ready) cudaStreamWaitEvent(s, rest_ready, 0);
     mark(s, depth, "wait-rest");
     chol_inv_leaf<<<1, LEAF_THREADS, kLeafSmem, s>>>((int)n, A, T, ld, goff, rc.st);
+    if (rc.lc) ++*rc.lc;
+    mark(s, depth, "leaf");
+    return;
+  }
+  if (n <= 2 * LEAF && first_block(n) == LEAF) {  // both leaves and the node's products in one CTA
+    constexpr int kNodeSmem = 6 * LEAF * LLD * sizeof(double);
+    if (first_use_on_device((const void*)chol_inv_node128))
+      cudaFuncSetAttribute(chol_inv_node128, cudaFuncAttributeMaxDynamicSharedMemorySize, kNodeSmem);
+    if (rest_ready) cudaStreamWaitEvent(s, rest_ready, 0);
+    mark(s, depth, "wait-rest");
+    chol_inv_node128<<<1, LEAF_THREADS, kNodeSmem, s>>>((int)n, A, T, ld, goff, rc.st);
     if (rc.lc) ++*rc.lc;
     mark(s, depth, "leaf");
     return;
