@@ -13,7 +13,13 @@
 namespace gls {
 namespace {
 
-constexpr int BM = 128, BN = 64, BK = 16, LDS_ = 20, STAGES = 3, THREADS = 256;
+#ifndef GLS_DGEMM_BK
+#define GLS_DGEMM_BK 16
+#endif
+#ifndef GLS_DGEMM_STAGES
+#define GLS_DGEMM_STAGES 3
+#endif
+constexpr int BM = 128, BN = 64, BK = GLS_DGEMM_BK, LDS_ = BK + 4, STAGES = GLS_DGEMM_STAGES, THREADS = 256;
 constexpr int A_TILE = BM * LDS_, B_TILE = BN * LDS_;
 constexpr int SMEM_BYTES = STAGES * (A_TILE + B_TILE) * 8;
 
@@ -120,7 +126,7 @@ __global__ void __launch_bounds__(THREADS, 2) dgemm_kernel(GemmParams p) {
     const double* as = As + (kt % STAGES) * A_TILE;
     const double* bs = Bs + (kt % STAGES) * B_TILE;
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
+    for (int ks = 0; ks < BK / 4; ++ks) {
       double a[4], b[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) a[t] = as[(wm * 32 + t * 8 + l4) * LDS_ + ks * 4 + kk];
