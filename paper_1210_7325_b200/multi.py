@@ -11,6 +11,8 @@ Only host-side plumbing lives here; every arithmetic step runs in libgls.so.
 """
 from __future__ import annotations
 
+import os
+
 
 def snp_range(m_total: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous problem range [lo, hi) of `rank` when m_total problems are split over `world`
@@ -18,6 +20,13 @@ def snp_range(m_total: int, world: int, rank: int) -> tuple[int, int]:
     if world < 1 or not (0 <= rank < world) or m_total < 0:
         raise ValueError("bad shard arguments")
     return (rank * m_total) // world, ((rank + 1) * m_total) // world
+
+
+def local_device(env=None) -> int:
+    """CUDA device of this process: LOCAL_RANK (torchrun sets it per node), so the same code runs on
+    one node or several -- the SNP shard follows the global rank, the device the local one."""
+    env = os.environ if env is None else env
+    return int(env.get("LOCAL_RANK", "0"))
 
 
 def weak_range(m_per_rank: int, rank: int) -> tuple[int, int]:

@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1210_7325_b200.multi import max_over_ranks, replicate_shared, snp_range, weak_range
+from paper_1210_7325_b200.multi import local_device, max_over_ranks, replicate_shared, snp_range, weak_range
 
 
 class FakeCtx:
@@ -92,3 +92,49 @@ def test_weak_range():
     assert weak_range(1_000_000, 7) == (7_000_000, 8_000_000)
     with pytest.raises(ValueError):
         snp_range(10, 2, 2)
+
+
+def _worker_2x2(rank, world, port, q):
+    """One rank of a 2-node x 2-GPU layout as torchrun --nnodes 2 --nproc-per-node 2 sets it up."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["LOCAL_RANK"] = str(rank % 2)
+    os.environ["LOCAL_WORLD_SIZE"] = "2"
+    os.environ["GROUP_RANK"] = str(rank // 2)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx = FakeCtx(root=(rank == 0))
+        replicate_shared(ctx, dist, src=0)
+        ref = FakeCtx(root=True)
+        same = all(torch.equal(a, b) for a, b in zip(ctx.bufs, ref.bufs))
+        t = max_over_ranks([float(rank)], dist)
+        q.put((rank, same, ctx.committed, local_device(), weak_range(1000, rank), t))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_replicate_and_shard_two_nodes_gloo():
+    """NEXT-3 host side: the protocol spans nodes unchanged -- rank 0 on node 0 broadcasts to the
+    ranks of both nodes, every rank's device is its LOCAL_RANK, its SNP shard follows its global
+    rank, and timings reduce over all four ranks."""
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_2x2, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, same, committed, dev, rng, t in res:
+        assert same and committed
+        assert dev == rank % 2
+        assert rng == (1000 * rank, 1000 * (rank + 1))
+        assert t == [3.0]
+
+
+def test_local_device_env():
+    assert local_device({}) == 0
+    assert local_device({"LOCAL_RANK": "3"}) == 3
