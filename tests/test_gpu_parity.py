@@ -220,11 +220,14 @@ def test_host_stream_equals_device_bitwise(glsmod):
         ctx.close()
 
 
-def test_not_spd_pivot_matches_oracle(glsmod):
+@pytest.mark.parametrize("piv", [5, 100, 200, 260, 299])
+def test_not_spd_pivot_matches_oracle(glsmod, piv):
+    """The first failing pivot, wherever it falls: a 64-row leaf, the first or the second sweep of a
+    fused 65-128-row node (n = 300 splits 192 = 128 + 64, then 108 = 64 + 44), the last row."""
     n = 300
     P = gen.make_problem(n, 3, 1, seed=4)
     M = P.M.copy()
-    M[200, 200] = -1.0  # first 200 pivots fine, pivot 200 negative
+    M[piv, piv] = -1.0  # the first piv pivots fine, pivot piv negative
     with pytest.raises(oracle.NotSPD) as ei:
         oracle.cholesky(M)
     with pytest.raises(glsmod.GLSError) as eg:
@@ -241,7 +244,7 @@ def test_not_spd_pivot_matches_oracle(glsmod):
     ctx_pivot = L.gls_failed_pivot(h)
     assert L.gls_solve_block(h, yd.data_ptr(), 1, yd.data_ptr()) == 6  # GLS_ERR_STATE
     L.gls_destroy(h)
-    assert ctx_pivot == ei.value.pivot == 200
+    assert ctx_pivot == ei.value.pivot == piv
 
 
 def test_rank_deficient_isolation(glsmod):
