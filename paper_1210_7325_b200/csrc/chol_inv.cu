@@ -12,6 +12,7 @@
 // Leaves (n <= 64) factor and invert one diagonal block inside one CTA in a single sweep.
 // NotSPD (reading A5): a pivot d_j <= 2^-52 * max_k M_kk records min(j) in st->fail.
 #include <climits>
+#include <cstdlib>
 #include <vector>
 
 #include "gls_internal.cuh"
@@ -312,6 +313,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_node128(int n, double* 
 // its own split-K workspace.
 constexpr int kMaxDepth = 24;
 constexpr int64_t kLookaheadMin = 1024;  // smallest trailing node split for look-ahead
+constexpr int kFreeSms = 16;             // SMs the off-critical-path GEMMs leave free
 struct RecCtx {
   cudaStream_t s;
   cudaStream_t side[kMaxDepth], aux[kMaxDepth];
@@ -321,6 +323,7 @@ struct RecCtx {
   std::vector<cudaEvent_t>* events;
   CholStatus* st;
   int64_t* lc;
+  int off_ctas;  // grid cap of the off-critical-path GEMMs (look-ahead and Y; 0: none)
 };
 
 // GLS_TRACE_CHOL=1 (diagnostics): timing events on the main stream after every step, printed per
@@ -411,19 +414,21 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
   if (h2 > g) {
     cudaStreamWaitEvent(sd, e_start, 0);
     dgemm(sd, h2 - g, h1, h1, 1.0, A21 + g, ld, 'N', T11, ld, 'T', 0.0, T21 + g, ld, GEMM_KMAX_COL, rc.lc,
-          rc.ws_side[d]);
+          rc.ws_side[d], rc.off_ctas);
     cudaStreamWaitEvent(sd, e_top, 0);
     // rows [g, h2) of the lower triangle: columns [0, g) full, [g, h2) lower
-    dgemm(sd, h2 - g, g, h1, -1.0, T21 + g, ld, 'N', T21, ld, 'T', 1.0, A22 + g, ld, 0, rc.lc, rc.ws_side[d]);
+    dgemm(sd, h2 - g, g, h1, -1.0, T21 + g, ld, 'N', T21, ld, 'T', 1.0, A22 + g, ld, 0, rc.lc, rc.ws_side[d],
+          rc.off_ctas);
     dgemm(sd, h2 - g, h2 - g, h1, -1.0, T21 + g, ld, 'N', T21 + g, ld, 'T', 1.0, A22 + g + g * ld, ld,
-          GEMM_LOWER_C, rc.lc, rc.ws_side[d]);
+          GEMM_LOWER_C, rc.lc, rc.ws_side[d], rc.off_ctas);
     e_rest = record(rc, sd);
   }
   // Y = L21 T11 -> A21's place, on the aux stream (after every read of A21 and every write of L21)
   cudaStream_t sa = rc.aux[d];
   cudaStreamWaitEvent(sa, record(rc, s), 0);
   if (e_rest) cudaStreamWaitEvent(sa, e_rest, 0);
-  dgemm(sa, h2, h1, h1, 1.0, T21, ld, 'N', T11, ld, 'N', 0.0, A21, ld, GEMM_KMIN_COL, rc.lc, rc.ws_aux[d]);
+  dgemm(sa, h2, h1, h1, 1.0, T21, ld, 'N', T11, ld, 'N', 0.0, A21, ld, GEMM_KMIN_COL, rc.lc, rc.ws_aux[d],
+        rc.off_ctas);
   cudaEvent_t e_y = record(rc, sa);
   chol_inv_rec(rc, h2, A22, T22, ld, goff + h1, e_rest, depth + 1);
   // T21 = -T22 Y  (overwrites L21: Y, and with it every reader of L21, must be complete)
@@ -453,6 +458,16 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
   rc.events = &events;
   rc.st = st;
   rc.lc = lc;
+  {
+    // The look-ahead GEMMs and Y (needed only at the end of their node) walk their tiles on a grid
+    // that leaves kFreeSms SMs to the critical path: their long CTAs would otherwise hold back its
+    // small kernels (a 128 x 128 x 128 product took 140 us instead of 10 behind a 5000^3 Y)
+    int dev0 = 0, sms = 148;
+    cudaGetDevice(&dev0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev0);
+    static const int freeq = getenv("GLS_CHOL_FREE_SMS") ? atoi(getenv("GLS_CHOL_FREE_SMS")) : kFreeSms;
+    rc.off_ctas = freeq > 0 && sms > freeq ? 2 * (sms - freeq) : 0;  // 2 CTAs per SM
+  }
   // split-K workspaces (main + side and aux per depth) from the stream-ordered pool
   double* ws = nullptr;
   const size_t nws = 1 + 2 * (size_t)depth;

@@ -60,8 +60,12 @@ __global__ void __launch_bounds__(THREADS, 2) dgemm_kernel(GemmParams p) {
   extern __shared__ double sm[];
   double* As = sm;
   double* Bs = sm + STAGES * A_TILE;
-  const int64_t r0 = (int64_t)blockIdx.x * BM, c0 = (int64_t)blockIdx.y * BN;
-  if (tile_skipped(p, r0, c0)) return;
+  // one output tile per CTA on the full grid; a capped grid (dgemm's max_ctas) walks the tiles
+  const int64_t tm = (p.M + BM - 1) / BM, ntiles = tm * ((p.N + BN - 1) / BN);
+  for (int64_t tile = blockIdx.x + (int64_t)blockIdx.y * gridDim.x; tile < ntiles;
+       tile += (int64_t)gridDim.x * gridDim.y) {
+  const int64_t r0 = (tile % tm) * BM, c0 = (tile / tm) * BN;
+  if (tile_skipped(p, r0, c0)) continue;
   int64_t kb = 0, ke = p.K;
   if (p.flags & GEMM_KMIN_COL) kb = (c0 / BK) * BK;
   if (p.flags & GEMM_KMAX_ROW) ke = min(ke, r0 + BM);
@@ -159,6 +163,8 @@ __global__ void __launch_bounds__(THREADS, 2) dgemm_kernel(GemmParams p) {
           }
         }
       }
+  __syncthreads();  // the next tile's prologue reuses the stages
+  }
 }
 
 // C = alpha * sum_z ws[z] + beta * C, splits summed in a fixed order (deterministic).
@@ -272,7 +278,7 @@ void trmm_lower_t_skinny(cudaStream_t s, int64_t n, int k, const double* T, int6
 
 void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, char opA, const double* B, int64_t ldb, char opB, double beta, double* C,
-           int64_t ldc, int flags, int64_t* launch_counter, double* ws) {
+           int64_t ldc, int flags, int64_t* launch_counter, double* ws, int max_ctas) {
   if (M <= 0 || N <= 0) return;
   GemmParams p{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, flags, 1, nullptr};
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
@@ -289,6 +295,7 @@ void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const 
       grid.z = sp;
     }
   }
+  if (max_ctas > 0 && p.nsplit == 1 && tiles > max_ctas) grid = dim3((unsigned)max_ctas);
   const bool ta = (opA == 'T'), tb = (opB == 'T');
   if (!ta && !tb) launch<false, false>(s, grid, p);
   else if (!ta && tb) launch<false, true>(s, grid, p);

@@ -62,7 +62,7 @@ enum GemmFlags : int {
 constexpr size_t kSplitKWsDoubles = (size_t)2 << 20;  // 16 MiB: (148 + 74) tiles x 128 x 64 doubles
 void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, char opA, const double* B, int64_t ldb, char opB, double beta, double* C,
-           int64_t ldc, int flags, int64_t* launch_counter, double* ws = nullptr);
+           int64_t ldc, int flags, int64_t* launch_counter, double* ws = nullptr, int max_ctas = 0);
 
 // Skinny products with a lower-triangular T (k <= 21 columns; memory-bound, deterministic):
 // W = T B (part: scratch of 32 * n * k doubles) and V = T^T W.
