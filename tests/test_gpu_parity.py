@@ -185,6 +185,28 @@ def test_convert_ahead_chunks(glsmod, n):
     assert_parity(b[pick], st[pick], b_or, st_or, label="convert-ahead vs oracle")
 
 
+@pytest.mark.parametrize("n,pL,pR,m", [(4100, 0, 20, 2500), (5000, 19, 1, 70000)])
+def test_large_p_with_convert_ahead(glsmod, n, pL, pR, m):
+    """p = 20 at n >= 4096: the 21-accumulator kernels, the separate batched posv (p > 8) and the
+    convert-ahead chunks together.  All rows against the FP64 path, sampled groups against the
+    oracle."""
+    P = gen.make_problem(n, pL, pR, seed=43)
+    cols = m * pR
+    Xd = torch.empty((cols, n), dtype=torch.float64, device="cuda")
+    for c in range(0, cols, 16384):
+        k = min(16384, cols - c)
+        glsmod.gen_xr_device(43, n, c, k, Xd[c:c + k])
+    counts = []
+    b, st, _ = run_gpu(glsmod, P, Xd, m, pR, counts=counts)
+    assert counts[1] == 0 and counts[0] >= 3, counts  # int8 only, several chunks
+    b64, st64, _ = run_gpu(glsmod, P, Xd, m, pR, path=glsmod.GLS_PATH_FP64)
+    assert_parity(b, st, b64, st64, label="int8 vs FP64 path")
+    pick = [0, 1, m // 3, m // 2, m - 2, m - 1]
+    XR = torch.cat([Xd[g * pR:(g + 1) * pR] for g in pick]).cpu().numpy()
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, pR)
+    assert_parity(b[pick], st[pick], b_or, st_or, label="vs oracle")
+
+
 def test_host_stream_equals_device_bitwise(glsmod):
     """Host-resident X_R (Alg. 8 double-buffered stream) gives the same bits as device X_R,
     for several block sizes (block-partition independence)."""
