@@ -663,8 +663,11 @@ int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, d
       c->bstage_groups = chunk_groups;
     }
   }
-  for (int64_t g0 = 0; g0 < m_blk; g0 += chunk_groups) {
-    const int64_t gc = (m_blk - g0 < chunk_groups) ? m_blk - g0 : chunk_groups;
+  // a quarter-size first chunk (the warm-up block of §4.3): the first copy is the
+  // one nothing hides
+  const int64_t first = (m_blk > chunk_groups && chunk_groups >= 4) ? chunk_groups / 4 : chunk_groups;
+  for (int64_t g0 = 0, gc = 0; g0 < m_blk; g0 += gc) {
+    gc = std::min<int64_t>(m_blk - g0, g0 == 0 ? first : chunk_groups);
     const int buf = (int)(c->seq++ & 1);
     CK(c, cudaStreamWaitEvent(c->h2d, c->ev_comp[buf], 0));
     // contiguous rows whose length is not a multiple of 16 bytes (the TMA row pitch): one linear copy
