@@ -19,7 +19,13 @@ namespace {
 #ifndef GLS_DGEMM_STAGES
 #define GLS_DGEMM_STAGES 3
 #endif
-constexpr int BM = 128, BN = 64, BK = GLS_DGEMM_BK, LDS_ = BK + 4, STAGES = GLS_DGEMM_STAGES, THREADS = 256;
+#ifndef GLS_DGEMM_BN
+#define GLS_DGEMM_BN 64
+#endif
+constexpr int BM = 128, BN = GLS_DGEMM_BN, BK = GLS_DGEMM_BK, LDS_ = BK + 4, STAGES = GLS_DGEMM_STAGES,
+              THREADS = 256;
+// warp grid: 8 warps as WM x WN, warp tile (BM / WM) x (BN / WN) = TM x TN DMMA 8x8 tiles
+constexpr int WM = BN == 64 ? 4 : 2, WN = 8 / WM, TM = BM / WM / 8, TN = BN / WN / 8;
 constexpr int A_TILE = BM * LDS_, B_TILE = BN * LDS_;
 constexpr int SMEM_BYTES = STAGES * (A_TILE + B_TILE) * 8;
 
@@ -56,7 +62,7 @@ __device__ __forceinline__ bool tile_skipped(const GemmParams& p, int64_t r0, in
 }
 
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(THREADS, 2) dgemm_kernel(GemmParams p) {
+__global__ void __launch_bounds__(THREADS, BN == 64 ? 2 : 1) dgemm_kernel(GemmParams p) {
   extern __shared__ double sm[];
   double* As = sm;
   double* Bs = sm + STAGES * A_TILE;
@@ -81,7 +87,7 @@ __global__ void __launch_bounds__(THREADS, 2) dgemm_kernel(GemmParams p) {
   }
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 3, wn = warp >> 2;
+  const int wm = warp % WM, wn = warp / WM;
 
   auto issue = [&](int kt, int stg) {
     const int64_t k0 = kb + (int64_t)kt * BK;
@@ -109,11 +115,11 @@ __global__ void __launch_bounds__(THREADS, 2) dgemm_kernel(GemmParams p) {
     }
   };
 
-  double acc[4][4][2];
+  double acc[TM][TN][2];
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+  for (int t = 0; t < TM; ++t)
 #pragma unroll
-    for (int s = 0; s < 4; ++s) acc[t][s][0] = acc[t][s][1] = 0.0;
+    for (int s = 0; s < TN; ++s) acc[t][s][0] = acc[t][s][1] = 0.0;
 
   const int l4 = lane >> 2, kk = lane & 3;
 #pragma unroll
@@ -131,27 +137,27 @@ __global__ void __launch_bounds__(THREADS, 2) dgemm_kernel(GemmParams p) {
     const double* bs = Bs + (kt % STAGES) * B_TILE;
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
-      double a[4], b[4];
+      double a[TM], b[TN];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) a[t] = as[(wm * 32 + t * 8 + l4) * LDS_ + ks * 4 + kk];
+      for (int t = 0; t < TM; ++t) a[t] = as[(wm * TM * 8 + t * 8 + l4) * LDS_ + ks * 4 + kk];
 #pragma unroll
-      for (int s = 0; s < 4; ++s) b[s] = bs[(wn * 32 + s * 8 + l4) * LDS_ + ks * 4 + kk];
+      for (int s = 0; s < TN; ++s) b[s] = bs[(wn * TN * 8 + s * 8 + l4) * LDS_ + ks * 4 + kk];
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < TM; ++t)
 #pragma unroll
-        for (int s = 0; s < 4; ++s) dmma(acc[t][s], a[t], b[s]);
+        for (int s = 0; s < TN; ++s) dmma(acc[t][s], a[t], b[s]);
     }
   }
   cp_async_wait<0>();
   // epilogue: lane holds C[m = l4][n = 2kk + e] of each 8x8 tile
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+  for (int t = 0; t < TM; ++t)
 #pragma unroll
-    for (int s = 0; s < 4; ++s)
+    for (int s = 0; s < TN; ++s)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int64_t gm = r0 + wm * 32 + t * 8 + l4;
-        const int64_t gn = c0 + wn * 32 + s * 8 + 2 * kk + e;
+        const int64_t gm = r0 + wm * TM * 8 + t * 8 + l4;
+        const int64_t gn = c0 + wn * TN * 8 + s * 8 + 2 * kk + e;
         if (gm < p.M && gn < p.N) {
           if (p.nsplit > 1) {
             p.ws[(int64_t)blockIdx.z * p.M * p.N + gm + gn * p.M] = acc[t][s][e];
