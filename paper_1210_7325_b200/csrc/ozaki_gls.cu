@@ -246,11 +246,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // tiles, into TMEM columns [0, 224) and [256, 480).  The step after the last is the V block.  The
   // accumulator region is single-buffered: the next step's MMAs wait until both epilogues drained it.
   const int nsteps = (kp.NBR + 1) / 2;
-  // Split completion (light epilogues): region 0 gets its own tfull commit and the MMAs of region 1's
-  // last ST-1 stages are deferred on purpose, so region 0's drain overlaps region 1's tail MMAs and the
-  // next step's region-0 MMAs queue behind that tail.  Measured +1 % on config 2; the heavy-epilogue
-  // variants (NA = 21) lose 1 % with it and keep one commit per step.
-  constexpr bool kSplit = NA <= 8;
+  // Split completion: region 0 gets its own tfull commit and the MMAs of region 1's last ST-1 stages
+  // are deferred on purpose, so region 0's drain overlaps region 1's tail MMAs and the next step's
+  // region-0 MMAs queue behind that tail.  Measured ~+1 % on configs 2 and 3 (for the 21-accumulator
+  // variants only since their epilogue stopped being the bottleneck).
+  constexpr bool kSplit = true;
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
