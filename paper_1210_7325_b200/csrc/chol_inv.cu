@@ -324,7 +324,16 @@ struct RecCtx {
   CholStatus* st;
   int64_t* lc;
   int off_ctas;  // grid cap of the off-critical-path GEMMs (look-ahead and Y; 0: none)
+  const ColsReady* arriving;  // nullable: A's columns still being uploaded
 };
+
+// stream st may touch columns [0, c) of A only after their upload chunks have landed
+void wait_cols(const RecCtx& rc, cudaStream_t st, int64_t c) {
+  if (!rc.arriving || c <= 0) return;
+  int64_t k = (c - 1) / rc.arriving->cols;
+  if (k >= rc.arriving->nchunks) k = rc.arriving->nchunks - 1;
+  cudaStreamWaitEvent(st, rc.arriving->ready[k], 0);
+}
 
 // GLS_TRACE_CHOL=1 (diagnostics): timing events on the main stream after every step, printed per
 // (depth, step) at the end of chol_inv.
@@ -370,6 +379,7 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
     if (first_use_on_device((const void*)chol_inv_leaf))
       cudaFuncSetAttribute(chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
     if (rest_ready) cudaStreamWaitEvent(s, rest_ready, 0);
+    wait_cols(rc, s, goff + n);
     mark(s, depth, "wait-rest");
     chol_inv_leaf<<<1, LEAF_THREADS, kLeafSmem, s>>>((int)n, A, T, ld, goff, rc.st);
     if (rc.lc) ++*rc.lc;
@@ -381,6 +391,7 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
     if (first_use_on_device((const void*)chol_inv_node128))
       cudaFuncSetAttribute(chol_inv_node128, cudaFuncAttributeMaxDynamicSharedMemorySize, kNodeSmem);
     if (rest_ready) cudaStreamWaitEvent(s, rest_ready, 0);
+    wait_cols(rc, s, goff + n);
     mark(s, depth, "wait-rest");
     chol_inv_node128<<<1, LEAF_THREADS, kNodeSmem, s>>>((int)n, A, T, ld, goff, rc.st);
     if (rc.lc) ++*rc.lc;
@@ -407,6 +418,7 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
   dgemm(s, g, h1, h1, 1.0, A21, ld, 'N', T11, ld, 'T', 0.0, T21, ld, GEMM_KMAX_COL, rc.lc, rc.ws_main);
   mark(s, depth, "L21top");
   cudaEvent_t e_top = record(rc, s);
+  wait_cols(rc, s, goff + h1 + g);
   dgemm(s, g, g, h1, -1.0, T21, ld, 'N', T21, ld, 'T', 1.0, A22, ld, GEMM_LOWER_C, rc.lc, rc.ws_main);
   mark(s, depth, "SYRK11");
   cudaEvent_t e_rest = nullptr;
@@ -416,6 +428,7 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
     dgemm(sd, h2 - g, h1, h1, 1.0, A21 + g, ld, 'N', T11, ld, 'T', 0.0, T21 + g, ld, GEMM_KMAX_COL, rc.lc,
           rc.ws_side[d], rc.off_ctas);
     cudaStreamWaitEvent(sd, e_top, 0);
+    wait_cols(rc, sd, goff + n);
     // rows [g, h2) of the lower triangle: columns [0, g) full, [g, h2) lower
     dgemm(sd, h2 - g, g, h1, -1.0, T21 + g, ld, 'N', T21, ld, 'T', 1.0, A22 + g, ld, 0, rc.lc, rc.ws_side[d],
           rc.off_ctas);
@@ -447,7 +460,7 @@ void chol_prepare(cudaStream_t s, int64_t n, const double* A, int64_t ld, CholSt
 }
 
 void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholStatus* st,
-              int64_t* lc) {
+              int64_t* lc, const ColsReady* arriving) {
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least urgent
   int depth = 1;
@@ -458,6 +471,7 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
   rc.events = &events;
   rc.st = st;
   rc.lc = lc;
+  rc.arriving = arriving && arriving->nchunks > 0 ? arriving : nullptr;
   {
     // The look-ahead GEMMs and Y (needed only at the end of their node) walk their tiles on a grid
     // that leaves kFreeSms SMs to the critical path: their long CTAs would otherwise hold back its

@@ -288,11 +288,41 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   CKS(dalloc(c, &st, sizeof(CholStatus)));
   if (c->oz_ok) CKS(dalloc(c, &esc, (size_t)((n + kOzR - 1) / kOzR) * kOzR * sizeof(int)));
   mark("alloc");
-  CKS(cudaMemcpyAsync(A, M, nn, cudaMemcpyDefault, s));
-  CKS(cudaMemsetAsync(T, 0, nn, s));
+  // A host M is uploaded in column chunks on the h2d stream while the factorisation runs: the
+  // recursion works left to right and waits for the chunks each kernel touches, so only the first
+  // chunk's copy is exposed.  The NotSPD tolerance (max of the diagonal) is then taken on the host.
+  ColsReady arriving;
+  std::vector<cudaEvent_t> col_ev;
+  const bool m_host = !is_device_ptr(M) && n >= kUploadChunkCols * 2;
+  if (m_host) {
+    double mx = 0.0;
+    for (int64_t k = 0; k < n; ++k) mx = std::fmax(mx, M[k + k * n]);
+    CholStatus h0;
+    h0.tol = std::ldexp(1.0, -52) * mx;
+    h0.fail = ULLONG_MAX;
+    CKS(cudaMemcpyAsync(st, &h0, sizeof h0, cudaMemcpyHostToDevice, s));
+    CKS(cudaStreamSynchronize(s));  // h0 lives on this stack frame; the allocations are in place too
+    const int64_t nch = (n + kUploadChunkCols - 1) / kUploadChunkCols;
+    col_ev.resize((size_t)nch);
+    for (int64_t k = 0; k < nch; ++k) {
+      const int64_t c0 = k * kUploadChunkCols, c1 = std::min(n, c0 + kUploadChunkCols);
+      CKS(cudaEventCreateWithFlags(&col_ev[(size_t)k], cudaEventDisableTiming));
+      CKS(cudaMemcpyAsync(A + c0 * n, M + c0 * n, (size_t)(c1 - c0) * n * sizeof(double), cudaMemcpyHostToDevice,
+                          c->h2d));
+      CKS(cudaEventRecord(col_ev[(size_t)k], c->h2d));
+    }
+    arriving.cols = kUploadChunkCols;
+    arriving.ready = col_ev.data();
+    arriving.nchunks = nch;
+    CKS(cudaMemsetAsync(T, 0, nn, s));
+  } else {
+    CKS(cudaMemcpyAsync(A, M, nn, cudaMemcpyDefault, s));
+    CKS(cudaMemsetAsync(T, 0, nn, s));
+  }
   mark("copy+zero");
-  chol_prepare(s, n, A, n, st, &c->launches);
-  chol_inv(s, n, A, T, n, st, &c->launches);
+  if (!m_host) chol_prepare(s, n, A, n, st, &c->launches);
+  chol_inv(s, n, A, T, n, st, &c->launches, m_host ? &arriving : nullptr);
+  if (m_host) CKS(cudaStreamWaitEvent(s, col_ev.back(), 0));  // M is the caller's again after return
   CKS(cudaGetLastError());
   mark("chol_inv");
   CKS(cudaMemcpyAsync(&hst, st, sizeof hst, cudaMemcpyDeviceToHost, s));
@@ -303,6 +333,7 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
     snprintf(buf, sizeof buf, "M is not SPD: Cholesky pivot %lld <= 2^-52 * max diag",
              (long long)hst.fail);
     c->err = buf;
+    for (auto e : col_ev) cudaEventDestroy(e);
     cleanup();
     return GLS_ERR_NOT_SPD;
   }
@@ -329,6 +360,7 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   }
   CKS(cudaGetLastError());
   CKS(cudaStreamSynchronize(s));
+  for (auto e : col_ev) cudaEventDestroy(e);
   mark("pack");
   cleanup();
   mark("free");

@@ -78,8 +78,16 @@ struct CholStatus {
   double tol;
   unsigned long long fail;  // ULLONG_MAX when no pivot failed
 };
+// Columns of A still arriving (host M uploaded in column chunks on another stream): columns
+// [k cols, (k+1) cols) are in place once ready[k] has fired.  chol_inv makes every stream wait for
+// the chunks a kernel touches before launching it.
+struct ColsReady {
+  int64_t cols = 0;
+  const cudaEvent_t* ready = nullptr;
+  int64_t nchunks = 0;
+};
 void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholStatus* st,
-              int64_t* launch_counter);
+              int64_t* launch_counter, const ColsReady* arriving = nullptr);
 void chol_prepare(cudaStream_t s, int64_t n, const double* A, int64_t ld, CholStatus* st,
                   int64_t* launch_counter);
 
@@ -164,6 +172,7 @@ struct OzArgs {
 constexpr int kOzPosvInKernelMaxP = 8;  // p above this: posv in a separate kernel (oz s_ws)
 constexpr int64_t kConvertAheadMinN = 4096;  // n below this: standalone FP64 -> int8 pass per chunk
 constexpr int64_t kSerialChunkBytes = 1ll << 30;  // int8 workspace per chunk when the passes are standalone
+constexpr int64_t kUploadChunkCols = 512;  // host M reaches the device in chunks of this many columns
 // rows of n int8 codes packed back to back -> the same rows at pitch ld8 (>= n); padding untouched
 void oz_repack_rows(cudaStream_t s, const int8_t* src, int64_t n, int64_t rows, int8_t* dst, int64_t ld8,
                     int64_t* launch_counter);

@@ -440,6 +440,29 @@ def test_api_async_streams_and_errors(glsmod):
         assert L.gls_solve_block_ex(ctx._h, Xd.data_ptr(), m, b1.data_ptr(), None, 7) == 1
 
 
+@pytest.mark.parametrize("n", [1100, 3000])
+def test_host_M_upload_overlapped_bitwise(glsmod, n):
+    """M in (pinned or pageable) host memory reaches the device in 512-column chunks while the
+    factorisation runs, each kernel waiting for the chunks it touches; the NotSPD tolerance comes
+    from the host.  Results must equal those of a device-resident M bit for bit, and a NotSPD pivot
+    in a late chunk must still be reported exactly."""
+    pL, pR, m = 3, 1, 500
+    P = gen.make_problem(n, pL, pR, seed=47)
+    XR = gen.make_XR(47, n, 0, m)
+    Xd = dev(XR)
+    b_dev, st_dev, _ = run_gpu(glsmod, P, Xd, m, pR)
+    for Mh in (torch.from_numpy(P.M).pin_memory(), np.ascontiguousarray(P.M)):
+        with glsmod.Context(n, pL, pR, Mh, dev(P.XL), dev(P.y)) as ctx:
+            b = torch.empty((m, pL + pR), dtype=torch.float64, device="cuda")
+            ctx.solve_block(Xd, m, b)
+            np.testing.assert_array_equal(b.cpu().numpy(), b_dev)
+    M2 = P.M.copy()
+    M2[n - 7, n - 7] = -1.0
+    with pytest.raises(glsmod.GLSError) as eg:
+        glsmod.Context(n, pL, pR, torch.from_numpy(M2).pin_memory(), dev(P.XL), dev(P.y))
+    assert eg.value.code == 3
+
+
 def test_repeated_create_destroy_is_deterministic(glsmod):
     """Pool-allocated contexts: create/solve/destroy three times gives identical bits."""
     n, m = 300, 150
