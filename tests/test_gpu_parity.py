@@ -440,7 +440,7 @@ def test_api_async_streams_and_errors(glsmod):
         assert L.gls_solve_block_ex(ctx._h, Xd.data_ptr(), m, b1.data_ptr(), None, 7) == 1
 
 
-@pytest.mark.parametrize("n", [1100, 3000])
+@pytest.mark.parametrize("n", [1024, 1100, 3000])
 def test_host_M_upload_overlapped_bitwise(glsmod, n):
     """M in (pinned or pageable) host memory reaches the device in 512-column chunks while the
     factorisation runs, each kernel waiting for the chunks it touches; the NotSPD tolerance comes
