@@ -436,9 +436,10 @@ def run_ooc(args, cfg, world, rank, local):
     Md = torch.from_numpy(P.M).cuda()
     XLd = torch.from_numpy(np.ascontiguousarray(P.XL)).cuda()
     yd = torch.from_numpy(P.y).cuda()
+    from paper_1210_7325_b200 import ooc
     props = torch.cuda.get_device_properties(local)
-    # chunk = the library's default host block: 4 waves of 128-column int8 tiles
-    blk_groups = (props.multi_processor_count * 16 * (32 // pR) * pR) // pR
+    # block = the library's default host chunk: 4 waves of 128-column int8 tiles
+    blk_groups = ooc.host_block_groups(props.multi_processor_count, pR)
     try:
         avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
     except (ValueError, OSError):
@@ -464,15 +465,7 @@ def run_ooc(args, cfg, world, rank, local):
         ctx = pkg.Context(n, pL, pR, Md, XLd, yd) if rank == 0 else pkg.Context(n, pL, pR, adopt=True)
         if world > 1:
             multi.replicate_shared(ctx, dist, src=0)
-        ctx.set_block_cols(blk_groups * pR)
-        for j in range(nblk):
-            lo = j * blk_groups
-            cnt = min(blk_groups, m - lo)
-            if args.codes:
-                ctx.solve_block_i8(pool[j % pool_n], cnt, b[lo:lo + cnt], st[lo:lo + cnt], async_=True)
-            else:
-                ctx.solve_block(pool[j % pool_n], cnt, b[lo:lo + cnt], st[lo:lo + cnt], async_=True)
-        ctx.sync()
+        ooc.stream_from_pool(ctx, pool, m, blk_groups, b, st, codes=args.codes)
         launches = ctx.kernel_launches
         ctx.close()
         return launches

@@ -4,8 +4,9 @@ This package holds none of the method's arithmetic: it draws M, X_L, y and the
 X_R genotype columns of BASELINE.json `configs` (recipe in DESIGN.md §"Inputs" and
 SURVEY.md §8(d)) with a counter-based Philox4x32-10 generator implemented in
 `glsgen.c`.  The GPU genotype generator (paper_1210_7325_b200/csrc/gen_device.cu)
-implements the same generator independently; `tests/test_gen_gpu.py` checks the
-two agree bit for bit.
+implements the same generator independently;
+`tests/test_gpu_parity.py::test_device_generator_matches_cpu` checks the two agree bit
+for bit.
 
 Array conventions (column-major, as the C ABI): an n x k column-major matrix is a
 C-contiguous numpy array of shape (k, n) -- row j of the array is column j.

@@ -485,7 +485,9 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
   // split-K workspaces (main + side and aux per depth) from the stream-ordered pool
   double* ws = nullptr;
   const size_t nws = 1 + 2 * (size_t)depth;
-  if (cudaMallocAsync((void**)&ws, nws * kSplitKWsDoubles * sizeof(double), s) != cudaSuccess) {
+  int wsdev = 0;
+  cudaGetDevice(&wsdev);
+  if (gls_pool_alloc((void**)&ws, nws * kSplitKWsDoubles * sizeof(double), wsdev, s) != cudaSuccess) {
     cudaGetLastError();
     ws = nullptr;
   }

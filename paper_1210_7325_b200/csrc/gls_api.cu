@@ -139,29 +139,56 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-// Device memory comes from the device's stream-ordered pool (cudaMallocAsync on the context's own
-// stream); freed blocks stay cached in the pool (release threshold GLS_POOL_KEEP_BYTES, default
-// 32 GiB -- the two FP64 host staging buffers alone are 12 GB at n = 1e4) so a create/destroy cycle
-// does not pay page unmapping and remapping every time (measured: with 8 GiB, destroying a context
-// after a FP64 host-input solve took 0.3-3.6 s and the next solve's first touch ~0.7 s more).
-void configure_pool(int device) {
-  static bool done = false;
-  if (done) return;
-  done = true;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
+// Device memory comes from a private stream-ordered pool per device (cudaMemPoolCreate, created
+// on first use; cudaMallocFromPoolAsync on the context's own stream).  Freed blocks stay cached in
+// it (release threshold GLS_POOL_KEEP_BYTES, default 32 GiB -- the two FP64 host staging buffers
+// alone are 12 GB at n = 1e4) so a create/destroy cycle does not pay page unmapping and remapping
+// every time (measured: with 8 GiB, destroying a context after a FP64 host-input solve took
+// 0.3-3.6 s and the next solve's first touch ~0.7 s more).  Being private, the cache never raises
+// the threshold of the device's default pool that PyTorch and other allocators rely on, and
+// gls_release_cached_memory hands it back to the driver.
+constexpr int kMaxDevices = 64;
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[kMaxDevices] = {};
+
+}  // namespace
+
+namespace gls {
+cudaMemPool_t gls_device_pool(int device) {
+  if (device < 0 || device >= kMaxDevices) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (g_pool[device]) return g_pool[device];
+  cudaMemPoolProps props;
+  memset(&props, 0, sizeof props);
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
     cudaGetLastError();
-    return;
+    return nullptr;
   }
   uint64_t keep = 32ull << 30;
   if (const char* e = getenv("GLS_POOL_KEEP_BYTES")) keep = strtoull(e, nullptr, 10);
   cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   cudaGetLastError();
+  g_pool[device] = pool;
+  return pool;
 }
+
+cudaError_t gls_pool_alloc(void** p, size_t bytes, int device, cudaStream_t s) {
+  cudaMemPool_t pool = gls_device_pool(device);
+  if (!pool) return cudaErrorMemoryAllocation;
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+}  // namespace gls
+
+namespace {
 
 template <typename T>
 cudaError_t dalloc(gls_ctx* c, T** p, size_t bytes) {
-  return cudaMallocAsync((void**)p, bytes, c->own_stream);
+  return gls_pool_alloc((void**)p, bytes, c->device, c->own_stream);
 }
 template <typename T>
 void dfree(gls_ctx* c, T*& p) {
@@ -209,7 +236,6 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
   c->Tpk_bytes = (size_t)tpk_total_tiles(c->NB) * kTileDoubles * sizeof(double);
   c->Wpk_bytes = (size_t)c->NB * wpk_rb_doubles(c->NW) * sizeof(double);
   c->G_bytes = (size_t)(pL + 1) * (pL + 1) * sizeof(double);
-  configure_pool(c->device);
   CK(c, dalloc(c, &c->Tpk, c->Tpk_bytes));
   CK(c, dalloc(c, &c->Wpk, c->Wpk_bytes));
   CK(c, dalloc(c, &c->G, c->G_bytes));
@@ -957,7 +983,18 @@ int gls_sync(gls_ctx* c) {
 
 int gls_set_stream(gls_ctx* c, void* stream) {
   if (!c) return GLS_ERR_ARG;
-  c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+  cudaStream_t next = stream ? (cudaStream_t)stream : c->own_stream;
+  if (next == c->stream) return GLS_OK;
+  // work still pending on the old stream uses the context's scratch buffers (x8, cflags, bscratch,
+  // staging): order the new stream after it, so reuse on the new stream cannot race with it
+  DeviceGuard g(c->device);
+  cudaEvent_t e = nullptr;
+  CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaError_t err = cudaEventRecord(e, c->stream);
+  if (err == cudaSuccess) err = cudaStreamWaitEvent(next, e, 0);
+  cudaEventDestroy(e);
+  if (err != cudaSuccess) return fail_cuda(c, err, "gls_set_stream");
+  c->stream = next;
   return GLS_OK;
 }
 
@@ -970,9 +1007,9 @@ int gls_set_block_cols(gls_ctx* c, int64_t cols) {
 
 int gls_release_cached_memory(void) {
   int dev = 0;
-  cudaMemPool_t pool;
+  cudaMemPool_t pool = nullptr;
   if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
-      cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess || cudaMemPoolTrimTo(pool, 0) != cudaSuccess) {
+      !(pool = gls_device_pool(dev)) || cudaMemPoolTrimTo(pool, 0) != cudaSuccess) {
     cudaGetLastError();
     return GLS_ERR_CUDA;
   }

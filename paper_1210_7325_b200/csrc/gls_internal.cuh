@@ -13,6 +13,11 @@ namespace gls {
 // returns true the first time it is called for (key, current device).
 bool first_use_on_device(const void* key);
 
+// The library's private stream-ordered device pool (one per device, created on first use) and an
+// allocation from it on stream s (gls_api.cu).  Every device buffer of the library comes from here.
+cudaMemPool_t gls_device_pool(int device);
+cudaError_t gls_pool_alloc(void** p, size_t bytes, int device, cudaStream_t s);
+
 // ---------------------------------------------------------------- hot-kernel tiling constants
 // Row block of T / z handled per epilogue ("nb" in DESIGN.md), K extent per pipeline stage.
 constexpr int kNB = 128;         // z rows per row block (4 warp slices x 32)

@@ -85,7 +85,6 @@ struct Workspace {
   // state machine, guarded by the engine mutex: 0 free, 1 loading, 2 loaded, 3 computed, 4 writing
   int state = 0;
   int64_t block = -1;
-  bool failed = false;
 };
 
 }  // namespace
@@ -190,10 +189,15 @@ extern "C" int gls_solve_file(gls_ctx* ctx, const char* xr_path, int64_t xr_offs
       r.bytes_written += blocks[j].cnt * p * (int64_t)sizeof(double);
     }
   } else if (rc == GLS_OK) {
-    // Alg. 8: reader and writer threads service one transfer of each kind at a time, in order
+    // Alg. 8: reader and writer threads service one transfer of each kind at a time, in order.
+    // io_error is sticky: the reader or the writer sets it on a failed transfer and nothing clears
+    // it; the orchestrator checks it after every wait and once more at the end, and on any failure
+    // it stops the helpers instead of handing the workspace to the writer (so no stale or
+    // uninitialised b is ever written, and a failed write cannot be masked by a later read).
     std::mutex mu;
     std::condition_variable cv;
     bool stop = false;
+    bool io_error = false;
     std::thread reader([&] {
       for (size_t j = 0; j < blocks.size(); ++j) {
         Workspace& w = ws[j & 1];
@@ -207,10 +211,11 @@ extern "C" int gls_solve_file(gls_ctx* ctx, const char* xr_path, int64_t xr_offs
         const bool ok = do_read(w, blocks[j]);
         {
           std::lock_guard<std::mutex> lk(mu);
-          w.failed = !ok;
+          if (!ok) io_error = true;
           w.state = 2;
         }
         cv.notify_all();
+        if (!ok) return;
       }
     });
     std::thread writer([&] {
@@ -225,10 +230,11 @@ extern "C" int gls_solve_file(gls_ctx* ctx, const char* xr_path, int64_t xr_offs
         const bool ok = do_write(w, blocks[j]);
         {
           std::lock_guard<std::mutex> lk(mu);
-          w.failed = w.failed || !ok;
+          if (!ok) io_error = true;
           w.state = 0;  // free: the reader may load block j + 2 into it
         }
         cv.notify_all();
+        if (!ok) return;
       }
     });
     for (size_t j = 0; j < blocks.size() && rc == GLS_OK; ++j) {
@@ -236,11 +242,13 @@ extern "C" int gls_solve_file(gls_ctx* ctx, const char* xr_path, int64_t xr_offs
       const auto t0 = Clock::now();
       {  // line 8: wait(current X_blk)
         std::unique_lock<std::mutex> lk(mu);
-        cv.wait(lk, [&] { return w.state == 2 && w.block == (int64_t)j; });
-        if (w.failed) rc = GLS_ERR_ARG;
+        cv.wait(lk, [&] { return io_error || (w.state == 2 && w.block == (int64_t)j); });
+        if (io_error) rc = GLS_ERR_ARG;
       }
+      if (rc != GLS_OK) break;
       const auto t1 = Clock::now();
-      if (rc == GLS_OK) rc = solve(w, blocks[j]);  // lines 9-14
+      rc = solve(w, blocks[j]);  // lines 9-14
+      if (rc != GLS_OK) break;  // never hand an unsolved workspace to the writer
       const auto t2 = Clock::now();
       {  // line 15: async_write(current b_blk)
         std::lock_guard<std::mutex> lk(mu);
@@ -251,8 +259,8 @@ extern "C" int gls_solve_file(gls_ctx* ctx, const char* xr_path, int64_t xr_offs
       if (j >= 1) {
         Workspace& pw = ws[(j - 1) & 1];
         std::unique_lock<std::mutex> lk(mu);
-        cv.wait(lk, [&] { return pw.state == 0 || pw.state == 1 || pw.state == 2 || pw.failed; });
-        if (pw.failed) rc = GLS_ERR_ARG;
+        cv.wait(lk, [&] { return io_error || pw.state == 0 || pw.state == 1 || pw.state == 2; });
+        if (io_error) rc = GLS_ERR_ARG;
       }
       const auto t3 = Clock::now();
       r.read_wait_s += secs(t0, t1);
@@ -268,10 +276,10 @@ extern "C" int gls_solve_file(gls_ctx* ctx, const char* xr_path, int64_t xr_offs
       if (rc == GLS_OK) {
         Workspace& lw = ws[(blocks.size() - 1) & 1];
         const auto t0 = Clock::now();
-        cv.wait(lk, [&] { return lw.state == 0 || lw.failed; });
+        cv.wait(lk, [&] { return io_error || lw.state == 0; });
         r.write_wait_s += secs(t0, Clock::now());
-        if (lw.failed) rc = GLS_ERR_ARG;
       }
+      if (rc == GLS_OK && io_error) rc = GLS_ERR_ARG;
       stop = true;
     }
     cv.notify_all();

@@ -37,15 +37,25 @@ def weak_range(m_per_rank: int, rank: int) -> tuple[int, int]:
 def replicate_shared(ctx, dist, src: int = 0, group=None) -> int:
     """Broadcast the shared state of `ctx` from rank `src` to every rank of `group`, then commit it
     on the receiving ranks.  `ctx` is a Context created with gls_create on `src` and with
-    adopt=True elsewhere.  Returns the number of bytes broadcast."""
-    rank = dist.get_rank(group) if group is not None else dist.get_rank()
+    adopt=True elsewhere.  `src` is a GLOBAL rank (torch.distributed's convention for broadcast).
+    Over NCCL the library's device buffers are broadcast in place (zero-copy tensors); over gloo
+    (host-only backend, used by the CPU-side tests) they are staged through host memory.
+    Returns the number of bytes broadcast."""
+    import torch
+    rank = dist.get_rank()  # global rank, comparable with src
     tensors = ctx.shared_tensors()
+    staged = bool(tensors) and tensors[0].is_cuda and dist.get_backend(group) == "gloo"
     nbytes = 0
     for t in tensors:
-        dist.broadcast(t, src=src, group=group)
+        if staged:
+            h = t.cpu()
+            dist.broadcast(h, src=src, group=group)
+            if rank != src:
+                t.copy_(h)
+        else:
+            dist.broadcast(t, src=src, group=group)
         nbytes += t.numel() * t.element_size()
     if tensors and tensors[0].is_cuda:
-        import torch
         torch.cuda.synchronize()
     if rank != src:
         ctx.commit_shared()

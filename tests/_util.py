@@ -35,3 +35,47 @@ def assert_parity(b_gpu, st_gpu, b_ora, st_ora, tol=PARITY_TOL, label=""):
     err = guarded_rel_err(b_gpu[ok], np.asarray(b_ora)[ok])
     assert err <= tol, "guarded relative error %.3e > %.1e %s" % (err, tol, label)
     return err
+
+
+# ----------------------------------------------------------------------------- parity report
+# Every full-size parity test records (label, problems checked, max guarded error, max norm-wise
+# error); conftest.py prints the table at the end of the session, also under -q.
+PARITY_REPORT = []
+
+
+def record_parity(label, b_gpu, b_ora, st_ora=None):
+    b_gpu = np.asarray(b_gpu)
+    b_ora = np.asarray(b_ora)
+    ok = np.ones(len(b_ora), bool) if st_ora is None else (np.asarray(st_ora) == 0)
+    g = guarded_rel_err(b_gpu[ok], b_ora[ok])
+    nw = normwise_err(b_gpu[ok], b_ora[ok])
+    PARITY_REPORT.append((label, int(len(b_ora)), g, nw))
+    return g, nw
+
+
+def edge_set(m, *periods, first_chunks=None):
+    """Sorted problem indices at the edges of a launch: for every boundary B of every period
+    (multiples of the period) and of the explicit chunk boundaries, the problems B - 1 and B; plus
+    0 and m - 1 (the ragged tail)."""
+    bnd = {0, m}
+    for per in periods:
+        bnd.update(range(0, m, per))
+    if first_chunks is not None:
+        bnd.update(first_chunks)
+    out = set()
+    for b in bnd:
+        for i in (b - 1, b):
+            if 0 <= i < m:
+                out.add(i)
+    return np.array(sorted(out), dtype=np.int64)
+
+
+def int8_chunk_bounds(m_groups, wave_groups, ahead=True):
+    """Chunk boundaries of one device block on the int8 path (gls_api.cu run_kernel): 1, 2, .., 8,
+    8, .. waves with convert-ahead (n >= 4096), else chunks of 8 waves."""
+    bnd = [0]
+    j = 1
+    while bnd[-1] < m_groups:
+        bnd.append(min(m_groups, bnd[-1] + (min(j, 8) if ahead else 8) * wave_groups))
+        j += 1
+    return bnd

@@ -18,3 +18,14 @@ def golden():
     import json
     with open(os.path.join(ROOT, "tests", "golden", "spec_examples.json")) as f:
         return json.load(f)
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    from _util import PARITY_REPORT
+    if not PARITY_REPORT:
+        return
+    tr = terminalreporter
+    tr.write_sep("-", "parity vs the CPU oracle (guarded = DESIGN.md reading A10, gate 1e-9)")
+    tr.write_line("%-58s %9s %12s %12s" % ("case", "problems", "max guarded", "max normwise"))
+    for label, k, g, nw in PARITY_REPORT:
+        tr.write_line("%-58s %9d %12.3e %12.3e" % (label, k, g, nw))

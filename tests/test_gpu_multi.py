@@ -36,16 +36,8 @@ def _rank_main(rank, world, init_file, out_dir):
         ctx = pkg.Context(N, PL, PR, d(P.M), d(P.XL), d(P.y))
     else:
         ctx = pkg.Context(N, PL, PR, adopt=True)
-    # gloo moves host tensors: stage the shared buffers through host memory around the broadcast
-    bufs = ctx.shared_tensors()
-    host = [b.cpu() for b in bufs]
-    for h in host:
-        dist.broadcast(h, src=0)
-    if rank != 0:
-        for b, h in zip(bufs, host):
-            b.copy_(h)
-        torch.cuda.synchronize()
-        ctx.commit_shared()
+    # the library's shared buffers broadcast from rank 0 (gloo: staged through host memory)
+    multi.replicate_shared(ctx, dist, src=0)
     lo, hi = multi.weak_range(M_PER_RANK, rank)
     X = torch.empty((M_PER_RANK * PR, N), dtype=torch.float64, device="cuda")
     pkg.gen_xr_device(SEED, N, lo * PR, M_PER_RANK * PR, X)

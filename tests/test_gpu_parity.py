@@ -10,7 +10,7 @@ import pytest
 import gen
 import oracle
 
-from _util import assert_parity, guarded_rel_err, normwise_err
+from _util import assert_parity, edge_set, int8_chunk_bounds, normwise_err, record_parity
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -72,9 +72,9 @@ def test_config0_all_snps(glsmod):
     glsmod.gen_xr_device(SEED, cfg.n, 0, cfg.cols, Xd)
     b, st, launches = run_gpu(glsmod, P, Xd, cfg.m, cfg.pR)
     assert launches > 0
-    err = assert_parity(b, st, b_or, st_or, label="config0")
+    assert_parity(b, st, b_or, st_or, label="config0")
     assert normwise_err(b, b_or) <= 1e-12
-    print("config0 guarded err %.3e" % err)
+    record_parity("config0 n=500 p=4: every SNP", b, b_or, st_or)
 
 
 @pytest.mark.parametrize("n,pL,pR,m,sex", [
@@ -306,21 +306,23 @@ def test_planted_beta_config1_all_snps(glsmod):
     assert err <= 1e-10, err
 
 
-def test_config1_sampled_parity(glsmod):
-    """Config 1 at full size in the bench launch configuration; oracle on a seeded sample
-    plus every panel/wave edge in the first and last waves."""
+def test_config1_all_snps(glsmod):
+    """Config 1 at full size (n=1500, m=220833) in the bench launch configuration (one device block):
+    EVERY SNP against the oracle (SURVEY §8(c) coverage plan), X_R for the oracle drawn on the CPU."""
     cfg = gen.CONFIGS[1]
     P = gen.config_problem(cfg)
     Xd = torch.empty((cfg.cols, cfg.n), dtype=torch.float64, device="cuda")
     glsmod.gen_xr_device(SEED, cfg.n, 0, cfg.cols, Xd)
     b, st, _ = run_gpu(glsmod, P, Xd, cfg.m, cfg.pR)
-    rng = np.random.default_rng(11)
-    edges = [0, 1, 63, 64, 65, 148 * 64 - 1, 148 * 64, cfg.m - 65, cfg.m - 2, cfg.m - 1]
-    sel = np.unique(np.concatenate([rng.choice(cfg.m, 1500, replace=False), edges]))
-    XRs = np.concatenate([gen.make_XR(SEED, cfg.n, int(i), 1) for i in sel])
-    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XRs, 1, sel=sel, xr_is_selected=True)
-    err = assert_parity(b[sel], st[sel], b_or, st_or, label="config1 sample")
-    print("config1 sampled guarded err %.3e normwise %.3e" % (err, normwise_err(b[sel], b_or)))
+    del Xd
+    XR = gen.make_XR(SEED, cfg.n, 0, cfg.cols)
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, cfg.pR)
+    assert_parity(b, st, b_or, st_or, label="config1 all SNPs")
+    record_parity("config1 n=1500 p=4: all 220833 SNPs", b, b_or, st_or)
+    # the FP64 DMMA path on the same inputs, every SNP
+    b64, st64, _ = run_gpu(glsmod, P, dev(XR), cfg.m, cfg.pR, path=glsmod.GLS_PATH_FP64)
+    assert_parity(b64, st64, b_or, st_or, label="config1 all SNPs, FP64 path")
+    record_parity("config1, FP64 DMMA path: all 220833 SNPs", b64, b_or, st_or)
 
 
 def test_adopt_shared_state_bitwise(glsmod):
@@ -357,8 +359,10 @@ def n1e4_factor():
 
 
 def test_config2_full_size_sampled_parity_and_planted_beta(glsmod, n1e4_factor):
-    """Config 2 at full size (n=1e4, m=1e6, one launch, the bench configuration): oracle parity on a
-    seeded sample plus panel / wave / tail edges; then the planted-beta identity on ALL 1e6 SNPs."""
+    """Config 2 at full size (n=1e4, m=1e6, one launch, the bench configuration): oracle parity on
+    1024 seeded SNPs plus the first and last SNP of every int8 conversion chunk, every wave of
+    128-column tiles, every 8192-column block, and the ragged tail; the FP64 DMMA path on the same
+    sample plus its own panel-wave edges; then the planted-beta identity on ALL 1e6 SNPs."""
     cfg = gen.CONFIGS[2]
     P, L = n1e4_factor
     Xd = torch.empty((cfg.cols, cfg.n), dtype=torch.float64, device="cuda")
@@ -367,14 +371,19 @@ def test_config2_full_size_sampled_parity_and_planted_beta(glsmod, n1e4_factor):
         glsmod.gen_xr_device(SEED, cfg.n, c, k, Xd[c:c + k])
     b, st, _ = run_gpu(glsmod, P, Xd, cfg.m, cfg.pR)
     assert np.all(st == 0)
+    wave = 148 * 128                     # SNPs per wave of int8 tiles (pR = 1)
+    edges = edge_set(cfg.m, wave, 8192, first_chunks=int8_chunk_bounds(cfg.m, wave))
+    edges64 = edge_set(cfg.m, 148 * 64)  # FP64 path: 64-column panels, one per SM per wave
     rng = np.random.default_rng(2)
-    wave = 148 * 64
-    edges = [0, 63, 64, wave - 1, wave, 105 * wave, cfg.m - 64, cfg.m - 1]
-    sel = np.unique(np.concatenate([rng.choice(cfg.m, 40, replace=False), edges]))
+    sel = np.unique(np.concatenate([rng.choice(cfg.m, 1024, replace=False), edges, edges64]))
     XRs = np.concatenate([gen.make_XR(SEED, cfg.n, int(i), 1) for i in sel])
     b_or, st_or = oracle.gls_sequence(L, P.XL, P.y, XRs, 1, sel=sel, xr_is_selected=True)
-    err = assert_parity(b[sel], st[sel], b_or, st_or, label="config2 sample")
-    print("config2 sampled guarded err %.3e normwise %.3e" % (err, normwise_err(b[sel], b_or)))
+    assert_parity(b[sel], st[sel], b_or, st_or, label="config2 sample")
+    record_parity("config2 n=1e4 p=4 m=1e6: 1024 seeded + %d edge SNPs" % (len(sel) - 1024), b[sel], b_or, st_or)
+    b64, st64, _ = run_gpu(glsmod, P, Xd, cfg.m, cfg.pR, path=glsmod.GLS_PATH_FP64)
+    assert_parity(b64[sel], st64[sel], b_or, st_or, label="config2 sample, FP64 path")
+    record_parity("config2, FP64 DMMA path: same %d SNPs" % len(sel), b64[sel], b_or, st_or)
+    del b64, st64
     P0 = gen.config_problem(cfg, noise=0.0)
     b0, st0, _ = run_gpu(glsmod, P0, Xd, cfg.m, cfg.pR)
     ref = np.concatenate([P0.beta_L, [0.0]])
@@ -388,14 +397,14 @@ def test_config3_shape_sampled_parity(glsmod, n1e4_factor):
     cfg = gen.CONFIGS[3]
     m = 4000
     P = gen.config_problem(cfg)
-    L = oracle.cholesky(P.M) if P.M.shape != n1e4_factor[0].M.shape or not np.array_equal(
-        P.M, n1e4_factor[0].M) else n1e4_factor[1]
+    assert np.array_equal(P.M, n1e4_factor[0].M)  # configs 2-4 share M (same seed and n)
+    L = n1e4_factor[1]
     XR = gen.make_XR(SEED, cfg.n, 0, m * cfg.pR)
     b, st, _ = run_gpu(glsmod, P, dev(XR), m, cfg.pR)
     sel = np.unique(np.concatenate([np.random.default_rng(3).choice(m, 24, replace=False), [0, 7, 8, 15, m - 1]]))
     b_or, st_or = oracle.gls_sequence(L, P.XL, P.y, XR, cfg.pR, sel=sel)
-    err = assert_parity(b[sel], st[sel], b_or, st_or, label="config3 sample")
-    print("config3 sampled guarded err %.3e" % err)
+    assert_parity(b[sel], st[sel], b_or, st_or, label="config3 sample")
+    record_parity("config3 shape (4000 groups): %d groups" % len(sel), b[sel], b_or, st_or)
     P0 = gen.config_problem(cfg, noise=0.0)
     b0, st0, _ = run_gpu(glsmod, P0, dev(XR), m, cfg.pR)
     ref = np.concatenate([P0.beta_L, np.zeros(cfg.pR)])
@@ -583,15 +592,23 @@ def test_algorithm_ladder_agrees(glsmod):
         "ladder", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "ladder.py"))
     ladder = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(ladder)
-    out = ladder.run(300, 3, 1, 300, 6, seed=26)
-    dev_ = out["max_rel_dev_from_hp_gwas"]
-    assert dev_["seq-gls"] <= 1e-11 and dev_["black-box"] <= 1e-11, dev_
+    n, pL, pR, m, m_bb, seed = 300, 3, 1, 300, 6, 26
+    out = ladder.run(n, pL, pR, m, m_bb, seed=seed, return_b=True)
+    # every rung against the oracle on the same seeded problem (ladder.run draws it the same way)
+    P = gen.make_problem(n, pL, pR, with_sex=True, seed=seed)
+    XR = gen.make_XR(seed, n, 0, m * pR)
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, pR)
+    for rung, b in out["_b"].items():
+        k = len(b)
+        assert_parity(b, np.zeros(k, np.int32), b_or[:k], st_or[:k], label="ladder " + rung)
+        record_parity("ladder n=300 p=4: %s (%d problems)" % (rung, k), b, b_or[:k])
 
 
-def test_config3_full_size_sampled_parity(glsmod):
+def test_config3_full_size_sampled_parity(glsmod, n1e4_factor):
     """Config 3 at full size (n=1e4, pL=16, pR=4, 5e5 groups = 2e6 columns, 160 GB of X_R in HBM; the
-    bench launch): oracle parity on sampled groups incl. tile / pair / wave edges, and the planted-beta
-    identity on every group."""
+    bench launch): oracle parity on 512 seeded groups plus the first and last group of every
+    128-column tile pair at the start and end, of every wave and of every int8 conversion chunk, and
+    the planted-beta identity on every group."""
     cfg = gen.CONFIGS[3]
     torch.cuda.empty_cache()  # earlier tests' X_R buffers sit in torch's cache
     glsmod.release_cached_memory()  # and earlier contexts' buffers in the library's pool
@@ -599,6 +616,8 @@ def test_config3_full_size_sampled_parity(glsmod):
     if free < 175e9:
         pytest.skip("needs ~170 GB of free device memory")
     P = gen.config_problem(cfg)
+    assert np.array_equal(P.M, n1e4_factor[0].M)
+    Lf = n1e4_factor[1]
     cols = cfg.m * cfg.pR
     Xd = torch.empty((cols, cfg.n), dtype=torch.float64, device="cuda")
     for c in range(0, cols, 65536):
@@ -606,15 +625,17 @@ def test_config3_full_size_sampled_parity(glsmod):
         glsmod.gen_xr_device(SEED, cfg.n, c, k, Xd[c:c + k])
     b, st, _ = run_gpu(glsmod, P, Xd, cfg.m, cfg.pR)
     assert np.all(st == 0)
-    tile_g = 32  # groups per 128-column tile at pR = 4
+    tile_g = 32  # groups per 128-column tile at pR = 4; a CTA pair covers 2 tiles
     wave_g = 148 * tile_g
-    edges = [0, 7, 8, tile_g - 1, tile_g, 2 * tile_g - 1, 2 * tile_g, wave_g - 1, wave_g, cfg.m - 1]
-    sel = np.unique(np.concatenate([np.random.default_rng(4).choice(cfg.m, 8, replace=False), edges]))
+    head_tail = [x for t in range(4) for x in (t * tile_g, (t + 1) * tile_g - 1)]
+    head_tail += [cfg.m - 1 - x for x in head_tail]
+    edges = edge_set(cfg.m, wave_g, first_chunks=int8_chunk_bounds(cfg.m, wave_g))
+    sel = np.unique(np.concatenate([np.random.default_rng(4).choice(cfg.m, 512, replace=False), edges,
+                                    head_tail, [7, 8]]))
     XRs = np.concatenate([gen.make_XR(SEED, cfg.n, int(i) * cfg.pR, cfg.pR) for i in sel])
-    Lf = oracle.cholesky(P.M)
     b_or, st_or = oracle.gls_sequence(Lf, P.XL, P.y, XRs, cfg.pR, sel=sel, xr_is_selected=True)
-    err = assert_parity(b[sel], st[sel], b_or, st_or, label="config3 full sample")
-    print("config3 full-size sampled guarded err %.3e" % err)
+    assert_parity(b[sel], st[sel], b_or, st_or, label="config3 full sample")
+    record_parity("config3 n=1e4 p=20 m=5e5: 512 seeded + %d edge groups" % (len(sel) - 512), b[sel], b_or, st_or)
     P0 = gen.config_problem(cfg, noise=0.0)
     b0, st0, _ = run_gpu(glsmod, P0, Xd, cfg.m, cfg.pR)
     del Xd
@@ -623,31 +644,62 @@ def test_config3_full_size_sampled_parity(glsmod):
     assert np.max(np.abs(b0 - ref)) / np.max(np.abs(P0.beta_L)) <= 1e-10
 
 
-def test_config4_shape_host_stream_codes(glsmod, n1e4_factor):
-    """The out-of-core launch configuration at n = 1e4: 200k SNPs streamed from pinned host memory as
-    int8 codes in several host chunks (Alg. 8) equal the in-HBM run bit for bit, and match the oracle
-    on sampled SNPs at chunk edges."""
+def test_config4_full_stream(glsmod, n1e4_factor):
+    """Config 4 in the bench launch configuration (bench.py run_ooc): m = 1e7 SNPs streamed from
+    pinned host memory as int8 genotype codes through the double-buffered H2D pipeline (Alg. 8), the
+    host blocks cycled from a pool of 4 distinct blocks (block j = pool block j mod 4).
+      * every one of the 1e7 b rows equals, bit for bit, the in-HBM solve of its pool block's SNP;
+      * 2e6 SNPs of the same stream from FP64 host X_R (a pool of 2 blocks) equal it bit for bit;
+      * the oracle checks 1024 seeded SNPs of the distinct region plus the first and last SNP of
+        every host block, wave of tiles and 8192-column block in it."""
+    from paper_1210_7325_b200 import ooc
     cfg = gen.CONFIGS[4]
     P, Lf = n1e4_factor
-    m = 200_000
-    Xd = torch.empty((m, cfg.n), dtype=torch.float64, device="cuda")
-    for c in range(0, m, 65536):
-        k = min(65536, m - c)
-        glsmod.gen_xr_device(SEED, cfg.n, c, k, Xd[c:c + k])
-    Gh = torch.empty((m, cfg.n), dtype=torch.int8).pin_memory()
-    Gh.copy_(Xd.to(torch.int8))
-    with glsmod.Context(cfg.n, cfg.pL, cfg.pR, dev(P.M), dev(P.XL), dev(P.y)) as ctx:
-        bd = torch.empty((m, 4), dtype=torch.float64, device="cuda")
-        ctx.solve_block(Xd, m, bd)
-        bd = bd.cpu().numpy()
-        bh = torch.empty((m, 4), dtype=torch.float64).pin_memory()
-        sh = torch.empty(m, dtype=torch.int32).pin_memory()
-        chunk = 148 * 128 * 4
-        ctx.solve_block_i8(Gh, m, bh, sh)
-        np.testing.assert_array_equal(bh.numpy(), bd)
-        assert not sh.numpy().any()
+    n, m = cfg.n, cfg.m
+    blk = ooc.host_block_groups(torch.cuda.get_device_properties(0).multi_processor_count, cfg.pR)
+    PB = 4
+    distinct = PB * blk
+    Xd = torch.empty((distinct, n), dtype=torch.float64, device="cuda")
+    for c in range(0, distinct, 65536):
+        k = min(65536, distinct - c)
+        glsmod.gen_xr_device(SEED, n, c, k, Xd[c:c + k])
+    pool8 = torch.empty((PB, blk, n), dtype=torch.int8).pin_memory()
+    for k in range(PB):
+        pool8[k].copy_(Xd[k * blk:(k + 1) * blk].to(torch.int8))
+    with glsmod.Context(n, cfg.pL, cfg.pR, dev(P.M), dev(P.XL), dev(P.y)) as ctx:
+        bd = torch.empty((distinct, 4), dtype=torch.float64, device="cuda")
+        ctx.solve_block(Xd, distinct, bd)
+        bd = bd.cpu()
+        b = torch.empty((m, 4), dtype=torch.float64).pin_memory()
+        st = torch.empty(m, dtype=torch.int32).pin_memory()
+        nblk = ooc.stream_from_pool(ctx, pool8, m, blk, b, st, codes=True)
+        assert nblk == (m + blk - 1) // blk
+        assert not st.numpy().any()
+        for j in range(nblk):
+            lo, cnt = j * blk, min(blk, m - j * blk)
+            k = j % PB
+            assert torch.equal(b[lo:lo + cnt], bd[k * blk:k * blk + cnt]), "stream block %d" % j
+        # FP64 host X_R through the same pipeline (8 bytes per genotype over PCIe)
+        del pool8
+        m64 = 2_000_000
+        pool64 = torch.empty((2, blk, n), dtype=torch.float64).pin_memory()
+        for k in range(2):
+            pool64[k].copy_(Xd[k * blk:(k + 1) * blk])
+        b64 = torch.empty((m64, 4), dtype=torch.float64).pin_memory()
+        st64 = torch.empty(m64, dtype=torch.int32).pin_memory()
+        nb64 = ooc.stream_from_pool(ctx, pool64, m64, blk, b64, st64, codes=False)
+        for j in range(nb64):
+            lo, cnt = j * blk, min(blk, m64 - j * blk)
+            k = j % 2
+            assert torch.equal(b64[lo:lo + cnt], bd[k * blk:k * blk + cnt]), "FP64 stream block %d" % j
+        del pool64
     del Xd
-    sel = np.unique([0, chunk - 1, chunk, 2 * chunk - 1, 2 * chunk, m - 1, 12345, 99999])
-    XRs = np.concatenate([gen.make_XR(SEED, cfg.n, int(i), 1) for i in sel])
+    bd = bd.numpy()
+    wave = 148 * 128
+    sel = np.unique(np.concatenate([np.random.default_rng(44).choice(distinct, 1024, replace=False),
+                                    edge_set(distinct, blk, wave, 8192)]))
+    XRs = np.concatenate([gen.make_XR(SEED, n, int(i), 1) for i in sel])
     b_or, st_or = oracle.gls_sequence(Lf, P.XL, P.y, XRs, 1, sel=sel, xr_is_selected=True)
-    assert_parity(bd[sel], np.zeros(len(sel), np.int32), b_or, st_or, label="config4 stream sample")
+    assert_parity(bd[sel], np.zeros(len(sel), np.int32), b_or, st_or, label="config4 sample")
+    record_parity("config4 n=1e4 p=4 m=1e7 streamed: 1024 seeded + %d edge SNPs" % (len(sel) - 1024),
+                  bd[sel], b_or, st_or)

@@ -138,3 +138,40 @@ def test_replicate_and_shard_two_nodes_gloo():
 def test_local_device_env():
     assert local_device({}) == 0
     assert local_device({"LOCAL_RANK": "3"}) == 3
+
+
+def _worker_subgroup(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        grp = dist.new_group([1, 2])
+        if rank in (1, 2):
+            # the subgroup's root is GLOBAL rank 1 (group rank 0): it must not commit, rank 2 must
+            ctx = FakeCtx(root=(rank == 1))
+            replicate_shared(ctx, dist, src=1, group=grp)
+            ref = FakeCtx(root=True)
+            same = all(torch.equal(a, b) for a, b in zip(ctx.bufs, ref.bufs))
+            q.put((rank, same, ctx.committed))
+        else:
+            q.put((rank, True, True))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_replicate_in_subgroup_rooted_at_global_rank_1():
+    """src is a global rank: in a subgroup {1, 2} rooted at global rank 1, rank 1 keeps its state
+    (no commit) and rank 2 receives it and commits (group-local vs global rank)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_subgroup, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(same and committed for _, same, committed in res), res

@@ -325,3 +325,57 @@ def test_selection_and_packing_agree():
     bpk, _ = oracle.solve(P.M, P.XL, P.y, packed, 2, sel=sel, xr_is_selected=True)
     np.testing.assert_array_equal(bsel, ball[sel])
     np.testing.assert_array_equal(bpk, ball[sel])
+
+
+# ----------------------------------------------------------------------------- p = 20 (config 3)
+@pytest.mark.parametrize("pL,pR", [(16, 4), (0, 20), (19, 1)])
+def test_p20_against_lapack(pL, pR):
+    """p = 20, the config-3 width (pL = 16 covariates + pR = 4 genotype columns) and the two extreme
+    splits: the oracle's 20-stride S / G arrays against the Alg. 1 route done by LAPACK (scipy
+    cholesky, solve_triangular, then gelsd least squares on the whitened X_i)."""
+    n, m = 260, 12
+    P = gen.make_problem(n, pL, pR, with_sex=False, seed=60 + pL)
+    XR = gen.make_XR(60 + pL, n, 0, m * pR)
+    b, st = oracle.solve(P.M, P.XL, P.y, XR, pR)
+    assert np.all(st == 0)
+    Ls = sla.cholesky(P.M, lower=True)
+    yw = sla.solve_triangular(Ls, P.y, lower=True)
+    XLw = sla.solve_triangular(Ls, P.XL.T, lower=True) if pL else np.zeros((n, 0))
+    for i in range(m):
+        xw = sla.solve_triangular(Ls, XR[i * pR:(i + 1) * pR].T, lower=True)
+        ref = np.linalg.lstsq(np.column_stack([XLw, xw]), yw, rcond=None)[0]
+        assert np.linalg.norm(b[i] - ref) <= 1e-12 * np.linalg.norm(ref), (i, b[i], ref)
+
+
+@pytest.mark.parametrize("n,pL,pR,m,seed", [(22, 16, 4, 2, 7), (23, 0, 20, 1, 8)])
+def test_exact_rational_brute_force_p20(n, pL, pR, m, seed):
+    """Eq. (1) in exact rationals at p = 20 (every index of the 20 x 20 S_i and of the b record)."""
+    rng = np.random.default_rng(200 + seed)
+    A = rng.integers(-2, 3, size=(n, n))
+    Mi = (A @ A.T + n * np.eye(n, dtype=np.int64)).astype(np.int64)
+    XLi = rng.integers(-2, 3, size=(pL, n))
+    if pL:
+        XLi[0] = 1
+    XRi = rng.integers(0, 3, size=(m * pR, n))
+    yi = rng.integers(-5, 6, size=n)
+    b_or, st = oracle.solve(Mi.astype(float), XLi.astype(float), yi.astype(float), XRi.astype(float), pR)
+    Mf = [[Fraction(int(v)) for v in row] for row in Mi]
+    for i in range(m):
+        cols = [XLi[k] for k in range(pL)] + [XRi[i * pR + k] for k in range(pR)]
+        assert np.linalg.matrix_rank(np.array(cols, dtype=float).T) == pL + pR
+        X = [[Fraction(int(c[r])) for c in cols] for r in range(n)]
+        b_ex = np.array([float(v) for v in exact_gls(Mf, X, [Fraction(int(v)) for v in yi])])
+        assert st[i] == 0
+        err = np.linalg.norm(b_or[i] - b_ex) / np.linalg.norm(b_ex)
+        assert err <= 1e-12, (i, err)
+
+
+def test_planted_beta_p20():
+    """Config-3 shape (pL = 16, pR = 4), noise-free y = X_L beta => b_i = (beta, 0, 0, 0, 0)."""
+    n = 200
+    P = gen.make_problem(n, 16, 4, with_sex=False, seed=61, noise=0.0)
+    XR = gen.make_XR(61, n, 0, 10 * 4)
+    b, st = oracle.solve(P.M, P.XL, P.y, XR, 4)
+    assert np.all(st == 0)
+    ref = np.concatenate([P.beta_L, np.zeros(4)])
+    assert np.max(np.abs(b - ref)) / np.max(np.abs(P.beta_L)) <= 1e-11

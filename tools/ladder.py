@@ -61,7 +61,7 @@ def timed_solve(n, pL, pR, M, XL, y, X, m, path=None):
         return time.perf_counter() - t0, b.cpu().numpy()
 
 
-def run(n, pL, pR, m, m_bb, seed=gen.DEFAULT_SEED):
+def run(n, pL, pR, m, m_bb, seed=gen.DEFAULT_SEED, return_b=False):
     p = pL + pR
     P = gen.make_problem(n, pL, pR, with_sex=True, seed=seed)
     XR = gen.make_XR(seed, n, 0, m * pR)
@@ -90,7 +90,7 @@ def run(n, pL, pR, m, m_bb, seed=gen.DEFAULT_SEED):
     t_bb = time.perf_counter() - t0
     rate = {"black-box": m_bb / t_bb, "seq-gls": m / t_sq, "hp-gwas": m / t_hp, "hp-gwas-fp64": m / t_hp64}
     dev_rel = lambda a, b: float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
-    return {"n": n, "pL": pL, "pR": pR, "p": p, "m": m, "m_blackbox": m_bb,
+    out = {"n": n, "pL": pL, "pR": pR, "p": p, "m": m, "m_blackbox": m_bb,
             "problems_per_s": rate,
             "ratio_to_hp_gwas": {k: rate["hp-gwas"] / v for k, v in rate.items()},
             "ratio_to_hp_gwas_fp64_same_arithmetic": {k: rate["hp-gwas-fp64"] / rate[k]
@@ -102,6 +102,9 @@ def run(n, pL, pR, m, m_bb, seed=gen.DEFAULT_SEED):
             "max_rel_dev_from_hp_gwas": {"seq-gls": dev_rel(b_sq, b_hp), "black-box": dev_rel(b_bb, b_hp[:m_bb])},
             "note": "solve time per rung after a warm-up (the m -> infinity cost of Table II); black-box "
                     "includes its per-problem factorization and runs on the first m_blackbox problems"}
+    if return_b:
+        out["_b"] = {"hp-gwas": b_hp, "seq-gls": b_sq, "black-box": b_bb}
+    return out
 
 
 def main():
