@@ -4,6 +4,8 @@ Every input comes from gen/ (CPU) or its independent device twin (libglsgen_dev.
 bit-exact here first); every expected value comes from oracle/.  Tolerance: the north-star
 1e-9 per b_i entry, guarded as in DESIGN.md reading A10 (tests/_util.py).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -574,6 +576,13 @@ def test_solve_file_sync_and_async_bitwise(glsmod, tmp_path):
         with pytest.raises(glsmod.GLSError) as e:
             ctx.solve_file(str(tmp_path / "missing.bin"), m, bpath)
         assert e.value.code == 1
+        # a b file whose writes fail (ENOSPC): both modes must report the failure, never GLS_OK
+        if os.path.exists("/dev/full"):
+            for mode in (glsmod.GLS_OOC_SYNC, glsmod.GLS_OOC_ASYNC):
+                with pytest.raises(glsmod.GLSError) as e:
+                    ctx.solve_file(str(f64), m, "/dev/full", elem_bytes=8, xr_offset=64, block_groups=300,
+                                   mode=mode)
+                assert e.value.code == 1
         short = tmp_path / "short.bin"
         XR[: m // 2].tofile(short)
         for mode in (glsmod.GLS_OOC_SYNC, glsmod.GLS_OOC_ASYNC):
@@ -587,7 +596,6 @@ def test_algorithm_ladder_agrees(glsmod):
     factorization per problem) on the B200 kernels reproduce hp-gwas's b -- an
     independent GPU-side check of the Fig. 1 partition."""
     import importlib.util
-    import os
     spec = importlib.util.spec_from_file_location(
         "ladder", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "ladder.py"))
     ladder = importlib.util.module_from_spec(spec)
