@@ -146,6 +146,28 @@ int gls_solve_block_i8(gls_ctx* ctx, const int8_t* G, int64_t ldg, int64_t m_blk
 int gls_set_timing(gls_ctx* ctx, int32_t enable);
 int gls_read_timing(gls_ctx* ctx, double* ms_int8, double* ms_fp64, double* ms_conv, int64_t* launches);
 
+/* Overlap accounting of the host -> HBM stream (Alg. 8; fig:double-buff,
+ * PAPER.md:698-704).  When enabled, every host chunk of gls_solve_block[_ex|_i8] with a host X_R is
+ * bracketed by CUDA timing events: its H2D copy (h2d stream), its compute (recorded on the compute
+ * stream after the two waits of Alg. 8 -- "wait(current X_blk)" and "wait(previous b_blk)" -- have
+ * cleared, up to the end of its kernels) and its D2H copy.  gls_read_stream_report synchronises,
+ * summarises every chunk since the last read (in issue order), and resets:
+ *   wall_ms          first chunk's H2D start -> last event
+ *   h2d/compute/d2h  summed busy time of each engine
+ *   first_load_ms    the first copy, which nothing can hide (§4.3 warm-up block)
+ *   exposed_h2d_ms   compute-stream idle time between chunks while the next X block was still in
+ *                    flight (wait(current X_blk) exposed)
+ *   exposed_other_ms the rest of the idle time between chunks (wait(previous b_blk), host gaps)
+ *   tail_ms          after the last compute (the final D2H)
+ * Perfect overlap (the paper's claim) means exposed_h2d_ms + exposed_other_ms ~ 0
+ * when compute is the slower engine. */
+typedef struct {
+  int64_t chunks, h2d_bytes, d2h_bytes;
+  double wall_ms, h2d_ms, compute_ms, d2h_ms, first_load_ms, exposed_h2d_ms, exposed_other_ms, tail_ms;
+} gls_stream_report;
+int gls_set_stream_report(gls_ctx* ctx, int32_t enable);
+int gls_read_stream_report(gls_ctx* ctx, gls_stream_report* rep);
+
 /* gls_get_dims -- n, pL, pR of a context (any state but NULL). */
 int gls_get_dims(const gls_ctx* ctx, int64_t* n, int32_t* pL, int32_t* pR);
 

@@ -86,6 +86,15 @@ struct gls_ctx {
   };
   std::vector<TimedLaunch> tl;
   std::vector<cudaEvent_t> ev_pool;
+  // optional overlap accounting of the host->HBM stream (gls_set_stream_report): per chunk, timing
+  // events around its H2D copy, its compute (recorded after Alg. 8's two waits have cleared) and its
+  // D2H copy, on the streams that run them
+  bool srep = false;
+  struct ChunkRec {
+    cudaEvent_t h0, h1, c0, c1, d0, d1;
+    int64_t hbytes, dbytes;
+  };
+  std::vector<ChunkRec> srec;
   // host-streaming workspaces (two, swapping roles -- fig:workspaces)
   int64_t block_cols = 0;
   int64_t stage_cols = 0, ld_stage = 0;
@@ -458,6 +467,14 @@ struct LaunchTimer {
   }
 };
 
+// A timing event on `s` when stream accounting is on (else nullptr).
+cudaEvent_t srep_mark(gls_ctx* c, cudaStream_t s) {
+  if (!c->srep) return nullptr;
+  cudaEvent_t e = pool_event(c);
+  if (e) cudaEventRecord(e, s);
+  return e;
+}
+
 int run_fp64(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt,
              const int* gate, cudaStream_t strm = nullptr) {
   if (!strm) strm = c->stream;
@@ -648,31 +665,42 @@ int solve_streamed(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out, 
     const int64_t gc = (m_blk - g0 < chunk_groups) ? m_blk - g0 : chunk_groups;
     const int buf = (int)(c->seq++ & 1);
     const double* src = X_R + (size_t)g0 * pR * n;
+    gls_ctx::ChunkRec rec{};
     CK(c, cudaStreamWaitEvent(c->h2d, c->ev_comp[buf], 0));
+    rec.h0 = srep_mark(c, c->h2d);
     if (ld == n)
       CK(c, cudaMemcpyAsync(c->stage[buf], src, (size_t)n * gc * pR * sizeof(double), cudaMemcpyDefault,
                             c->h2d));
     else
       CK(c, cudaMemcpy2DAsync(c->stage[buf], ld * sizeof(double), src, n * sizeof(double),
                               n * sizeof(double), gc * pR, cudaMemcpyDefault, c->h2d));
+    rec.h1 = srep_mark(c, c->h2d);
+    rec.hbytes = (int64_t)n * gc * pR * (int64_t)sizeof(double);
     CK(c, cudaEventRecord(c->ev_h2d[buf], c->h2d));
-    CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d[buf], 0));
-    CK(c, cudaStreamWaitEvent(c->stream, c->ev_d2h[buf], 0));
+    CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d[buf], 0));  // wait(current X_blk)
+    CK(c, cudaStreamWaitEvent(c->stream, c->ev_d2h[buf], 0));  // wait(previous b_blk) of this workspace
+    rec.c0 = srep_mark(c, c->stream);
     double* bdst = b_dev ? b_out + (size_t)g0 * p : c->bstage[buf];
     int32_t* sdst = status_out ? (s_dev ? status_out + g0 : c->sstage[buf]) : nullptr;
     rc = run_kernel(c, c->stage[buf], ld, gc, bdst, sdst);
     if (rc) return rc;
+    rec.c1 = srep_mark(c, c->stream);
     CK(c, cudaEventRecord(c->ev_comp[buf], c->stream));
     if (!b_dev || (status_out && !s_dev)) {
       CK(c, cudaStreamWaitEvent(c->d2h, c->ev_comp[buf], 0));
+      rec.d0 = srep_mark(c, c->d2h);
       if (!b_dev)
         CK(c, cudaMemcpyAsync(b_out + (size_t)g0 * p, c->bstage[buf], (size_t)gc * p * sizeof(double),
                               cudaMemcpyDeviceToHost, c->d2h));
       if (status_out && !s_dev)
         CK(c, cudaMemcpyAsync(status_out + g0, c->sstage[buf], (size_t)gc * sizeof(int32_t),
                               cudaMemcpyDeviceToHost, c->d2h));
+      rec.d1 = srep_mark(c, c->d2h);
+      rec.dbytes = (int64_t)gc * ((b_dev ? 0 : p * (int64_t)sizeof(double)) +
+                                  ((status_out && !s_dev) ? (int64_t)sizeof(int32_t) : 0));
       CK(c, cudaEventRecord(c->ev_d2h[buf], c->d2h));
     }
+    if (c->srep) c->srec.push_back(rec);
   }
   return GLS_OK;
 }
@@ -731,15 +759,20 @@ int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, d
     // contiguous rows whose length is not a multiple of 16 bytes (the TMA row pitch): one linear copy
     // (a pitched copy of short rows runs at a fraction of the link rate), repacked on the device
     const bool repack = ldg == n && c->ld8 != n;
+    gls_ctx::ChunkRec rec{};
+    rec.h0 = srep_mark(c, c->h2d);
     if (repack)
       CK(c, cudaMemcpyAsync(c->raw8[buf], G + (size_t)g0 * pR * ldg, (size_t)gc * pR * n, cudaMemcpyDefault,
                             c->h2d));
     else
       CK(c, cudaMemcpy2DAsync(c->stage8[buf], c->ld8, G + (size_t)g0 * pR * ldg, ldg, n, gc * pR,
                               cudaMemcpyDefault, c->h2d));
+    rec.h1 = srep_mark(c, c->h2d);
+    rec.hbytes = (int64_t)n * gc * pR;
     CK(c, cudaEventRecord(c->ev_h2d[buf], c->h2d));
-    CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d[buf], 0));
-    CK(c, cudaStreamWaitEvent(c->stream, c->ev_d2h[buf], 0));
+    CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d[buf], 0));  // wait(current X_blk)
+    CK(c, cudaStreamWaitEvent(c->stream, c->ev_d2h[buf], 0));  // wait(previous b_blk) of this workspace
+    rec.c0 = srep_mark(c, c->stream);
     if (repack) {
       oz_repack_rows(c->stream, c->raw8[buf], n, gc * pR, c->stage8[buf], c->ld8, &c->launches);
       CK(c, cudaGetLastError());
@@ -748,17 +781,23 @@ int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, d
     int32_t* sdst = status_out ? (s_dev ? status_out + g0 : c->sstage[buf]) : nullptr;
     rc = run_int8(c, c->stage8[buf], c->ld8, gc, bdst, sdst, nullptr);
     if (rc) return rc;
+    rec.c1 = srep_mark(c, c->stream);
     CK(c, cudaEventRecord(c->ev_comp[buf], c->stream));
     if (!b_dev || (status_out && !s_dev)) {
       CK(c, cudaStreamWaitEvent(c->d2h, c->ev_comp[buf], 0));
+      rec.d0 = srep_mark(c, c->d2h);
       if (!b_dev)
         CK(c, cudaMemcpyAsync(b_out + (size_t)g0 * p, c->bstage[buf], (size_t)gc * p * sizeof(double),
                               cudaMemcpyDeviceToHost, c->d2h));
       if (status_out && !s_dev)
         CK(c, cudaMemcpyAsync(status_out + g0, c->sstage[buf], (size_t)gc * sizeof(int32_t),
                               cudaMemcpyDeviceToHost, c->d2h));
+      rec.d1 = srep_mark(c, c->d2h);
+      rec.dbytes = (int64_t)gc * ((b_dev ? 0 : p * (int64_t)sizeof(double)) +
+                                  ((status_out && !s_dev) ? (int64_t)sizeof(int32_t) : 0));
       CK(c, cudaEventRecord(c->ev_d2h[buf], c->d2h));
     }
+    if (c->srep) c->srec.push_back(rec);
   }
   return GLS_OK;
 }
@@ -968,6 +1007,65 @@ int gls_read_timing(gls_ctx* c, double* ms_int8, double* ms_fp64, double* ms_con
   *ms_int8 = t[0];
   *ms_fp64 = t[1];
   *ms_conv = t[2];
+  return GLS_OK;
+}
+
+int gls_set_stream_report(gls_ctx* c, int32_t enable) {
+  if (!c) return GLS_ERR_ARG;
+  c->srep = enable != 0;
+  return GLS_OK;
+}
+
+int gls_read_stream_report(gls_ctx* c, gls_stream_report* r) {
+  if (!c || !r) return GLS_ERR_ARG;
+  DeviceGuard g(c->device);
+  int rc = sync_all(c);
+  if (rc) return rc;
+  memset(r, 0, sizeof *r);
+  if (!c->srec.empty()) {
+    const cudaEvent_t t0 = c->srec.front().h0;
+    auto at = [&](cudaEvent_t e) -> double {  // ms since the first chunk's H2D start
+      float ms = 0.f;
+      if (!e || !t0 || cudaEventElapsedTime(&ms, t0, e) != cudaSuccess) {
+        cudaGetLastError();
+        return 0.0;
+      }
+      return (double)ms;
+    };
+    double end = 0.0, prev_c1 = 0.0;
+    for (size_t j = 0; j < c->srec.size(); ++j) {
+      const gls_ctx::ChunkRec& x = c->srec[j];
+      const double h0 = at(x.h0), h1 = at(x.h1), c0 = at(x.c0), c1 = at(x.c1);
+      r->h2d_ms += h1 - h0;
+      r->compute_ms += c1 - c0;
+      r->h2d_bytes += x.hbytes;
+      r->d2h_bytes += x.dbytes;
+      end = std::max(end, c1);
+      if (x.d0) {
+        const double d1 = at(x.d1);
+        r->d2h_ms += d1 - at(x.d0);
+        end = std::max(end, d1);
+      }
+      if (j == 0) {
+        r->first_load_ms = c0 - h0;
+      } else {
+        // the compute stream's idle time between chunk j-1 and chunk j: the part before chunk j's
+        // data had arrived waited at wait(current X_blk), the rest at wait(previous b_blk)
+        const double stall = std::max(0.0, c0 - prev_c1);
+        const double on_h2d = std::min(stall, std::max(0.0, h1 - prev_c1));
+        r->exposed_h2d_ms += on_h2d;
+        r->exposed_other_ms += stall - on_h2d;
+      }
+      prev_c1 = c1;
+    }
+    r->tail_ms = std::max(0.0, end - prev_c1);
+    r->wall_ms = end;
+    r->chunks = (int64_t)c->srec.size();
+    for (auto& x : c->srec)
+      for (cudaEvent_t e : {x.h0, x.h1, x.c0, x.c1, x.d0, x.d1})
+        if (e) c->ev_pool.push_back(e);
+    c->srec.clear();
+  }
   return GLS_OK;
 }
 

@@ -36,13 +36,25 @@ class OocReport(ctypes.Structure):
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
+
+class StreamReport(ctypes.Structure):
+    """gls_stream_report: overlap accounting of the host -> HBM stream (Alg. 8)."""
+    _fields_ = [("chunks", ctypes.c_int64), ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
+                ("wall_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("compute_ms", ctypes.c_double),
+                ("d2h_ms", ctypes.c_double), ("first_load_ms", ctypes.c_double),
+                ("exposed_h2d_ms", ctypes.c_double), ("exposed_other_ms", ctypes.c_double),
+                ("tail_ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
 ABI_SYMBOLS = (
     "gls_create", "gls_solve_block", "gls_solve_block_ex", "gls_sync", "gls_set_stream",
     "gls_set_block_cols", "gls_destroy", "gls_failed_pivot", "gls_last_error",
     "gls_error_string", "gls_create_adopt", "gls_shared_view", "gls_commit_shared",
     "gls_kernel_launches", "gls_set_path", "gls_path_counts", "gls_solve_block_i8",
     "gls_set_timing", "gls_read_timing", "gls_get_dims", "gls_solve_file", "gls_select_block_size",
-    "gls_release_cached_memory",
+    "gls_release_cached_memory", "gls_set_stream_report", "gls_read_stream_report",
 )
 
 
@@ -115,6 +127,10 @@ def load(build_if_missing: bool = True):
     L.gls_select_block_size.argtypes = [i64, i32, i32, i32, i64, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_double, ctypes.POINTER(i32)]
     L.gls_select_block_size.restype = i64
+    L.gls_set_stream_report.argtypes = [vp, i32]
+    L.gls_set_stream_report.restype = ctypes.c_int
+    L.gls_read_stream_report.argtypes = [vp, ctypes.POINTER(StreamReport)]
+    L.gls_read_stream_report.restype = ctypes.c_int
     L.gls_release_cached_memory.argtypes = []
     L.gls_release_cached_memory.restype = ctypes.c_int
     _lib = L
@@ -228,6 +244,15 @@ class Context:
         self._check(self._lib.gls_read_timing(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                                               ctypes.byref(k)))
         return {"int8_ms": a.value, "fp64_ms": b.value, "conv_ms": c.value, "launches": k.value}
+
+    def set_stream_report(self, enable: bool = True):
+        self._check(self._lib.gls_set_stream_report(self._h, 1 if enable else 0))
+
+    def read_stream_report(self):
+        """Overlap accounting of the host chunks streamed since the last read (synchronises)."""
+        r = StreamReport()
+        self._check(self._lib.gls_read_stream_report(self._h, ctypes.byref(r)))
+        return r.as_dict()
 
     def sync(self):
         self._check(self._lib.gls_sync(self._h))

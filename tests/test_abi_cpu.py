@@ -76,6 +76,8 @@ def test_null_handles_extensions(lib):
     assert lib.gls_set_timing(None, 1) == 1
     d = ctypes.c_double()
     assert lib.gls_read_timing(None, ctypes.byref(d), ctypes.byref(d), ctypes.byref(d), ctypes.byref(a)) == 1
+    assert lib.gls_set_stream_report(None, 1) == 1
+    assert lib.gls_read_stream_report(None, None) == 1
 
 
 def test_select_block_size_condition():

@@ -244,6 +244,38 @@ def test_host_stream_equals_device_bitwise(glsmod):
         ctx.close()
 
 
+def test_stream_report_accounts_every_chunk(glsmod):
+    """Overlap accounting of the host -> HBM stream (Alg. 8): every chunk of every streamed call is
+    reported, the byte counts are exact, the engine times fit inside the wall time, and the
+    accounting changes no bit of b."""
+    n, pL, pR, m = 2048, 3, 1, 20000
+    P = gen.make_problem(n, pL, pR, seed=27)
+    XR = gen.make_XR(27, n, 0, m)
+    XRh = torch.from_numpy(XR).pin_memory()
+    G = torch.from_numpy(XR.astype(np.int8)).pin_memory()
+    with glsmod.Context(n, pL, pR, dev(P.M), dev(P.XL), dev(P.y)) as ctx:
+        ref = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+        ctx.solve_block(dev(XR), m, ref)
+        ref = ref.cpu()
+        ctx.set_block_cols(3000)
+        ctx.set_stream_report(True)
+        for label, fn, esz in (("f64", lambda bh, sh: ctx.solve_block(XRh, m, bh, sh), 8),
+                               ("i8", lambda bh, sh: ctx.solve_block_i8(G, m, bh, sh), 1)):
+            bh = torch.empty((m, 4), dtype=torch.float64).pin_memory()
+            sh = torch.empty(m, dtype=torch.int32).pin_memory()
+            fn(bh, sh)
+            r = ctx.read_stream_report()
+            assert torch.equal(bh, ref), label
+            nch = (m + 2999) // 3000 if label == "f64" else 1 + (m - 750 + 2999) // 3000  # i8: quarter first chunk
+            assert r["chunks"] == nch, (label, r)
+            assert r["h2d_bytes"] == m * n * esz and r["d2h_bytes"] == m * (4 * 8 + 4), (label, r)
+            busy = r["compute_ms"] + r["first_load_ms"] + r["exposed_h2d_ms"] + r["exposed_other_ms"] + r["tail_ms"]
+            assert r["wall_ms"] > 0 and abs(busy - r["wall_ms"]) <= 1e-3 * r["wall_ms"] + 0.05, (label, r)
+            assert min(r["first_load_ms"], r["exposed_h2d_ms"], r["exposed_other_ms"], r["tail_ms"]) >= 0, r
+            assert r["h2d_ms"] <= r["wall_ms"] and r["compute_ms"] <= r["wall_ms"], r
+        assert ctx.read_stream_report()["chunks"] == 0  # the read resets
+
+
 @pytest.mark.parametrize("piv", [5, 100, 200, 260, 299])
 def test_not_spd_pivot_matches_oracle(glsmod, piv):
     """The first failing pivot, wherever it falls: a 64-row leaf, the first or the second sweep of a
