@@ -44,17 +44,29 @@ OZ_SLICES = 7
 
 
 def int8_peak():
-    """Dense int8 tensor peak: the driver-measured bf16 GEMM rate (MEASURED_PEAKS.json) x the nominal
-    int8:bf16 ratio 4.5:2.25 (B200_PROFILING.md).  The BURST figure is the denominator: the kernel
-    runs inside a long step, but it measurably exceeds 2 x the sustained bf16 rate (it draws less
-    power than a dense bf16 GEMM), so the sustained figure would not bound it."""
+    """Dense int8 tensor peak, MEASURED on this pool's B200 by tools/umma_probe/peak_i8.cu
+    (profiles/r02_peak_i8.json: tcgen05.mma.cta_group::2.kind::i8, M = 256, N = 224 -- the hot kernel's
+    shape -- K = 32, operands resident in shared memory, 148 CTAs).  The hot kernel runs inside a long
+    step, so the SUSTAINED figure (back-to-back launches for 4 s) is the denominator; the burst figure
+    (one 20 ms launch) is reported beside it.  Fallback when the probe file is absent: 2 x the
+    driver-measured bf16 rates of MEASURED_PEAKS.json (nominal int8:bf16 = 4.5:2.25 PF dense).
+    Returns (denominator, other, source)."""
+    try:
+        rows = [json.loads(l) for l in open(os.path.join(ROOT, "profiles", "r02_peak_i8.json")) if l.strip()]
+        r = next(x for x in rows if x.get("N") == 224)
+        return (float(r["sustained_tops"]), float(r["burst_tops"]),
+                "tcgen05 kind::i8 M=256 N=224 K=32 microbenchmark (tools/umma_probe/peak_i8.cu, "
+                "profiles/r02_peak_i8.json): sustained %.1f TOP/s (4 s back to back) is the denominator; "
+                "burst %.1f" % (r["sustained_tops"], r["burst_tops"]))
+    except Exception:
+        pass
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         b, bs = float(mp["bf16_tflops"]), float(mp["bf16_tflops_sustained"])
-        return 2.0 * b, 2.0 * bs, ("2 x bf16_tflops %.1f (burst) of MEASURED_PEAKS.json; nominal int8:bf16 = "
-                                   "4.5:2.25 PF dense" % b)
+        return 2.0 * bs, 2.0 * b, ("2 x bf16_tflops_sustained %.1f of MEASURED_PEAKS.json; nominal int8:bf16 = "
+                                   "4.5:2.25 PF dense" % bs)
     except Exception:
-        return 2.0 * 1590.0, 2.0 * 1400.0, "2 x 1590 TF/s bf16 burst (B200_PROFILING.md fallback)"
+        return 2.0 * 1400.0, 2.0 * 1590.0, "2 x 1400 TF/s bf16 sustained (B200_PROFILING.md fallback)"
 
 
 def parse():
@@ -67,6 +79,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the sub-records (FP64 path, OOC, weak scaling)")
+    ap.add_argument("--scaling", default="auto", choices=["auto", "strong", "weak"],
+                    help="auto: strong (the config's m split over the GPUs) when N > 1")
+    ap.add_argument("--replicate", default="redundant", choices=["redundant", "bcast"],
+                    help="N > 1: every rank factors M (paper, PAPER.md:812-814) or rank 0 + NCCL broadcast")
     ap.add_argument("--codes", action="store_true",
                     help="config 4: stream X_R as int8 genotype codes (gls_solve_block_i8) instead of FP64")
     ap.add_argument("--seed", type=int, default=gen.DEFAULT_SEED)
@@ -141,12 +158,25 @@ def cpu_threads():
     return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
 
+def workload(args, cfg, world):
+    """(scaling, m_total, config dict) of the timed workload -- the same for both arms."""
+    scaling = args.scaling if args.scaling != "auto" else ("strong" if world > 1 else "weak")
+    m_total = (args.m or cfg.m) * (1 if scaling == "strong" else world)
+    conf = {"workload": "config%d: n=%d pL=%d pR=%d, %d SNPs in HBM, %s (rank r owns SNPs [%s))"
+                        % (args.config, cfg.n, cfg.pL, cfg.pR, m_total,
+                           "split over the GPUs" if scaling == "strong" else "per GPU",
+                           "floor(r m/N), floor((r+1) m/N)" if scaling == "strong" else "r m, (r+1) m"),
+            "n": cfg.n, "pL": cfg.pL, "pR": cfg.pR, "m_total": m_total, "seed": args.seed}
+    return scaling, m_total, conf
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cfg = gen.CONFIGS[args.config]
-    m = args.m or cfg.m
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    scaling, m, conf = workload(args, cfg, world)
     P = gen.config_problem(cfg, seed=args.seed)
     nsnp = 64 if cfg.n >= 5000 else 512
     L, t_chol, _ = oracle_sample(P, cfg, args.seed, 8)
@@ -158,13 +188,13 @@ def run_reference(args):
     rate = nsnp / statistics.median(times)
     value = m / (t_chol + m / rate)
     sample = ("oracle Cholesky of the full n=%d M (%.2f s, once) + %d seeded SNPs per step (Alg. 4 "
-              "per-problem steps); value = m / (t_chol + m / rate)" % (cfg.n, t_chol, nsnp))
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+              "per-problem steps); value = m / (t_chol + m / rate), m = the whole job's %d SNPs"
+              % (cfg.n, t_chol, nsnp, m))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": "config%d" % args.config, "n": cfg.n, "pL": cfg.pL, "pR": cfg.pR,
-                       "m_per_rank": m},
+            "config": conf,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -173,6 +203,131 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
+class Job:
+    """One rank's share of a config-2-shaped workload resident in HBM, and the step that solves it:
+    gls_create (each rank factors M itself -- the paper's "factorization of M redundantly",
+    PAPER.md:812-814 -- or rank 0 factors and broadcasts, --replicate bcast) + gls_solve_block over
+    the rank's SNPs, on a dedicated stream whose CUDA events bracket the library's launches."""
+
+    def __init__(self, args, cfg, P, world, rank, m_rank, g0, torch, pkg, multi, dist):
+        self.args, self.cfg, self.P, self.world, self.rank = args, cfg, P, world, rank
+        self.m, self.g0 = m_rank, g0
+        self.torch, self.pkg, self.multi, self.dist = torch, pkg, multi, dist
+        n, pR, p = cfg.n, cfg.pR, cfg.p
+        self.Md = torch.from_numpy(P.M).cuda()
+        self.XLd = torch.from_numpy(np.ascontiguousarray(P.XL)).cuda()
+        self.yd = torch.from_numpy(P.y).cuda()
+        self.Xd = torch.empty((max(m_rank, 1) * pR, n), dtype=torch.float64, device="cuda")
+        chunk = 65536
+        for c in range(0, m_rank * pR, chunk):
+            k = min(chunk, m_rank * pR - c)
+            pkg.gen_xr_device(args.seed, n, g0 * pR + c, k, self.Xd[c:c + k])
+        self.b = torch.empty((max(m_rank, 1), p), dtype=torch.float64, device="cuda")
+        self.st = torch.empty(max(m_rank, 1), dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
+        # a real (non-legacy) stream: the library's kernels are enqueued on it via gls_set_stream,
+        # so CUDA events recorded on it bracket exactly the fused kernel
+        self.stream = torch.cuda.Stream()
+        torch.cuda.set_stream(self.stream)
+
+    def make_ctx(self, Mx, XLx, yx):
+        cfg, pkg = self.cfg, self.pkg
+        if self.world > 1 and self.args.replicate == "bcast":
+            ctx = (pkg.Context(cfg.n, cfg.pL, cfg.pR, Mx, XLx, yx) if self.rank == 0
+                   else pkg.Context(cfg.n, cfg.pL, cfg.pR, adopt=True))
+            self.multi.replicate_shared(ctx, self.dist, src=0)
+        else:
+            ctx = pkg.Context(cfg.n, cfg.pL, cfg.pR, Mx, XLx, yx)
+        return ctx
+
+    def run(self, steps, warmup, path=None, clocks=None):
+        torch, dist, multi = self.torch, self.dist, self.multi
+        kern_ms, create_ms, timing, launches = [], [], [], [0]
+
+        def step(timed):
+            tc = time.perf_counter()
+            ctx = self.make_ctx(self.Md, self.XLd, self.yd)
+            if timed:
+                create_ms.append(1e3 * (time.perf_counter() - tc))
+            if path is not None:
+                ctx.set_path(path)
+            ctx.set_stream(self.stream.cuda_stream)
+            ctx.set_timing(timed)
+            k0 = torch.cuda.Event(enable_timing=True)
+            k1 = torch.cuda.Event(enable_timing=True)
+            k0.record(self.stream)
+            if self.m > 0:
+                ctx.solve_block(self.Xd, self.m, self.b, self.st, async_=True)
+            k1.record(self.stream)
+            ctx.sync()
+            if timed:
+                launches[0] += ctx.kernel_launches
+                k1.synchronize()
+                kern_ms.append(k0.elapsed_time(k1))
+                timing.append(ctx.read_timing())
+                timing[-1]["paths"] = ctx.path_counts()
+            ctx.close()
+
+        for _ in range(warmup):
+            step(False)
+        if clocks:
+            clocks.start()
+        if self.world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(self.stream)
+        for _ in range(steps):
+            step(True)
+        e1.record(self.stream)
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        clk = clocks.stop() if clocks else None
+        total_ms = e0.elapsed_time(e1)
+        vals = multi.max_over_ranks([total_ms, statistics.mean(kern_ms),
+                                     statistics.mean(t["int8_ms"] for t in timing),
+                                     statistics.mean(t["fp64_ms"] for t in timing),
+                                     statistics.mean(t["conv_ms"] for t in timing),
+                                     statistics.mean(create_ms)], dist, device="cuda")
+        return {"ms_per_step": vals[0] / steps, "solve_block_ms": vals[1], "int8_ms": vals[2], "fp64_ms": vals[3],
+                "conv_ms": vals[4], "create_ms": vals[5], "paths": timing[-1]["paths"], "launches": launches[0],
+                "clocks": clk}
+
+
+def int8_roofline(r, n, m, pR, traffic):
+    flops = float(n) * n * m * pR          # FP64 trsm flops, n^2 per X_R column (north star)
+    ops = OZ_SLICES * flops                # int8 ops: 7 digit products per FP64 MAC
+    peak, peak_burst, psrc = int8_peak()
+    achieved = ops / (r["int8_ms"] / 1e3) / 1e12
+    fp64eq = flops / (r["int8_ms"] / 1e3) / 1e12
+    return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s (int8)",
+            "frac": achieved / peak, "traffic": traffic, "kernel": "ozaki_trsm_gls_kernel",
+            "kernel_ms": r["int8_ms"],
+            "kernel_includes": "the FP64 -> int8 conversion of the next chunk's X_R (two convert-ahead "
+                               "warps, concurrent with the MMAs; only the first chunk's pass is separate)",
+            "fp64_fallback_ms": r["fp64_ms"] if r["paths"][1] > 0 else 0.0,
+            "solve_block_ms": r["solve_block_ms"], "exposed_overhead_ms": r["solve_block_ms"] - r["int8_ms"],
+            "create_ms": r["create_ms"], "int8_ops_per_launch": ops, "peak_source": psrc,
+            "frac_of_burst_peak": achieved / peak_burst, "burst_peak": peak_burst,
+            "fp64_equivalent": {"achieved_tflops": fp64eq, "dmma_peak_tflops": FP64_DMMA_PEAK_SUSTAINED,
+                                "ratio_to_dmma_peak": fp64eq / FP64_DMMA_PEAK_SUSTAINED,
+                                "note": "n^2 FP64 trsm flops per column / kernel time; the FP64 DMMA pipe "
+                                        "peak is measured in profiles/r01_probe.txt"}}
+
+
+def fp64_roofline(r, n, m, pR, traffic):
+    flops = float(n) * n * m * pR
+    achieved = flops / (r["fp64_ms"] / 1e3) / 1e12
+    return {"bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK_SUSTAINED, "unit": "TFLOP/s",
+            "frac": achieved / FP64_DMMA_PEAK_SUSTAINED, "traffic": traffic, "kernel": "fused_trsm_gls_kernel",
+            "kernel_ms": r["fp64_ms"], "solve_block_ms": r["solve_block_ms"], "create_ms": r["create_ms"],
+            "flops_per_launch": flops,
+            "peak_source": "FP64 DMMA.8x8x4 microbenchmark on this pool's B200, 4 s sustained "
+                           "(profiles/r01_probe.txt); MEASURED_PEAKS.json has no FP64 entry"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -186,105 +341,31 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = multi.local_device()
+    # GLS_BENCH_DEVICE / GLS_BENCH_BACKEND: functional checks of the N > 1 code path with several ranks
+    # on one GPU over gloo (tools/gpu_*.sh); never used for a measurement
+    local = int(os.environ.get("GLS_BENCH_DEVICE", multi.local_device()))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("GLS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     pkg.load()
 
     cfg = gen.CONFIGS[args.config]
     if args.config == 4:
         return run_ooc(args, cfg, world, rank, local)
     n, pL, pR, p = cfg.n, cfg.pL, cfg.pR, cfg.p
-    m = args.m or cfg.m
-    col0 = multi.weak_range(m, rank)[0] * pR  # this rank's SNP range [rank*m, (rank+1)*m)
-
+    scaling, m_total, conf = workload(args, cfg, world)
+    if scaling == "strong":
+        g0, g1 = multi.snp_range(m_total, world, rank)   # the config's m split over the ranks
+    else:
+        g0, g1 = multi.weak_range(args.m or cfg.m, rank)  # every rank owns a config-sized range
+    m = g1 - g0
     P = gen.config_problem(cfg, seed=args.seed)
-    Md = torch.from_numpy(P.M).cuda()
-    XLd = torch.from_numpy(np.ascontiguousarray(P.XL)).cuda()
-    yd = torch.from_numpy(P.y).cuda()
-    Xd = torch.empty((m * pR, n), dtype=torch.float64, device="cuda")
-    chunk = 65536
-    for c in range(0, m * pR, chunk):
-        k = min(chunk, m * pR - c)
-        pkg.gen_xr_device(args.seed, n, col0 + c, k, Xd[c:c + k])
-    b = torch.empty((m, p), dtype=torch.float64, device="cuda")
-    st = torch.empty(m, dtype=torch.int32, device="cuda")
-    torch.cuda.synchronize()
-    # a real (non-legacy) stream: the library's kernels are enqueued on it via gls_set_stream,
-    # so CUDA events recorded on it bracket exactly the fused kernel
-    stream = torch.cuda.Stream()
-    torch.cuda.set_stream(stream)
+    job = Job(args, cfg, P, world, rank, m, g0, torch, pkg, multi, dist)
 
-    def make_ctx(Mx, XLx, yx):
-        # rank 0 factors; the others adopt the broadcast shared state
-        if rank == 0:
-            ctx = pkg.Context(n, pL, pR, Mx, XLx, yx)
-        else:
-            ctx = pkg.Context(n, pL, pR, adopt=True)
-        if world > 1:
-            multi.replicate_shared(ctx, dist, src=0)
-        return ctx
-
-    kern_ms = []
-    create_ms = []
-    timing = []
-    launches = [0]
-
-    def step(timed: bool):
-        tc = time.perf_counter()
-        ctx = make_ctx(Md, XLd, yd)
-        if timed:
-            create_ms.append(1e3 * (time.perf_counter() - tc))
-        ctx.set_stream(stream.cuda_stream)
-        ctx.set_timing(timed)
-        k0 = torch.cuda.Event(enable_timing=True)
-        k1 = torch.cuda.Event(enable_timing=True)
-        k0.record(stream)
-        ctx.solve_block(Xd, m, b, st, async_=True)
-        k1.record(stream)
-        ctx.sync()
-        if timed:
-            launches[0] += ctx.kernel_launches
-            k1.synchronize()
-            kern_ms.append(k0.elapsed_time(k1))
-            timing.append(ctx.read_timing())
-            timing[-1]["paths"] = ctx.path_counts()
-        ctx.close()
-
-    for _ in range(args.warmup):
-        step(False)
-    clocks = ClockSampler(local)
-    clocks.start()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step(True)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    total_ms = e0.elapsed_time(e1)
-    total_ms, kern_avg_ms = multi.max_over_ranks([total_ms, statistics.mean(kern_ms)], dist, device="cuda")
-    ms_per_step = total_ms / args.steps
-    value = world * m / (ms_per_step / 1e3)
-
-    # parity spot check of this run's output against the planted structure is in tests/; here only
-    # a sanity count of RankDeficient rows (seeded data has none).
-    n_bad = int(st.sum().item())
-
-    # ---- roofline of the dominant kernel, timed per launch with CUDA events on its own stream
-    int8_ms = statistics.mean(t["int8_ms"] for t in timing)
-    fp64_ms = statistics.mean(t["fp64_ms"] for t in timing)
-    conv_ms = statistics.mean(t["conv_ms"] for t in timing)
-    int8_ms, fp64_ms, conv_ms, kern_avg_ms = multi.max_over_ranks([int8_ms, fp64_ms, conv_ms, kern_avg_ms],
-                                                                  dist, device="cuda")
-    flops_per_launch = float(n) * n * m * pR          # FP64 trsm flops, n^2 per X_R column (north star)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
@@ -292,40 +373,44 @@ def main():
             traffic = json.load(open(tfile)).get("config%d" % args.config)
         except Exception:
             traffic = None
-    paths = timing[-1]["paths"]
-    if paths[0] > 0:   # int8 digit-split path (integer genotypes)
-        ops = OZ_SLICES * flops_per_launch           # int8 ops: 7 digit products per FP64 MAC
-        peak, peak_sus, psrc = int8_peak()
-        achieved = ops / (int8_ms / 1e3) / 1e12
-        fp64eq = flops_per_launch / (int8_ms / 1e3) / 1e12
-        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s (int8)",
-                    "frac": achieved / peak, "traffic": traffic, "kernel": "ozaki_trsm_gls_kernel",
-                    "kernel_ms": int8_ms,
-                    "kernel_includes": "the FP64 -> int8 conversion of the next chunk's X_R (two convert-ahead "
-                                       "warps, concurrent with the MMAs; only the first chunk's pass is separate)",
-                    "fp64_fallback_ms": fp64_ms if paths[1] > 0 else 0.0,
-                    "solve_block_ms": kern_avg_ms, "exposed_overhead_ms": kern_avg_ms - int8_ms,
-                    "create_ms": statistics.mean(create_ms),
-                    "int8_ops_per_launch": ops, "peak_source": psrc,
-                    "frac_of_sustained_peak": achieved / peak_sus,
-                    "fp64_equivalent": {"achieved_tflops": fp64eq, "dmma_peak_tflops": FP64_DMMA_PEAK_SUSTAINED,
-                                        "ratio_to_dmma_peak": fp64eq / FP64_DMMA_PEAK_SUSTAINED,
-                                        "note": "n^2 FP64 trsm flops per column / kernel time; the FP64 "
-                                                "DMMA pipe peak is measured in profiles/r01_probe.txt"}}
-    else:              # FP64 DMMA path
-        achieved_tf = flops_per_launch / (fp64_ms / 1e3) / 1e12
-        roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_DMMA_PEAK_SUSTAINED,
-                    "unit": "TFLOP/s", "frac": achieved_tf / FP64_DMMA_PEAK_SUSTAINED, "traffic": traffic,
-                    "kernel": "fused_trsm_gls_kernel", "kernel_ms": fp64_ms, "solve_block_ms": kern_avg_ms,
-                    "create_ms": statistics.mean(create_ms), "flops_per_launch": flops_per_launch,
-                    "peak_source": "FP64 DMMA.8x8x4 microbenchmark on this pool's B200, 4 s sustained "
-                                   "(profiles/r01_probe.txt); MEASURED_PEAKS.json has no FP64 entry"}
 
+    r = job.run(args.steps, args.warmup, clocks=ClockSampler(local))
+    value = m_total / (r["ms_per_step"] / 1e3)
+    n_bad = int(job.st[:m].sum().item()) if m else 0
+    b_ref = job.b[:m].cpu()  # the main run's b (the sub-records below reuse job.b)
+    m_max = max(multi.max_over_ranks([float(m)], dist, device="cuda"))
+    roofline = (int8_roofline(r, n, int(m_max), pR, traffic) if r["paths"][0] > 0
+                else fp64_roofline(r, n, int(m_max), pR, traffic))
+    solve_only = m_total / (r["solve_block_ms"] / 1e3)
+
+    # ---- evidence that every rank holds the same shared state (redundant factorisations)
+    replication = None
+    if world > 1:
+        ctx = job.make_ctx(job.Md, job.XLd, job.yd)
+        dg = torch.tensor(multi.shared_state_digest(ctx), dtype=torch.int64, device="cuda")
+        ctx.close()
+        hi, lo = dg.clone(), dg.clone()
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        replication = {"mode": args.replicate, "shared_state_bitwise_equal_across_ranks": bool(torch.equal(hi, lo)),
+                       "evidence": "per-buffer 64-bit digests of the shared state (multi.shared_state_digest), "
+                                   "min == max over ranks"}
+
+    # ---- sub-records (fixed small step counts, so the default run stays within minutes)
+    subs = {}
+    if not args.no_sub and r["paths"][0] > 0:
+        # the FP64 tensor-pipe path on the same workload: the metric's "FP64 tensor-pipe % of peak"
+        r64 = job.run(2, 1, path=pkg.GLS_PATH_FP64)
+        rl64 = fp64_roofline(r64, n, int(m_max), pR, None)
+        subs["fp64_path"] = {"value": m_total / (r64["ms_per_step"] / 1e3), "unit": UNIT, "steps": 2, "warmup": 1,
+                             "ms_per_step": r64["ms_per_step"],
+                             "fp64_tensor_pipe_pct_of_peak": 100.0 * rl64["frac"], "roofline": rl64,
+                             "arithmetic": "FP64 on the DMMA tensor pipe (GLS_PATH_FP64), same step, same data"}
     # ---- e2e: the same job through the C ABI with HOST buffers, host<->device copies inside the
     # timed region (Alg. 8 double-buffered stream).  Primary: X_R as genotype codes (int8, one byte
     # per genotype -- gls_solve_block_i8); secondary: X_R as FP64 (gls_solve_block, 8 bytes).
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and job.m > 0:
         try:
             avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
         except (ValueError, OSError):
@@ -334,87 +419,183 @@ def main():
         Mh = torch.from_numpy(P.M).pin_memory()
         XLh = torch.from_numpy(np.ascontiguousarray(P.XL)).pin_memory()
         yh = torch.from_numpy(P.y).pin_memory()
+        mj = job.m
 
-        def timed_e2e(solve, m_e):
+        def timed_e2e(solve, m_e, steps):
             bh = torch.empty((m_e, p), dtype=torch.float64, pin_memory=True)
             sh = torch.empty(m_e, dtype=torch.int32, pin_memory=True)
 
             def one():
-                ctx = make_ctx(Mh, XLh, yh)
+                ctx = job.make_ctx(Mh, XLh, yh)
+                ctx.set_stream_report(True)
                 solve(ctx, m_e, bh, sh)
+                rep = ctx.read_stream_report()
                 ctx.close()
+                return rep
 
             one()
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            for _ in range(args.steps):
-                one()
+            reps = [one() for _ in range(steps)]
             torch.cuda.synchronize()
-            dt = multi.max_over_ranks([(time.perf_counter() - t0) / args.steps], dist, device="cuda")[0]
-            return dt, bool(torch.equal(bh, b[:m_e].cpu()))
+            dt = multi.max_over_ranks([(time.perf_counter() - t0) / steps], dist, device="cuda")[0]
+            return dt, bool(torch.equal(bh, b_ref[:m_e])), overlap_summary(reps[-1])
 
-        # int8 genotype codes: m x n bytes per rank
-        m_i8 = int(min(m, 0.6 * avail / local_world / (n * pR)))
-        m_i8 = max(m_i8 - m_i8 % 64, 64)
+        chunk = 65536
+        m_i8 = int(min(mj, 0.6 * avail / local_world / (n * pR)))
+        m_i8 = max(m_i8 - m_i8 % 64, 64) if m_i8 < mj else mj
         Gh = torch.empty((m_i8 * pR, n), dtype=torch.int8, pin_memory=True)
         for c in range(0, m_i8 * pR, chunk):
             k = min(chunk, m_i8 * pR - c)
-            Gh[c:c + k].copy_(Xd[c:c + k].to(torch.int8))
-        dt8, same8 = timed_e2e(lambda ctx, me, bh, sh: ctx.solve_block_i8(Gh, me, bh, sh), m_i8)
+            Gh[c:c + k].copy_(job.Xd[c:c + k].to(torch.int8))
+        dt8, same8, ov8 = timed_e2e(lambda ctx, me, bh, sh: ctx.solve_block_i8(Gh, me, bh, sh), m_i8, args.steps)
         del Gh
-        e2e = {"value": world * m_i8 / dt8, "unit": UNIT,
+        m_i8_all = multi.sum_over_ranks([float(m_i8)], dist, device="cuda")[0]
+        e2e = {"value": m_i8_all / dt8, "unit": UNIT,
                "h2d_bytes_per_step": int((n * n + n * (pL + 1)) * 8 + m_i8 * pR * n),
                "d2h_bytes_per_step": int(m_i8 * p * 8 + m_i8 * 4),
-               "m_per_rank": m_i8,
+               "m_per_rank": m_i8, "overlap": ov8,
                "path": "C ABI gls_solve_block_i8: M, X_L, y (FP64) and X_R as int8 genotype codes in pinned "
                        "host memory -> double-buffered H2D stream; b and status back to pinned host memory",
                "bitwise_equal_to_device_run": same8}
-        # FP64 X_R from host (8 bytes per genotype over PCIe), on at most 250k SNPs per rank (20 GB
-        # pinned per rank at n = 1e4: a secondary number, kept cheap for the multi-GPU runs)
-        m_f = int(min(m, 250_000, 0.6 * avail / local_world / (n * pR * 8)))
+        # FP64 X_R from host (8 bytes per genotype over PCIe): a SUBSET of the rank's SNPs (at most 250k,
+        # 20 GB of pinned memory per rank at n = 1e4), 2 timed steps
+        m_f = int(min(mj, 250_000, 0.6 * avail / local_world / (n * pR * 8)))
         m_f = max(m_f - m_f % 64, 64)
         Xh = torch.empty((m_f * pR, n), dtype=torch.float64, pin_memory=True)
         for c in range(0, m_f * pR, chunk):
             k = min(chunk, m_f * pR - c)
-            Xh[c:c + k].copy_(Xd[c:c + k])
-        dtf, samef = timed_e2e(lambda ctx, me, bh, sh: ctx.solve_block(Xh, me, bh, sh), m_f)
+            Xh[c:c + k].copy_(job.Xd[c:c + k])
+        dtf, samef, ovf = timed_e2e(lambda ctx, me, bh, sh: ctx.solve_block(Xh, me, bh, sh), m_f, 2)
         del Xh
-        e2e["fp64_host_input"] = {"value": world * m_f / dtf, "unit": UNIT, "m_per_rank": m_f,
+        m_f_all = multi.sum_over_ranks([float(m_f)], dist, device="cuda")[0]
+        e2e["fp64_host_input"] = {"value": m_f_all / dtf, "unit": UNIT, "m_per_rank": m_f,
+                                  "subset": m_f < mj,
+                                  "note": "a subset of the rank's SNPs (PCIe-bound: 8 bytes per genotype); "
+                                          "rate = subset SNPs / subset time",
                                   "h2d_bytes_per_step": int((n * n + n * (pL + 1) + m_f * pR * n) * 8),
-                                  "d2h_bytes_per_step": int(m_f * p * 8 + m_f * 4),
+                                  "d2h_bytes_per_step": int(m_f * p * 8 + m_f * 4), "overlap": ovf,
+                                  "h2d_roofline_snps_per_s": H2D_GBS * 1e9 / (8.0 * n * pR),
                                   "path": "C ABI gls_solve_block, FP64 X_R in pinned host memory",
                                   "bitwise_equal_to_device_run": samef}
+
+    if world > 1 and scaling == "strong" and not args.no_sub:
+        # weak scaling as a labelled sub-record: every rank owns a full config-sized range
+        job = None
+        torch.cuda.empty_cache()
+        mw = args.m or cfg.m
+        gw0, gw1 = multi.weak_range(mw, rank)
+        jw = Job(args, cfg, P, world, rank, mw, gw0, torch, pkg, multi, dist)
+        rw = jw.run(2, 1)
+        subs["weak_scaling"] = {"value": world * mw / (rw["ms_per_step"] / 1e3), "unit": UNIT,
+                                "m_per_rank": mw, "ms_per_step": rw["ms_per_step"], "steps": 2, "warmup": 1}
+        del jw
+
+    # ---- out-of-core sub-record (config-4 shape, reduced m): the Alg. 8 stream from pinned host
+    # memory, codes and FP64, with the overlap accounting of every chunk
+    if not args.no_sub and args.config == 2:
+        job = None
+        torch.cuda.empty_cache()
+        subs["ooc_config4_reduced"] = ooc_subrecord(args, gen.CONFIGS[4], world, rank, pkg, multi, dist, torch)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nsnp = 64 if n >= 5000 else 512
         L, t_chol, t_snp = oracle_sample(P, cfg, args.seed, nsnp)
         rate = nsnp / t_snp
-        cpu = {"value": m / (t_chol + m / rate), "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+        cpu = {"value": m_total / (t_chol + m_total / rate), "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
                "sample": "oracle Cholesky of the full n=%d M (%.2f s) + %d seeded SNPs of the workload "
                          "(%.2f s); value = m / (t_chol + m / rate)" % (n, t_chol, nsnp, t_snp)}
 
     if rank == 0:
+        int8 = roofline["kernel"].startswith("ozaki")
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+                "scaling": scaling, "vs_baseline": None,
+                "dtype": "f64 (exact int8x7 digit products)" if int8 else "f64",
+                "data": "synthetic",
                 "arithmetic": ("FP64 results; the trsm as exact int8 x int8 -> int32 digit products on tcgen05 "
                                "(T = L^-1 split into 7 base-256 digits, 55 bits per row; X_R integer) combined "
-                               "and reduced in FP64 (DESIGN.md reading A15)") if roofline["kernel"].startswith("ozaki")
+                               "and reduced in FP64 (DESIGN.md reading A15)") if int8
                               else "FP64 on the DMMA tensor pipe",
-                "config": {"workload": "config%d: n=%d pL=%d pR=%d, %d SNPs per GPU in HBM (rank r owns "
-                                       "SNPs [r*m, (r+1)*m))" % (args.config, n, pL, pR, m),
-                           "n": n, "pL": pL, "pR": pR, "m_per_rank": m, "seed": args.seed,
-                           "step": "gls_create (+NCCL broadcast) + gls_solve_block over all rank SNPs",
-                           "l2": "inputs larger than L2 (X_R %.1f GB per rank)" % (m * pR * n * 8 / 1e9)},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches[0],
-                "clocks": clk, "rank_deficient_rows": n_bad}
+                "config": {**conf, "m_per_rank_max": int(m_max), "replicate": args.replicate if world > 1 else None,
+                           "step": "gls_create (every rank factors M itself, or rank 0 + NCCL broadcast) + "
+                                   "gls_solve_block over the rank's SNPs",
+                           "l2": "inputs larger than L2 (X_R %.1f GB per rank)" % (m_max * pR * n * 8 / 1e9)},
+                "solve_only": {"value": solve_only, "unit": UNIT,
+                               "note": "SNPs / gls_solve_block time, gls_create excluded (SURVEY §8(d)'s timed "
+                                       "region); value above includes gls_create every step"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": r["launches"],
+                "clocks": r["clocks"], "rank_deficient_rows": n_bad, "replication": replication, **subs}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def overlap_summary(rep):
+    """Fractions of the stream report (gls_read_stream_report) for the JSON line."""
+    w = rep["wall_ms"] or 1e-9
+    exposed = rep["first_load_ms"] + rep["exposed_h2d_ms"] + rep["exposed_other_ms"] + rep["tail_ms"]
+    return {"chunks": rep["chunks"], "wall_ms": rep["wall_ms"], "h2d_busy_frac": rep["h2d_ms"] / w,
+            "compute_busy_frac": rep["compute_ms"] / w, "d2h_busy_frac": rep["d2h_ms"] / w,
+            "exposed_wait_pct": 100.0 * exposed / w, "first_load_ms": rep["first_load_ms"],
+            "exposed_h2d_ms": rep["exposed_h2d_ms"], "exposed_other_ms": rep["exposed_other_ms"],
+            "tail_ms": rep["tail_ms"], "h2d_gbs": rep["h2d_bytes"] / max(rep["h2d_ms"], 1e-9) / 1e6}
+
+
+def ooc_subrecord(args, cfg, world, rank, pkg, multi, dist, torch):
+    """Config-4-shaped out-of-core stream with a reduced m (2e6 SNPs per rank): the blocks of a pool
+    of 2 distinct pinned host blocks cycled (block j = pool block j mod 2), once as int8 genotype codes
+    and once as FP64, one warm-up and one timed pass each, with per-chunk overlap accounting."""
+    from paper_1210_7325_b200 import ooc
+    n, pL, pR, p = cfg.n, cfg.pL, cfg.pR, cfg.p
+    m = 2_000_000
+    P = gen.config_problem(cfg, seed=args.seed)
+    Md = torch.from_numpy(P.M).cuda()
+    XLd = torch.from_numpy(np.ascontiguousarray(P.XL)).cuda()
+    yd = torch.from_numpy(P.y).cuda()
+    blk = ooc.host_block_groups(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count, pR)
+    g0 = multi.weak_range(m, rank)[0]
+    tmp = torch.empty((blk * pR, n), dtype=torch.float64, device="cuda")
+    pool64 = torch.empty((2, blk * pR, n), dtype=torch.float64, pin_memory=True)
+    pool8 = torch.empty((2, blk * pR, n), dtype=torch.int8, pin_memory=True)
+    for k in range(2):
+        pkg.gen_xr_device(args.seed, n, (g0 + k * blk) * pR, blk * pR, tmp)
+        pool64[k].copy_(tmp)
+        pool8[k].copy_(tmp.to(torch.int8))
+    del tmp
+    b = torch.empty((m, p), dtype=torch.float64, pin_memory=True)
+    st = torch.empty(m, dtype=torch.int32, pin_memory=True)
+    out = {"m_per_rank": m, "block_snps": blk, "pool_blocks": 2,
+           "snp_to_block": "block j -> pool block j mod 2", "steps": 1, "warmup": 1}
+    peak8, _, _ = int8_peak()
+    for name, pool, codes, esz in (("codes", pool8, True, 1), ("fp64", pool64, False, 8)):
+        res = None
+        for it in range(2):
+            ctx = pkg.Context(n, pL, pR, Md, XLd, yd)
+            ctx.set_stream_report(True)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ooc.stream_from_pool(ctx, pool, m, blk, b, st, codes=codes)
+            dt = time.perf_counter() - t0
+            rep = ctx.read_stream_report()
+            ctx.close()
+            res = (dt, rep)
+        dt, rep = res
+        dt = multi.max_over_ranks([dt], dist, device="cuda")[0]
+        t_comp = OZ_SLICES * float(n) * n * m * pR / (peak8 * 1e12)
+        t_h2d = float(esz) * n * m * pR / (H2D_GBS * 1e9)
+        out[name] = {"value": world * m / dt, "unit": UNIT, "s_per_pass": dt,
+                     "bound": "tensor (int8)" if t_comp >= t_h2d else "h2d",
+                     "roofline_frac": max(t_comp, t_h2d) / dt,
+                     "t_compute_roofline_s": t_comp, "t_h2d_roofline_s": t_h2d,
+                     "h2d_bytes": int(esz * n * m * pR), "overlap": overlap_summary(rep)}
+    return out
 
 
 # ----------------------------------------------------------------------------- config 4 (OOC)

@@ -69,3 +69,27 @@ def max_over_ranks(values, dist, device=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(x) for x in t.cpu()]
+
+
+def sum_over_ranks(values, dist, device=None):
+    """Element-wise sum of a list of floats over all ranks."""
+    import torch
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(x) for x in t.cpu()]
+
+
+def shared_state_digest(ctx) -> list[int]:
+    """One 64-bit checksum per shared-state buffer of `ctx` (wrapping sum of its 8-byte words, plus
+    a position-weighted sum), computed on the device.  Equal digests on every rank are the evidence
+    that redundant per-rank factorisations (the paper's plan) produced the same bits."""
+    import torch
+    out = []
+    for t in ctx.shared_tensors():
+        nb = t.numel() - t.numel() % 8
+        w = t[:nb].view(torch.int64)
+        pos = torch.arange(w.numel(), device=w.device, dtype=torch.int64) % 65521 + 1
+        out.append(int(w.sum().item()))
+        out.append(int((w * pos).sum().item()))
+    return out

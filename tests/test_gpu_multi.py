@@ -1,11 +1,15 @@
 """Replicate-then-shard through the real library on one GPU.
 
 Two processes, world size 2 over the gloo backend (NCCL refuses two ranks on one device; only one GPU
-is available to this build), both on cuda:0: rank 0 runs gls_create, rank 1 gls_create_adopt; the
-shared state (packed T, W, G, the int8 digit tiles of T and V, the row scales) is broadcast from
-rank 0 with multi.replicate_shared -- the same code bench.py runs over NCCL -- then each rank solves
-its own SNP range.  The two shards must equal a single-process solve bit for bit, and rank 1 must have
-done its work on the int8 path with the broadcast state.  The ranks' kernels never wait on each other.
+is available to this build), both on cuda:0.  Two ways to replicate the shared state:
+  bcast     -- rank 0 runs gls_create, rank 1 gls_create_adopt; the shared state (packed T, W, G, the
+               int8 digit tiles of T and V, the row scales) is broadcast from rank 0 with
+               multi.replicate_shared (the code bench.py runs with --replicate bcast);
+  redundant -- every rank runs gls_create itself (the paper's "factorization of M redundantly",
+               PAPER.md:812-814; bench.py's default), and the shared-state digests must agree.
+Then each rank solves its strong-scaling shard multi.snp_range(m, 2, rank) of an odd m.  The two
+shards must equal a single-process solve of all m problems bit for bit, and both ranks must have done
+their work on the int8 path.  The ranks' kernels never wait on each other.
 """
 import os
 
@@ -17,11 +21,11 @@ import gen
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-N, PL, PR, M_PER_RANK = 700, 3, 1, 3000
+N, PL, PR, M_TOTAL = 700, 3, 1, 6001
 SEED = 31
 
 
-def _rank_main(rank, world, init_file, out_dir):
+def _rank_main(rank, world, init_file, out_dir, mode):
     import torch
     import torch.distributed as dist
 
@@ -32,17 +36,18 @@ def _rank_main(rank, world, init_file, out_dir):
     dist.init_process_group("gloo", init_method="file://" + init_file, rank=rank, world_size=world)
     P = gen.make_problem(N, PL, PR, seed=SEED)
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    if rank == 0:
-        ctx = pkg.Context(N, PL, PR, d(P.M), d(P.XL), d(P.y))
+    if mode == "bcast":
+        ctx = pkg.Context(N, PL, PR, d(P.M), d(P.XL), d(P.y)) if rank == 0 else pkg.Context(N, PL, PR, adopt=True)
+        # the library's shared buffers broadcast from rank 0 (gloo: staged through host memory)
+        multi.replicate_shared(ctx, dist, src=0)
     else:
-        ctx = pkg.Context(N, PL, PR, adopt=True)
-    # the library's shared buffers broadcast from rank 0 (gloo: staged through host memory)
-    multi.replicate_shared(ctx, dist, src=0)
-    lo, hi = multi.weak_range(M_PER_RANK, rank)
-    X = torch.empty((M_PER_RANK * PR, N), dtype=torch.float64, device="cuda")
-    pkg.gen_xr_device(SEED, N, lo * PR, M_PER_RANK * PR, X)
-    b = torch.empty((M_PER_RANK, PL + PR), dtype=torch.float64, device="cuda")
-    ctx.solve_block(X, M_PER_RANK, b)
+        ctx = pkg.Context(N, PL, PR, d(P.M), d(P.XL), d(P.y))
+    np.save(os.path.join(out_dir, "digest%d.npy" % rank), np.array(multi.shared_state_digest(ctx)))
+    lo, hi = multi.snp_range(M_TOTAL, world, rank)
+    X = torch.empty((hi - lo) * PR, N, dtype=torch.float64, device="cuda")
+    pkg.gen_xr_device(SEED, N, lo * PR, (hi - lo) * PR, X)
+    b = torch.empty((hi - lo, PL + PR), dtype=torch.float64, device="cuda")
+    ctx.solve_block(X, hi - lo, b)
     counts = ctx.path_counts()
     np.save(os.path.join(out_dir, "b%d.npy" % rank), b.cpu().numpy())
     np.save(os.path.join(out_dir, "paths%d.npy" % rank), np.array(counts))
@@ -51,7 +56,8 @@ def _rank_main(rank, world, init_file, out_dir):
     dist.destroy_process_group()
 
 
-def test_replicate_then_shard_two_processes(tmp_path):
+@pytest.mark.parametrize("mode", ["bcast", "redundant"])
+def test_replicate_then_shard_two_processes(tmp_path, mode):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
@@ -59,18 +65,20 @@ def test_replicate_then_shard_two_processes(tmp_path):
     import paper_1210_7325_b200 as pkg
 
     init_file = str(tmp_path / "dist_init")
-    mp.start_processes(_rank_main, args=(2, init_file, str(tmp_path)), nprocs=2, join=True,
+    mp.start_processes(_rank_main, args=(2, init_file, str(tmp_path), mode), nprocs=2, join=True,
                        start_method="spawn")
     b0, b1 = np.load(tmp_path / "b0.npy"), np.load(tmp_path / "b1.npy")
+    assert len(b0) == M_TOTAL // 2 and len(b1) == M_TOTAL - M_TOTAL // 2
     for r in (0, 1):
         assert tuple(np.load(tmp_path / ("paths%d.npy" % r))) == (1, 0)  # int8 path on both ranks
-    # single-process reference over both ranks' SNPs
+    np.testing.assert_array_equal(np.load(tmp_path / "digest0.npy"), np.load(tmp_path / "digest1.npy"))
+    # single-process reference over all m problems
     P = gen.make_problem(N, PL, PR, seed=SEED)
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    X = torch.empty((2 * M_PER_RANK * PR, N), dtype=torch.float64, device="cuda")
-    pkg.gen_xr_device(SEED, N, 0, 2 * M_PER_RANK * PR, X)
+    X = torch.empty((M_TOTAL * PR, N), dtype=torch.float64, device="cuda")
+    pkg.gen_xr_device(SEED, N, 0, M_TOTAL * PR, X)
     with pkg.Context(N, PL, PR, d(P.M), d(P.XL), d(P.y)) as ctx:
-        b = torch.empty((2 * M_PER_RANK, PL + PR), dtype=torch.float64, device="cuda")
-        ctx.solve_block(X, 2 * M_PER_RANK, b)
+        b = torch.empty((M_TOTAL, PL + PR), dtype=torch.float64, device="cuda")
+        ctx.solve_block(X, M_TOTAL, b)
         ref = b.cpu().numpy()
     np.testing.assert_array_equal(np.concatenate([b0, b1]), ref)
