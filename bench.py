@@ -174,6 +174,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # torchrun sets OMP_NUM_THREADS=1 for every rank; rank 0 runs the oracle alone (the other ranks
+        # exit at once), so it gets the host's cores -- read by libgomp when oracle/ is first loaded
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     cfg = gen.CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     scaling, m, conf = workload(args, cfg, world)

@@ -215,6 +215,25 @@ int64_t gls_select_block_size(int64_t n, int32_t p, int32_t pR, int32_t elem_byt
                               double compute_groups_per_s, double io_bytes_per_s, double io_latency_s,
                               int32_t* io_bound);
 
+/* ---- GenABEL's gwfgls (Alg. 6) on the B200 kernels: a rung of the algorithm
+ * ladder (NEXT-2 of SURVEY §8(f)) kept for Table II's cost comparison, not the hot
+ * path.  It follows the listing: M^{-1} explicitly (line 1; here T^T T with T = L^{-1} from this
+ * library's potrf + inverse), W_L = M^{-1} X_L (line 2), then per problem w = M^{-1} x_R (line 3:
+ * GLS_GWFGLS_GEMV = one gemv per column as listed, GLS_GWFGLS_GEMM = the block's gemvs as one GEMM),
+ * S_i = W^T X_i with all p x p entries (line 4), W^T y (line 5) and an LU solve with partial pivoting
+ * (line 6; a zero or non-finite pivot => NaN record, status 1).
+ *   gls_gwfgls_create: as gls_create (M, X_L, y host or device, copied; GLS_ERR_NOT_SPD if potrf fails).
+ *   gls_gwfgls_solve:  X_R (n x m_blk pR, column-major) and b_out (m_blk x p) / status_out (nullable)
+ *                      are DEVICE pointers; synchronous.  Errors: GLS_ERR_ARG, GLS_ERR_DIM, GLS_ERR_CUDA. */
+typedef struct gls_gwfgls gls_gwfgls;
+enum { GLS_GWFGLS_GEMV = 0, GLS_GWFGLS_GEMM = 1 };
+int gls_gwfgls_create(int64_t n, int32_t pL, int32_t pR, const double* M, const double* X_L, const double* y,
+                      gls_gwfgls** out);
+int gls_gwfgls_solve(gls_gwfgls* g, const double* X_R, int64_t m_blk, double* b_out, int32_t* status_out,
+                     int32_t mode);
+int64_t gls_gwfgls_launches(const gls_gwfgls* g);
+void gls_gwfgls_destroy(gls_gwfgls* g);
+
 #ifdef __cplusplus
 }
 #endif

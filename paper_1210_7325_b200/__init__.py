@@ -3,5 +3,6 @@
 `gls` is the ctypes binding of libgls.so (C ABI in include/gls.h); `build` compiles the
 in-tree CUDA libraries for sm_100a.  See DESIGN.md.
 """
-from .gls import (GLS_OOC_ASYNC, GLS_OOC_SYNC, GLS_PATH_AUTO, GLS_PATH_FP64, Context, GLSError,  # noqa: F401
-                  gen_xr_device, load, release_cached_memory, select_block_size)
+from .gls import (GLS_GWFGLS_GEMM, GLS_GWFGLS_GEMV, GLS_OOC_ASYNC, GLS_OOC_SYNC, GLS_PATH_AUTO,  # noqa: F401
+                  GLS_PATH_FP64, Context, GLSError, Gwfgls, gen_xr_device, load, release_cached_memory,
+                  select_block_size)

@@ -22,7 +22,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-Xcompiler", "-Wall"]
 
 LIBS = {
-    "libgls.so": ["gls_api.cu", "dgemm.cu", "chol_inv.cu", "fused_trsm_gls.cu", "ozaki_gls.cu", "ooc_file.cu"],
+    "libgls.so": ["gls_api.cu", "dgemm.cu", "chol_inv.cu", "fused_trsm_gls.cu", "ozaki_gls.cu", "ooc_file.cu",
+                  "gwfgls.cu"],
     "libglsgen_dev.so": ["gen_device.cu"],
 }
 DEPS = ["gls_internal.cuh", "umma.cuh", os.path.join("..", "..", "include", "gls.h")]

@@ -25,6 +25,8 @@ GLS_PATH_AUTO = 0
 GLS_PATH_FP64 = 1
 GLS_OOC_SYNC = 0
 GLS_OOC_ASYNC = 1
+GLS_GWFGLS_GEMV = 0
+GLS_GWFGLS_GEMM = 1
 
 
 class OocReport(ctypes.Structure):
@@ -55,6 +57,7 @@ ABI_SYMBOLS = (
     "gls_kernel_launches", "gls_set_path", "gls_path_counts", "gls_solve_block_i8",
     "gls_set_timing", "gls_read_timing", "gls_get_dims", "gls_solve_file", "gls_select_block_size",
     "gls_release_cached_memory", "gls_set_stream_report", "gls_read_stream_report",
+    "gls_gwfgls_create", "gls_gwfgls_solve", "gls_gwfgls_launches", "gls_gwfgls_destroy",
 )
 
 
@@ -131,6 +134,14 @@ def load(build_if_missing: bool = True):
     L.gls_set_stream_report.restype = ctypes.c_int
     L.gls_read_stream_report.argtypes = [vp, ctypes.POINTER(StreamReport)]
     L.gls_read_stream_report.restype = ctypes.c_int
+    L.gls_gwfgls_create.argtypes = [i64, i32, i32, dp, dp, dp, ctypes.POINTER(vp)]
+    L.gls_gwfgls_create.restype = ctypes.c_int
+    L.gls_gwfgls_solve.argtypes = [vp, dp, i64, dp, dp, i32]
+    L.gls_gwfgls_solve.restype = ctypes.c_int
+    L.gls_gwfgls_launches.argtypes = [vp]
+    L.gls_gwfgls_launches.restype = i64
+    L.gls_gwfgls_destroy.argtypes = [vp]
+    L.gls_gwfgls_destroy.restype = None
     L.gls_release_cached_memory.argtypes = []
     L.gls_release_cached_memory.restype = ctypes.c_int
     _lib = L
@@ -321,3 +332,44 @@ def gen_xr_device(seed: int, n: int, col0: int, ncols: int, X, ld: int | None = 
     rc = load_gen().glsgen_dev_xr(seed, n, col0, ncols, X.data_ptr(), ld or n, stream)
     if rc != 0:
         raise GLSError(GLS_ERR_CUDA, "glsgen_dev_xr failed with cudaError %d" % rc)
+
+
+class Gwfgls:
+    """GenABEL's gwfgls (Alg. 6) on the B200 kernels (gls_gwfgls_*): a ladder rung for
+    Table II's cost comparison.  Device tensors only for solve()."""
+
+    def __init__(self, n: int, pL: int, pR: int, M, X_L, y):
+        L = load()
+        self._lib = L
+        self.n, self.pL, self.pR, self.p = n, pL, pR, pL + pR
+        h = ctypes.c_void_p()
+        rc = L.gls_gwfgls_create(n, pL, pR, _ptr(M), _ptr(X_L) if pL > 0 else None, _ptr(y), ctypes.byref(h))
+        if rc != GLS_OK:
+            raise GLSError(rc, error_string(rc))
+        self._h = h
+
+    def solve(self, X_R, m_blk: int, b_out, status_out=None, mode: int = GLS_GWFGLS_GEMV):
+        rc = self._lib.gls_gwfgls_solve(self._h, _ptr(X_R), m_blk, _ptr(b_out), _ptr(status_out, "int32"), mode)
+        if rc != GLS_OK:
+            raise GLSError(rc, error_string(rc))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self._lib.gls_gwfgls_launches(self._h))
+
+    def close(self):
+        if self._h and self._h.value:
+            self._lib.gls_gwfgls_destroy(self._h)
+        self._h = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

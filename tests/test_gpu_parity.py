@@ -743,3 +743,25 @@ def test_config4_full_stream(glsmod, n1e4_factor):
     assert_parity(bd[sel], np.zeros(len(sel), np.int32), b_or, st_or, label="config4 sample")
     record_parity("config4 n=1e4 p=4 m=1e7 streamed: 1024 seeded + %d edge SNPs" % (len(sel) - 1024),
                   bd[sel], b_or, st_or)
+
+
+@pytest.mark.parametrize("n,pL,pR,m", [(500, 3, 1, 300), (260, 16, 4, 40), (300, 0, 2, 50)])
+def test_gwfgls_rung_matches_oracle(glsmod, n, pL, pR, m):
+    """NEXT-2: GenABEL's gwfgls (Alg. 6) on the B200 kernels -- explicit M^-1, per-column
+    gemv (as listed) or one GEMM per block, full p x p S_i = W^T X_i, gesv -- reaches Eq. (1)'s b: every
+    problem against the oracle in both modes; a zero SNP is RankDeficient (NaN, status 1)."""
+    P = gen.make_problem(n, pL, pR, with_sex=pL >= 3, seed=28 + n)
+    XR = gen.make_XR(28 + n, n, 0, m * pR)
+    XR[3 * pR:4 * pR] = 0.0  # problem 3: an all-zero genotype block
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, pR)
+    assert st_or[3] == 1
+    with glsmod.Gwfgls(n, pL, pR, dev(P.M), dev(P.XL) if pL else None, dev(P.y)) as g:
+        for mode in (glsmod.GLS_GWFGLS_GEMV, glsmod.GLS_GWFGLS_GEMM):
+            b = torch.empty((m, pL + pR), dtype=torch.float64, device="cuda")
+            st = torch.empty(m, dtype=torch.int32, device="cuda")
+            g.solve(dev(XR), m, b, st, mode=mode)
+            b, st = b.cpu().numpy(), st.cpu().numpy()
+            assert_parity(b, st, b_or, st_or, label="gwfgls mode %d" % mode)
+        assert g.kernel_launches > 0
+        with pytest.raises(glsmod.GLSError):
+            g.solve(dev(XR), 0, torch.empty((1, pL + pR), dtype=torch.float64, device="cuda"))
