@@ -282,10 +282,37 @@ void trmm_lower_t_skinny(cudaStream_t s, int64_t n, int k, const double* T, int6
   if (lc) ++*lc;
 }
 
+#ifdef GLS_AB_CUBLAS
+}  // namespace gls
+#include <cublas_v2.h>
+namespace gls {
+// A/B diagnostics only (build with -DGLS_AB_CUBLAS, run with GLS_DGEMM_CUBLAS=1): the same products
+// through cuBLAS DGEMM (full K ranges, full C) to price the GEMM kernel's efficiency in gls_create.
+static bool ab_cublas(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                      char opA, const double* B, int64_t ldb, char opB, double beta, double* C, int64_t ldc) {
+  static const bool on = getenv("GLS_DGEMM_CUBLAS") != nullptr;
+  if (!on) return false;
+  static cublasHandle_t h[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!h[dev]) cublasCreate(&h[dev]);
+  cublasSetStream(h[dev], s);
+  cublasDgemm(h[dev], opA == 'T' ? CUBLAS_OP_T : CUBLAS_OP_N, opB == 'T' ? CUBLAS_OP_T : CUBLAS_OP_N, (int)M, (int)N,
+              (int)K, &alpha, A, (int)lda, B, (int)ldb, &beta, C, (int)ldc);
+  return true;
+}
+#endif
+
 void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, char opA, const double* B, int64_t ldb, char opB, double beta, double* C,
            int64_t ldc, int flags, int64_t* launch_counter, double* ws, int max_ctas) {
   if (M <= 0 || N <= 0) return;
+#ifdef GLS_AB_CUBLAS
+  if (ab_cublas(s, M, N, K, alpha, A, lda, opA, B, ldb, opB, beta, C, ldc)) {
+    if (launch_counter) ++*launch_counter;
+    return;
+  }
+#endif
   GemmParams p{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, flags, 1, nullptr};
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
   // small output, long K: split K so the launch fills the machine (the recursion's deep levels)
