@@ -42,6 +42,13 @@
 #include "gls_internal.cuh"
 #include "umma.cuh"
 
+// TMEM round trips per row-block drain in the epilogue: 2 = digits 0-3 then 4-6 (default; integer
+// sums, so the same bits as 4 = two digits per load pair).  A/B on one box (tools/gpu_ab_drain.sh,
+// config 2): 232.0 vs 233.5 ms per 1e6 SNPs (~0.7 %); config 3: no measurable difference.
+#ifndef GLS_OZ_DRAIN_RT
+#define GLS_OZ_DRAIN_RT 2
+#endif
+
 namespace gls {
 namespace {
 
@@ -405,6 +412,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // in int64 (two partial sums), then one FP64 rounding each
     auto drain = [&](int sl, double (&z)[16]) {
       const uint32_t tr = tlane + sl * 256 + h * 16;
+#if GLS_OZ_DRAIN_RT == 2
+      // two TMEM round trips: digits 0-3 (the high part), then digits 4-6
+      long long hi[16];
+      {
+        int32_t d0[16], d1[16], d2[16], d3[16];
+        tmem_ld16(tr, d0);
+        tmem_ld16(tr + 1 * kR, d1);
+        tmem_ld16(tr + 2 * kR, d2);
+        tmem_ld16(tr + 3 * kR, d3);
+        tmem_wait_ld();
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          hi[r] = (long long)d0[r] * 16777216LL + (long long)d1[r] * 65536LL + (long long)d2[r] * 256LL +
+                  (long long)d3[r];
+      }
+      {
+        int32_t d4[16], d5[16], d6[16];
+        tmem_ld16(tr + 4 * kR, d4);
+        tmem_ld16(tr + 5 * kR, d5);
+        tmem_ld16(tr + 6 * kR, d6);
+        tmem_wait_ld();
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const long long lo = (long long)d4[r] * 65536LL + (long long)d5[r] * 256LL + (long long)d6[r];
+          z[r] = fma((double)hi[r], 16777216.0, (double)lo);
+        }
+      }
+#else
       long long hi[16], lo[16];
       int32_t va[16], vb[16];
       // two digits per TMEM round trip (4 waits instead of 7)
@@ -427,6 +462,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tmem_wait_ld();
 #pragma unroll
       for (int r = 0; r < 16; ++r) z[r] = fma((double)hi[r], 16777216.0, (double)(lo[r] + (long long)va[r]));
+#endif
     };
     // acc layout: the Gram row at the bottom, acc[b] (b < pR), the V block's outputs at the top,
     // acc[NA - 1 - w] (w < pL + 1): static register indices for both whatever pL and pR are.
