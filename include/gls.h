@@ -113,6 +113,15 @@ const char* gls_error_string(int code);         /* static text for any return co
 int gls_create_adopt(int64_t n, int32_t pL, int32_t pR, gls_ctx** out);
 int gls_shared_view(gls_ctx* ctx, void** ptrs, int64_t* bytes, int32_t* count);
 int gls_commit_shared(gls_ctx* ctx);
+/* Int8-only replication: gls_create_adopt_int8 allocates only the int8 path's shared state (no packed T
+ * for the FP64 kernel -- n^2 * 4 bytes less per GPU, never broadcast); the root lists the matching
+ * buffers with gls_shared_view_ex(ctx, GLS_SHARE_INT8_ONLY, ...).  An int8-only context solves genotype
+ * codes (gls_solve_block_i8) and integer-valued double X_R (converted on the device; a block holding any
+ * other value fails with GLS_ERR_ARG and the call synchronises); gls_set_path(GLS_PATH_FP64) on it is
+ * GLS_ERR_STATE.  GLS_ERR_DIM when n > 131071. */
+enum { GLS_SHARE_INT8_ONLY = 1 };
+int gls_create_adopt_int8(int64_t n, int32_t pL, int32_t pR, gls_ctx** out);
+int gls_shared_view_ex(gls_ctx* ctx, int32_t flags, void** ptrs, int64_t* bytes, int32_t* count);
 
 /* Number of kernel launches this context issued so far (evidence counter for bench.py). */
 int64_t gls_kernel_launches(const gls_ctx* ctx);
@@ -233,6 +242,43 @@ int gls_gwfgls_solve(gls_gwfgls* g, const double* X_R, int64_t m_blk, double* b_
                      int32_t mode);
 int64_t gls_gwfgls_launches(const gls_gwfgls* g);
 void gls_gwfgls_destroy(gls_gwfgls* g);
+
+/* ---- Distributed create: M beyond one GPU (NEXT-3 of SURVEY §8(f); §6).
+ * G ranks (one per GPU) each hold the column blocks j (width nb, a multiple of 128) with j % G == rank
+ * of M and of T = L^{-1}, and run a right-looking blocked Cholesky fused with the forward substitution
+ * that forms T, one panel per block column, then build the int8 path's shared state from the
+ * distributed T.  The library computes; the caller moves data between the steps (e.g. torch.distributed
+ * over NCCL; paper_1210_7325_b200/multi.py dist_create runs the whole protocol):
+ *   for k in 0..K-1:  owner (k % G): gls_dist_step(FACTOR, k)  (GLS_ERR_NOT_SPD: pivot in
+ *                                    gls_dist_failed_pivot; every rank must stop)
+ *                     broadcast the GLS_DIST_PANEL buffer of k from the owner
+ *                     all: gls_dist_step(UPDATE, k)
+ *   all: gls_dist_step(PARTIALS);  W = sum over ranks (in rank order) of every rank's GLS_DIST_WPART,
+ *        written to GLS_DIST_W;  GLS_DIST_ROWMAX all-reduced with MAX
+ *   all: gls_dist_step(PACK);      GLS_DIST_VMAX all-reduced with MAX
+ *   all: gls_dist_step(PACK2);     GLS_DIST_T8 and GLS_DIST_V8 all-reduced with SUM (bytes; each byte has
+ *                                  exactly one nonzero contributor)
+ *   all: gls_dist_finish -> an int8-only context (see gls_create_adopt_int8), identical on every rank.
+ * gls_dist_create: M (n x n column-major, host or device; each rank copies its own column blocks),
+ * X_L, y as gls_create; GLS_ERR_ARG unless 0 <= rank < nranks and nb is a positive multiple of 128;
+ * GLS_ERR_DIM unless the gls_create conditions hold and n <= 131071.  Device memory per rank:
+ * 2 n (n / G) 8 bytes for the local blocks of M and T (+ a n x nb panel), plus the int8 state.
+ * gls_dist_buffer: device pointer and byte size of a buffer (k: block index for GLS_DIST_PANEL).
+ * Every step synchronises.  gls_dist_finish hands the context to the caller (destroy it with
+ * gls_destroy); gls_dist_destroy frees the rest. */
+typedef struct gls_dist gls_dist;
+enum { GLS_DIST_FACTOR = 0, GLS_DIST_UPDATE = 1, GLS_DIST_PARTIALS = 2, GLS_DIST_PACK = 3, GLS_DIST_PACK2 = 4 };
+enum { GLS_DIST_PANEL = 0, GLS_DIST_WPART = 1, GLS_DIST_W = 2, GLS_DIST_ROWMAX = 3, GLS_DIST_VMAX = 4,
+       GLS_DIST_T8 = 5, GLS_DIST_V8 = 6 };
+int gls_dist_create(int64_t n, int32_t pL, int32_t pR, int64_t nb, int32_t nranks, int32_t rank, const double* M,
+                    const double* X_L, const double* y, gls_dist** out);
+int gls_dist_info(const gls_dist* d, int64_t* nb, int64_t* nblocks, int64_t* nloc);
+int gls_dist_buffer(gls_dist* d, int32_t which, int64_t k, void** ptr, int64_t* bytes);
+int gls_dist_step(gls_dist* d, int32_t phase, int64_t k);
+int gls_dist_finish(gls_dist* d, gls_ctx** out);
+int64_t gls_dist_failed_pivot(const gls_dist* d);
+int64_t gls_dist_launches(const gls_dist* d);
+void gls_dist_destroy(gls_dist* d);
 
 #ifdef __cplusplus
 }

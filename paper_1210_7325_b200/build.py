@@ -23,7 +23,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-X
 
 LIBS = {
     "libgls.so": ["gls_api.cu", "dgemm.cu", "chol_inv.cu", "fused_trsm_gls.cu", "ozaki_gls.cu", "ooc_file.cu",
-                  "gwfgls.cu"],
+                  "gwfgls.cu", "dist_create.cu"],
     "libglsgen_dev.so": ["gen_device.cu"],
 }
 DEPS = ["gls_internal.cuh", "umma.cuh", os.path.join("..", "..", "include", "gls.h")]

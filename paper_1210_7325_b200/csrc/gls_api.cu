@@ -63,6 +63,7 @@ struct gls_ctx {
   size_t vscale_bytes = 0;
   int path = GLS_PATH_AUTO;
   bool oz_ok = false;  // n small enough for exact int32 digit products
+  bool fp64_ok = true;  // false: an int8-only context (no packed T for the FP64 kernel; gls_create_adopt_int8)
   // int8 conversion workspaces (two, swapping roles) and their rejection flags
   int64_t x8_cols = 0, ld8 = 0;
   double* sws = nullptr;     // per-problem records for the separate posv of large p (OzArgs::s_ws)
@@ -212,7 +213,7 @@ int check_dims(int64_t n, int32_t pL, int32_t pR) {
   return GLS_OK;
 }
 
-int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
+int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR, bool fp64_state = true) {
   c->n = n;
   c->pL = pL;
   c->pR = pR;
@@ -245,8 +246,13 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR) {
   c->Tpk_bytes = (size_t)tpk_total_tiles(c->NB) * kTileDoubles * sizeof(double);
   c->Wpk_bytes = (size_t)c->NB * wpk_rb_doubles(c->NW) * sizeof(double);
   c->G_bytes = (size_t)(pL + 1) * (pL + 1) * sizeof(double);
-  CK(c, dalloc(c, &c->Tpk, c->Tpk_bytes));
-  CK(c, dalloc(c, &c->Wpk, c->Wpk_bytes));
+  c->fp64_ok = fp64_state;
+  if (fp64_state) {
+    CK(c, dalloc(c, &c->Tpk, c->Tpk_bytes));
+    CK(c, dalloc(c, &c->Wpk, c->Wpk_bytes));
+  } else {
+    c->Tpk_bytes = c->Wpk_bytes = 0;
+  }
   CK(c, dalloc(c, &c->G, c->G_bytes));
   CK(c, dalloc(c, &c->flags, 2 * sizeof(int) + 2 * sizeof(unsigned long long)));
   CK(c, dalloc(c, &c->ran, 2 * sizeof(unsigned long long)));
@@ -283,10 +289,12 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   cudaStream_t s = c->stream;
   double *A = nullptr, *T = nullptr, *B = nullptr, *W = nullptr;
   int* esc = nullptr;
+  double* rmax = nullptr;  // row maxima of T (int8 setup scratch)
   CholStatus* st = nullptr;
   CholStatus hst;
   int rc = GLS_OK;
   auto cleanup = [&]() {
+    dfree(c, rmax);
     dfree(c, A);
     dfree(c, T);
     dfree(c, B);
@@ -321,7 +329,10 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   CKS(dalloc(c, &B, (size_t)n * (pL + 1) * sizeof(double)));
   CKS(dalloc(c, &W, (size_t)n * (pL + 1) * sizeof(double)));
   CKS(dalloc(c, &st, sizeof(CholStatus)));
-  if (c->oz_ok) CKS(dalloc(c, &esc, (size_t)((n + kOzR - 1) / kOzR) * kOzR * sizeof(int)));
+  if (c->oz_ok) {
+    CKS(dalloc(c, &esc, (size_t)((n + kOzR - 1) / kOzR) * kOzR * sizeof(int)));
+    CKS(dalloc(c, &rmax, (size_t)((n + kOzR - 1) / kOzR) * kOzR * sizeof(double)));
+  }
   mark("alloc");
   // A host M is uploaded in column chunks on the h2d stream while the factorisation runs: the
   // recursion works left to right and waits for the chunks each kernel touches, so only the first
@@ -391,7 +402,7 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   if (c->oz_ok) {
     // V = T^T W = M^{-1} [X_L | y] into B (free again: W = T B is formed)
     trmm_lower_t_skinny(s, n, pL + 1, T, n, W, n, B, n, &c->launches);
-    oz_setup(s, T, n, n, W, pL + 1, c->T8, c->aux, esc, B, c->V8, c->vscale, &c->launches);
+    oz_setup(s, T, n, n, W, pL + 1, c->T8, c->aux, esc, B, c->V8, c->vscale, rmax, &c->launches);
   }
   CKS(cudaGetLastError());
   CKS(cudaStreamSynchronize(s));
@@ -561,6 +572,44 @@ int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* 
   return GLS_OK;
 }
 
+// An int8-only context (no packed T for the FP64 kernel): a double X block is converted chunk by chunk
+// by standalone passes and solved on the int8 path; a chunk that is not integer-valued cannot fall back
+// to the FP64 kernel, so the block fails with GLS_ERR_ARG (checked on the host after the block: this
+// entry point synchronises).
+int run_kernel_int8_only(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt) {
+  const int pR = c->pR, p = c->p;
+  const int64_t cpt = 4 * (int64_t)((32 / pR) * pR);
+  const int64_t wave_groups = (int64_t)c->num_sms * cpt / pR;
+  const int64_t ld8 = (c->n + 15) & ~(int64_t)15;
+  int64_t cap = std::min<int64_t>(8 * wave_groups, kSerialChunkBytes / (ld8 * pR)) / wave_groups * wave_groups;
+  if (cap < wave_groups) cap = wave_groups;
+  const int64_t chunk = std::min(cap, groups);
+  int rc = ensure_x8(c, chunk * pR);
+  if (rc) return rc;
+  unsigned long long* work = (unsigned long long*)(c->flags + 2);
+  CK(c, cudaMemsetAsync(c->flags, 0, sizeof(int), c->stream));
+  for (int64_t g0 = 0; g0 < groups; g0 += chunk) {
+    const int64_t gc = std::min(chunk, groups - g0);
+    CK(c, cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->stream));
+    {
+      LaunchTimer lt(c, c->stream, 2);
+      oz_convert(c->stream, X + (size_t)g0 * pR * ldx, ldx, c->n, gc * pR, c->x8[0], c->ld8, c->flags, work,
+                 c->num_sms, &c->launches);
+      CK(c, cudaGetLastError());
+    }
+    rc = run_int8(c, c->x8[0], c->ld8, gc, b + (size_t)g0 * p, stt ? stt + g0 : nullptr, nullptr);
+    if (rc) return rc;
+  }
+  int bad = 0;
+  CK(c, cudaMemcpyAsync(&bad, c->flags, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  if (bad) {
+    c->err = "int8-only context: X_R holds a value that is not an integer in [-128, 127] (no FP64 fallback)";
+    return GLS_ERR_ARG;
+  }
+  return GLS_OK;
+}
+
 // One block of device-resident double X (column-major, ld = ldx, even, 16-byte aligned).
 // Path AUTO: chunks of up to 8 waves of int8 tiles (1, 2, .. 8, 8, ..).  Chunk 0 is converted to int8
 // by a standalone pass; every later chunk j+1 is converted by the convert-ahead warps of the int8
@@ -569,6 +618,7 @@ int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* 
 // the int8 kernel and the FP64 kernel are both launched, each gated on the device by the chunk's
 // flag, so exactly one of them does the work and the host never waits.
 int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt) {
+  if (!c->fp64_ok) return run_kernel_int8_only(c, X, ldx, groups, b, stt);
   if (c->path == GLS_PATH_FP64 || !c->oz_ok) return run_fp64(c, X, ldx, groups, b, stt, nullptr);
   const int pR = c->pR, p = c->p;
   const int64_t cpt = 4 * (int64_t)((32 / pR) * pR);
@@ -858,28 +908,50 @@ int gls_create_adopt(int64_t n, int32_t pL, int32_t pR, gls_ctx** out) {
   return GLS_OK;
 }
 
-int gls_shared_view(gls_ctx* c, void** ptrs, int64_t* bytes, int32_t* count) {
-  if (!c || !ptrs || !bytes || !count) return GLS_ERR_ARG;
-  if (c->state == ST_FAILED) return GLS_ERR_STATE;
-  ptrs[0] = c->Tpk;
-  bytes[0] = (int64_t)c->Tpk_bytes;
-  ptrs[1] = c->Wpk;
-  bytes[1] = (int64_t)c->Wpk_bytes;
-  ptrs[2] = c->G;
-  bytes[2] = (int64_t)c->G_bytes;
-  *count = 3;
-  if (c->oz_ok) {
-    ptrs[3] = c->T8;
-    bytes[3] = (int64_t)c->T8_bytes;
-    ptrs[4] = c->aux;
-    bytes[4] = (int64_t)c->aux_bytes;
-    ptrs[5] = c->V8;
-    bytes[5] = (int64_t)c->V8_bytes;
-    ptrs[6] = c->vscale;
-    bytes[6] = (int64_t)c->vscale_bytes;
-    *count = 7;
-  }
+int gls_create_adopt_int8(int64_t n, int32_t pL, int32_t pR, gls_ctx** out) {
+  if (!out) return GLS_ERR_ARG;
+  *out = nullptr;
+  int rc = check_dims(n, pL, pR);
+  if (rc) return rc;
+  if (n > kOzMaxN) return GLS_ERR_DIM;
+  gls_ctx* c = new gls_ctx();
+  *out = c;
+  rc = ctx_init(c, n, pL, pR, false);
+  if (rc) return rc;
+  c->state = ST_ADOPT;
   return GLS_OK;
+}
+
+int gls_shared_view_ex(gls_ctx* c, int32_t flags, void** ptrs, int64_t* bytes, int32_t* count) {
+  if (!c || !ptrs || !bytes || !count || (flags & ~GLS_SHARE_INT8_ONLY)) return GLS_ERR_ARG;
+  if (c->state == ST_FAILED) return GLS_ERR_STATE;
+  const bool fp64 = c->fp64_ok && !(flags & GLS_SHARE_INT8_ONLY);
+  if (!fp64 && !c->oz_ok) return GLS_ERR_STATE;
+  int k = 0;
+  if (fp64) {
+    ptrs[k] = c->Tpk;
+    bytes[k++] = (int64_t)c->Tpk_bytes;
+    ptrs[k] = c->Wpk;
+    bytes[k++] = (int64_t)c->Wpk_bytes;
+  }
+  ptrs[k] = c->G;
+  bytes[k++] = (int64_t)c->G_bytes;
+  if (c->oz_ok) {
+    ptrs[k] = c->T8;
+    bytes[k++] = (int64_t)c->T8_bytes;
+    ptrs[k] = c->aux;
+    bytes[k++] = (int64_t)c->aux_bytes;
+    ptrs[k] = c->V8;
+    bytes[k++] = (int64_t)c->V8_bytes;
+    ptrs[k] = c->vscale;
+    bytes[k++] = (int64_t)c->vscale_bytes;
+  }
+  *count = k;
+  return GLS_OK;
+}
+
+int gls_shared_view(gls_ctx* c, void** ptrs, int64_t* bytes, int32_t* count) {
+  return gls_shared_view_ex(c, 0, ptrs, bytes, count);
 }
 
 int gls_commit_shared(gls_ctx* c) {
@@ -1166,6 +1238,7 @@ void gls_destroy(gls_ctx* c) {
 int gls_set_path(gls_ctx* c, int32_t path) {
   if (!c) return GLS_ERR_ARG;
   if (path != GLS_PATH_AUTO && path != GLS_PATH_FP64) return GLS_ERR_ARG;
+  if (path == GLS_PATH_FP64 && !c->fp64_ok) return GLS_ERR_STATE;
   c->path = path;
   return GLS_OK;
 }

@@ -142,9 +142,29 @@ inline int oz_nv(int pl1) { return ((8 * pl1 + 31) / 32) * 32; }
 // aux table [sigma_r, W~_r,0 .. W~_r,pL] (stride pl1 + 1, ceil(n/32)*32 rows).  escale: int[rows].
 // V = T^T W = M^{-1} [X_L | y] (n x pl1, column-major) -> column scales vscale[pl1] and digit tiles
 // V8 (oz_nchunks(n) x oz_nv(pl1) x 128 bytes): S_BL and b_B of a column x are x^T V (§5.4).
+// Column ownership of T for the setup kernels: global column j is owned when (j / nb) % nranks == rank,
+// and lives at local column ((j / nb) / nranks) nb + j % nb of the rank's array.  The default owns
+// every column at its own index (single-GPU create).
+struct ColOwn {
+  int64_t nb = (int64_t)1 << 40;
+  int nranks = 1, rank = 0;
+  __host__ __device__ bool owned(int64_t j) const { return (j / nb) % nranks == rank; }
+  __host__ __device__ int64_t local(int64_t j) const { return ((j / nb) / nranks) * nb + j % nb; }
+};
+// Setup of the int8 path from T = L^{-1} (dense, column-major, ld) and W = [X~_L | y~], V = M^{-1}[X_L|y]:
+// row scales + aux, digit tiles T8, V digits.  scratch: (n + 31) / 32 * 32 doubles.
 void oz_setup(cudaStream_t s, const double* T, int64_t ld, int64_t n, const double* W, int pl1,
               int8_t* T8, double* aux, int* escale, const double* V, int8_t* V8, double* vscale,
-              int64_t* launch_counter);
+              double* scratch, int64_t* lc);
+// Its steps, for the distributed create (dist_create.cu), each touching owned columns / chunks only:
+void oz_rowmax(cudaStream_t s, const double* T, int64_t ld, int64_t n, ColOwn own, double* rowmax, int64_t* lc);
+void oz_rowscale(cudaStream_t s, const double* rowmax, int64_t n, int* escale, double* aux, int pl1, int64_t* lc);
+void oz_pack(cudaStream_t s, const double* T, int64_t ld, int64_t n, ColOwn own, const int* escale, int8_t* T8,
+             int64_t* lc);
+void oz_aux_from_w(cudaStream_t s, const double* W, int64_t n, int pl1, double* aux, int64_t* lc);
+void oz_vmax(cudaStream_t s, const double* V, int64_t n, int pl1, ColOwn own, double* vmax, int64_t* lc);
+void oz_vdigits(cudaStream_t s, const double* V, int64_t n, int pl1, ColOwn own, const double* vmax, int* ev,
+                double* vscale, int8_t* V8, int64_t* lc);
 // X (double) -> X8 (int8, ld8 % 16 == 0); *flag |= 1 if some value is not an integer in [-128,127].
 // work: a zeroed unsigned long long (the pass's work-stealing counter).
 void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t cols, int8_t* X8,

@@ -668,45 +668,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------- setup kernels
-// Row scale: e_r with max_j |T_rj| 2^e_r <= 127; sigma_r = 2^-(e_r + 48).  One CTA per 32 rows,
+// Every setup kernel reads T through a column-ownership map (ColOwn, gls_internal.cuh): the single-GPU
+// create owns every column (identity map); the distributed create (dist_create.cu) gives each rank the
+// column blocks j with j % nranks == rank, stored contiguously, and a kernel only touches owned columns.
+
+// Row maxima over owned columns: rowmax_r = max_{j <= r, j owned} |T_rj|.  One CTA per 32 rows,
 // 8 column strands per row (T column-major, so a warp reads 32 consecutive rows of one column).
-__global__ void oz_rowscale_kernel(const double* __restrict__ T, int64_t ld, int64_t n,
-                                   int* __restrict__ escale, double* __restrict__ aux, int as) {
+__global__ void oz_rowmax_kernel(const double* __restrict__ T, int64_t ld, int64_t n, ColOwn own,
+                                 double* __restrict__ rowmax) {
   __shared__ double sm[8][32];
   const int rl = threadIdx.x & 31, strand = threadIdx.x >> 5;
   const int64_t r = (int64_t)blockIdx.x * 32 + rl;
   double mx = 0.0;
   if (r < n) {
 #pragma unroll 8
-    for (int64_t j = strand; j <= r; j += 8) mx = fmax(mx, fabs(T[r + j * ld]));
+    for (int64_t j = strand; j <= r; j += 8)
+      if (own.owned(j)) mx = fmax(mx, fabs(T[r + own.local(j) * ld]));
   }
   sm[strand][rl] = mx;
   __syncthreads();
   if (strand == 0) {
     for (int k = 1; k < 8; ++k) mx = fmax(mx, sm[k][rl]);
-    int e = 0;
-    double sig = 0.0;
-    if (mx > 0.0) {
-      int E;
-      const double f = frexp(mx, &E);  // mx = f 2^E, f in [0.5, 1)
-      e = (f * 128.0 <= 127.0) ? 7 - E : 6 - E;
-      sig = ldexp(1.0, -(e + 48));
-    }
+    rowmax[r] = mx;  // rows >= n: 0
+  }
+}
+
+// Row scale from the row maximum: e_r with max_j |T_rj| 2^e_r <= 127; sigma_r = 2^-(e_r + 48).
+__device__ __forceinline__ void scale_of(double mx, int& e, double& sig) {
+  e = 0;
+  sig = 0.0;
+  if (mx > 0.0) {
+    int E;
+    const double f = frexp(mx, &E);  // mx = f 2^E, f in [0.5, 1)
+    e = (f * 128.0 <= 127.0) ? 7 - E : 6 - E;
+    sig = ldexp(1.0, -(e + 48));
+  }
+}
+__global__ void oz_rowscale_kernel(const double* __restrict__ rowmax, int64_t rows, int* __restrict__ escale,
+                                   double* __restrict__ aux, int as) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    int e;
+    double sig;
+    scale_of(rowmax[r], e, sig);
     escale[r] = e;
     aux[r * as] = sig;  // rows >= n: sigma = 0 (their T digits are zero too)
   }
 }
 
-// Digits of every element of every packed tile: tile (i, c) holds rows 32i..32i+31, K columns
-// 128c..128c+127; B row s*32 + rr holds digit s of row 32i + rr (plain 128-byte rows; the TMA load
-// applies the 128-byte swizzle).
-__global__ void oz_pack_kernel(const double* __restrict__ T, int64_t ld, int64_t n,
+// Digits of every element of every packed tile whose K chunk is owned: tile (i, c) holds rows
+// 32i..32i+31, K columns 128c..128c+127; B row s*32 + rr holds digit s of row 32i + rr (plain
+// 128-byte rows; the TMA load applies the 128-byte swizzle).  Tiles of chunks owned by other ranks
+// are not written (the distributed create sums the ranks' zero-initialised T8 buffers).
+__global__ void oz_pack_kernel(const double* __restrict__ T, int64_t ld, int64_t n, ColOwn own,
                                const int* __restrict__ escale, int NBR, int8_t* __restrict__ T8) {
   const int64_t tile = blockIdx.x;
   int i = (int)sqrt(2.0 * (double)tile);  // invert oz_tile_offset
   while (i > 0 && oz_tile_offset(i) > tile) --i;
   while (i + 1 <= NBR && oz_tile_offset(i + 1) <= tile) ++i;
   const int c = (int)(tile - oz_tile_offset(i));
+  if (!own.owned((int64_t)c * kKC)) return;  // a chunk lies inside one column block (nb % 128 == 0)
   int8_t* dst = T8 + tile * (int64_t)kOzTileBytes;
   // thread = (row rr of the block, 16 consecutive K): reads T column-major (a warp covers 32 rows of
   // one column: coalesced), writes one 16-byte vector per digit
@@ -721,7 +741,7 @@ __global__ void oz_pack_kernel(const double* __restrict__ T, int64_t ld, int64_t
     for (int kk = 0; kk < 16; ++kk) {
       const int64_t j = (int64_t)c * kKC + kq * 16 + kk;
       long long V = 0;
-      if (r < n && j <= r) V = llrint(ldexp(T[r + j * ld], e + 48));
+      if (r < n && j <= r) V = llrint(ldexp(T[r + own.local(j) * ld], e + 48));
 #pragma unroll
       for (int s = kNSL - 1; s > 0; --s) {  // signed base-256 digits, least significant first
         const int8_t lo = (int8_t)(V & 0xff);
@@ -736,40 +756,41 @@ __global__ void oz_pack_kernel(const double* __restrict__ T, int64_t ld, int64_t
   }
 }
 
-// Column scales of V = M^{-1} [X_L | y] (n x pl1): e_w with max_r |V_rw| 2^e_w <= 127.  One CTA per column.
-__global__ void oz_vscale_kernel(const double* __restrict__ V, int64_t n, int* __restrict__ ev,
-                                 double* __restrict__ vscale) {
+// Column maxima of V = M^{-1} [X_L | y] (n x pl1) over the rows of owned chunks.  One CTA per column.
+__global__ void oz_vmax_kernel(const double* __restrict__ V, int64_t n, ColOwn own, double* __restrict__ vmax) {
   __shared__ double sm[256];
   const int w = blockIdx.x;
   double mx = 0.0;
-  for (int64_t r = threadIdx.x; r < n; r += blockDim.x) mx = fmax(mx, fabs(V[r + w * n]));
+  for (int64_t r = threadIdx.x; r < n; r += blockDim.x)
+    if (own.owned(r)) mx = fmax(mx, fabs(V[r + w * n]));
   sm[threadIdx.x] = mx;
   __syncthreads();
   for (int k = 128; k > 0; k >>= 1) {
     if (threadIdx.x < k) sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + k]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    mx = sm[0];
-    int e = 0;
-    double sig = 0.0;
-    if (mx > 0.0) {
-      int E;
-      const double f = frexp(mx, &E);
-      e = (f * 128.0 <= 127.0) ? 7 - E : 6 - E;
-      sig = ldexp(1.0, -(e + 48));
-    }
+  if (threadIdx.x == 0) vmax[w] = sm[0];
+}
+// Column scales of V: e_w with max_r |V_rw| 2^e_w <= 127.
+// vmax and vscale may alias (each thread reads its maximum before writing its scale)
+__global__ void oz_vscale_kernel(const double* vmax, int pl1, int* __restrict__ ev, double* vscale) {
+  const int w = threadIdx.x;
+  if (w < pl1) {
+    int e;
+    double sig;
+    scale_of(vmax[w], e, sig);
     ev[w] = e;
     vscale[w] = sig;
   }
 }
 
-// Digit tiles of V: chunk c holds NV rows of 128 bytes (K = rows 128c..128c+127 of V); row 8w + s is
-// digit s (most significant first) of column w; rows 8w + 7 and w >= pl1 are zero.  Plain layout:
-// the TMA load applies the 128-byte swizzle.
-__global__ void oz_vpack_kernel(const double* __restrict__ V, int64_t n, int pl1, const int* __restrict__ ev,
-                                int NV, int8_t* __restrict__ V8) {
+// Digit tiles of V for the owned chunks: chunk c holds NV rows of 128 bytes (K = rows 128c..128c+127
+// of V); row 8w + s is digit s (most significant first) of column w; rows 8w + 7 and w >= pl1 are
+// zero.  Plain layout: the TMA load applies the 128-byte swizzle.
+__global__ void oz_vpack_kernel(const double* __restrict__ V, int64_t n, int pl1, ColOwn own,
+                                const int* __restrict__ ev, int NV, int8_t* __restrict__ V8) {
   const int c = blockIdx.x;
+  if (!own.owned((int64_t)c * kKC)) return;
   int8_t* dst = V8 + (int64_t)c * NV * kKC;
   for (int idx = threadIdx.x; idx < (NV / 8) * kKC; idx += blockDim.x) {
     const int w = idx / kKC, k = idx % kKC;
@@ -958,21 +979,53 @@ __global__ void __launch_bounds__(256) oz_repack_kernel(const int8_t* __restrict
 
 int64_t oz_total_tiles(int64_t NBR) { return oz_tile_offset(NBR); }
 
+void oz_rowmax(cudaStream_t s, const double* T, int64_t ld, int64_t n, ColOwn own, double* rowmax, int64_t* lc) {
+  const int NBR = (int)((n + kR - 1) / kR);
+  oz_rowmax_kernel<<<NBR, 256, 0, s>>>(T, ld, n, own, rowmax);
+  if (lc) ++*lc;
+}
+void oz_rowscale(cudaStream_t s, const double* rowmax, int64_t n, int* escale, double* aux, int pl1, int64_t* lc) {
+  const int64_t rows = (n + kR - 1) / kR * kR;
+  oz_rowscale_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(rowmax, rows, escale, aux, pl1 + 1);
+  if (lc) ++*lc;
+}
+void oz_pack(cudaStream_t s, const double* T, int64_t ld, int64_t n, ColOwn own, const int* escale, int8_t* T8,
+             int64_t* lc) {
+  const int NBR = (int)((n + kR - 1) / kR);
+  oz_pack_kernel<<<(unsigned)oz_total_tiles(NBR), 256, 0, s>>>(T, ld, n, own, escale, NBR, T8);
+  if (lc) ++*lc;
+}
+void oz_aux_from_w(cudaStream_t s, const double* W, int64_t n, int pl1, double* aux, int64_t* lc) {
+  const int64_t rows = (n + kR - 1) / kR * kR;
+  const int64_t tot = rows * pl1;
+  oz_aux_w_kernel<<<(unsigned)((tot + 255) / 256 < 2048 ? (tot + 255) / 256 : 2048), 256, 0, s>>>(W, n, n, pl1, rows,
+                                                                                                   aux);
+  if (lc) ++*lc;
+}
+void oz_vmax(cudaStream_t s, const double* V, int64_t n, int pl1, ColOwn own, double* vmax, int64_t* lc) {
+  oz_vmax_kernel<<<pl1, 256, 0, s>>>(V, n, own, vmax);
+  if (lc) ++*lc;
+}
+void oz_vdigits(cudaStream_t s, const double* V, int64_t n, int pl1, ColOwn own, const double* vmax, int* ev,
+                double* vscale, int8_t* V8, int64_t* lc) {
+  oz_vscale_kernel<<<1, 32, 0, s>>>(vmax, pl1, ev, vscale);
+  oz_vpack_kernel<<<(unsigned)oz_nchunks(n), 256, 0, s>>>(V, n, pl1, own, ev, oz_nv(pl1), V8);
+  if (lc) *lc += 2;
+}
+
+// Single-GPU setup of the int8 path (every column owned).  scratch: (n + 31) / 32 * 32 doubles.
 void oz_setup(cudaStream_t s, const double* T, int64_t ld, int64_t n, const double* W, int pl1,
               int8_t* T8, double* aux, int* escale, const double* V, int8_t* V8, double* vscale,
-              int64_t* lc) {
-  const int NBR = (int)((n + kR - 1) / kR);
-  const int as = pl1 + 1;
-  oz_rowscale_kernel<<<NBR, 256, 0, s>>>(T, ld, n, escale, aux, as);
-  oz_pack_kernel<<<(unsigned)oz_total_tiles(NBR), 256, 0, s>>>(T, ld, n, escale, NBR, T8);
-  const int64_t rows = (int64_t)NBR * kR;
-  const int64_t tot = rows * pl1;
-  oz_aux_w_kernel<<<(unsigned)((tot + 255) / 256 < 2048 ? (tot + 255) / 256 : 2048), 256, 0, s>>>(
-      W, n, n, pl1, rows, aux);
-  // V digits (the row-exponent scratch is free again once oz_pack_kernel has run: same stream)
-  oz_vscale_kernel<<<pl1, 256, 0, s>>>(V, n, escale, vscale);
-  oz_vpack_kernel<<<(unsigned)oz_nchunks(n), 256, 0, s>>>(V, n, pl1, escale, oz_nv(pl1), V8);
-  if (lc) *lc += 5;
+              double* scratch, int64_t* lc) {
+  const ColOwn all;
+  oz_rowmax(s, T, ld, n, all, scratch, lc);
+  oz_rowscale(s, scratch, n, escale, aux, pl1, lc);
+  oz_pack(s, T, ld, n, all, escale, T8, lc);
+  oz_aux_from_w(s, W, n, pl1, aux, lc);
+  // V digits (the row-exponent scratch is free again once oz_pack_kernel has run: same stream); the
+  // column maxima of V land in vscale and are turned into the scales in place
+  oz_vmax(s, V, n, pl1, all, vscale, lc);
+  oz_vdigits(s, V, n, pl1, all, vscale, escale, vscale, V8, lc);
 }
 
 void oz_repack_rows(cudaStream_t s, const int8_t* src, int64_t n, int64_t rows, int8_t* dst, int64_t ld8,

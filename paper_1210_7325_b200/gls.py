@@ -27,6 +27,9 @@ GLS_OOC_SYNC = 0
 GLS_OOC_ASYNC = 1
 GLS_GWFGLS_GEMV = 0
 GLS_GWFGLS_GEMM = 1
+GLS_SHARE_INT8_ONLY = 1
+GLS_DIST_FACTOR, GLS_DIST_UPDATE, GLS_DIST_PARTIALS, GLS_DIST_PACK, GLS_DIST_PACK2 = range(5)
+GLS_DIST_PANEL, GLS_DIST_WPART, GLS_DIST_W, GLS_DIST_ROWMAX, GLS_DIST_VMAX, GLS_DIST_T8, GLS_DIST_V8 = range(7)
 
 
 class OocReport(ctypes.Structure):
@@ -58,6 +61,9 @@ ABI_SYMBOLS = (
     "gls_set_timing", "gls_read_timing", "gls_get_dims", "gls_solve_file", "gls_select_block_size",
     "gls_release_cached_memory", "gls_set_stream_report", "gls_read_stream_report",
     "gls_gwfgls_create", "gls_gwfgls_solve", "gls_gwfgls_launches", "gls_gwfgls_destroy",
+    "gls_create_adopt_int8", "gls_shared_view_ex",
+    "gls_dist_create", "gls_dist_info", "gls_dist_buffer", "gls_dist_step", "gls_dist_finish",
+    "gls_dist_failed_pivot", "gls_dist_launches", "gls_dist_destroy",
 )
 
 
@@ -142,6 +148,26 @@ def load(build_if_missing: bool = True):
     L.gls_gwfgls_launches.restype = i64
     L.gls_gwfgls_destroy.argtypes = [vp]
     L.gls_gwfgls_destroy.restype = None
+    L.gls_create_adopt_int8.argtypes = [i64, i32, i32, ctypes.POINTER(vp)]
+    L.gls_create_adopt_int8.restype = ctypes.c_int
+    L.gls_shared_view_ex.argtypes = [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(i64), ctypes.POINTER(i32)]
+    L.gls_shared_view_ex.restype = ctypes.c_int
+    L.gls_dist_create.argtypes = [i64, i32, i32, i64, i32, i32, dp, dp, dp, ctypes.POINTER(vp)]
+    L.gls_dist_create.restype = ctypes.c_int
+    L.gls_dist_info.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.gls_dist_info.restype = ctypes.c_int
+    L.gls_dist_buffer.argtypes = [vp, i32, i64, ctypes.POINTER(vp), ctypes.POINTER(i64)]
+    L.gls_dist_buffer.restype = ctypes.c_int
+    L.gls_dist_step.argtypes = [vp, i32, i64]
+    L.gls_dist_step.restype = ctypes.c_int
+    L.gls_dist_finish.argtypes = [vp, ctypes.POINTER(vp)]
+    L.gls_dist_finish.restype = ctypes.c_int
+    L.gls_dist_failed_pivot.argtypes = [vp]
+    L.gls_dist_failed_pivot.restype = i64
+    L.gls_dist_launches.argtypes = [vp]
+    L.gls_dist_launches.restype = i64
+    L.gls_dist_destroy.argtypes = [vp]
+    L.gls_dist_destroy.restype = None
     L.gls_release_cached_memory.argtypes = []
     L.gls_release_cached_memory.restype = ctypes.c_int
     _lib = L
@@ -192,6 +218,18 @@ def release_cached_memory() -> None:
         raise GLSError(rc, error_string(rc))
 
 
+def device_bytes(ptr: int, nbytes: int):
+    """A zero-copy torch uint8 CUDA tensor over `nbytes` of library-owned device memory at `ptr`."""
+    import torch
+
+    class _Raw:
+        def __init__(self, p, nb):
+            self.__cuda_array_interface__ = {"shape": (nb,), "typestr": "|u1",
+                                             "data": (p, False), "version": 2, "strides": None}
+
+    return torch.as_tensor(_Raw(ptr, nbytes), device="cuda")
+
+
 def error_string(code: int) -> str:
     return load().gls_error_string(code).decode()
 
@@ -199,12 +237,21 @@ def error_string(code: int) -> str:
 class Context:
     """gls_ctx wrapper.  Context(n, pL, pR, M, X_L, y) runs gls_create on the current device."""
 
-    def __init__(self, n: int, pL: int, pR: int, M=None, X_L=None, y=None, adopt: bool = False):
+    def __init__(self, n: int, pL: int, pR: int, M=None, X_L=None, y=None, adopt: bool = False,
+                 int8_only: bool = False, _handle=None):
         L = load()
         self._lib = L
         self.n, self.pL, self.pR, self.p = n, pL, pR, pL + pR
+        self.int8_only = int8_only
+        self.share_flags = 0
         h = ctypes.c_void_p()
-        if adopt:
+        if _handle is not None:  # a context the library built elsewhere (gls_dist_finish)
+            self._h = _handle
+            self.failed_pivot = -1
+            return
+        if adopt and int8_only:
+            rc = L.gls_create_adopt_int8(n, pL, pR, ctypes.byref(h))
+        elif adopt:
             rc = L.gls_create_adopt(n, pL, pR, ctypes.byref(h))
         else:
             rc = L.gls_create(n, pL, pR, _ptr(M), _ptr(X_L) if pL > 0 else None, _ptr(y), ctypes.byref(h))
@@ -274,23 +321,19 @@ class Context:
     def set_block_cols(self, cols: int):
         self._check(self._lib.gls_set_block_cols(self._h, cols))
 
-    def shared_view(self):
+    def shared_view(self, flags: int | None = None):
+        """gls_shared_view_ex with `flags` (default: self.share_flags; GLS_SHARE_INT8_ONLY lists only the
+        int8 path's state -- what an int8-only receiver needs)."""
         ptrs = (ctypes.c_void_p * 8)()
         nbytes = (ctypes.c_int64 * 8)()
         cnt = ctypes.c_int32()
-        self._check(self._lib.gls_shared_view(self._h, ptrs, nbytes, ctypes.byref(cnt)))
+        f = self.share_flags if flags is None else flags
+        self._check(self._lib.gls_shared_view_ex(self._h, f, ptrs, nbytes, ctypes.byref(cnt)))
         return [(ptrs[k], nbytes[k]) for k in range(cnt.value)]
 
-    def shared_tensors(self):
+    def shared_tensors(self, flags: int | None = None):
         """The shared-state buffers as zero-copy torch uint8 CUDA tensors (for dist.broadcast)."""
-        import torch
-
-        class _Raw:
-            def __init__(self, ptr, nbytes):
-                self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
-                                                 "data": (ptr, False), "version": 2, "strides": None}
-
-        return [torch.as_tensor(_Raw(p, nb), device="cuda") for p, nb in self.shared_view()]
+        return [device_bytes(p, nb) for p, nb in self.shared_view(flags)]
 
     def commit_shared(self):
         self._check(self._lib.gls_commit_shared(self._h))
@@ -367,6 +410,69 @@ class Gwfgls:
 
     def __exit__(self, *exc):
         self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DistFactor:
+    """gls_dist_* (include/gls.h): this rank's share of the distributed create of an M beyond one GPU
+    (NEXT-3).  multi.dist_create runs the protocol; this class only marshals."""
+
+    def __init__(self, n: int, pL: int, pR: int, nb: int, nranks: int, rank: int, M, X_L, y):
+        L = load()
+        self._lib = L
+        self.n, self.pL, self.pR = n, pL, pR
+        self.nranks, self.rank = nranks, rank
+        h = ctypes.c_void_p()
+        rc = L.gls_dist_create(n, pL, pR, nb, nranks, rank, _ptr(M), _ptr(X_L) if pL > 0 else None, _ptr(y),
+                               ctypes.byref(h))
+        if rc != GLS_OK:
+            raise GLSError(rc, error_string(rc))
+        self._h = h
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        L.gls_dist_info(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
+        self.nb, self.nblocks, self.nloc = a.value, b.value, c.value
+
+    def buffer(self, which: int, k: int = 0):
+        """Zero-copy uint8 CUDA tensor over a gls_dist buffer (GLS_DIST_*)."""
+        p, nb = ctypes.c_void_p(), ctypes.c_int64()
+        rc = self._lib.gls_dist_buffer(self._h, which, k, ctypes.byref(p), ctypes.byref(nb))
+        if rc != GLS_OK:
+            raise GLSError(rc, error_string(rc))
+        return device_bytes(p.value, nb.value)
+
+    def step(self, phase: int, k: int = 0) -> int:
+        """gls_dist_step; returns the return code (GLS_ERR_NOT_SPD is reported, not raised)."""
+        rc = self._lib.gls_dist_step(self._h, phase, k)
+        if rc not in (GLS_OK, GLS_ERR_NOT_SPD):
+            raise GLSError(rc, error_string(rc))
+        return rc
+
+    @property
+    def failed_pivot(self) -> int:
+        return int(self._lib.gls_dist_failed_pivot(self._h))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self._lib.gls_dist_launches(self._h))
+
+    def finish(self) -> Context:
+        h = ctypes.c_void_p()
+        rc = self._lib.gls_dist_finish(self._h, ctypes.byref(h))
+        if rc != GLS_OK:
+            raise GLSError(rc, error_string(rc))
+        ctx = Context(self.n, self.pL, self.pR, int8_only=True, _handle=h)
+        ctx.share_flags = GLS_SHARE_INT8_ONLY
+        return ctx
+
+    def close(self):
+        if self._h and self._h.value:
+            self._lib.gls_dist_destroy(self._h)
+        self._h = ctypes.c_void_p()
 
     def __del__(self):
         try:

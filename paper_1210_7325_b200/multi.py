@@ -34,16 +34,20 @@ def weak_range(m_per_rank: int, rank: int) -> tuple[int, int]:
     return rank * m_per_rank, (rank + 1) * m_per_rank
 
 
-def replicate_shared(ctx, dist, src: int = 0, group=None) -> int:
+def replicate_shared(ctx, dist, src: int = 0, group=None, int8_only: bool = False) -> int:
     """Broadcast the shared state of `ctx` from rank `src` to every rank of `group`, then commit it
     on the receiving ranks.  `ctx` is a Context created with gls_create on `src` and with
     adopt=True elsewhere.  `src` is a GLOBAL rank (torch.distributed's convention for broadcast).
     Over NCCL the library's device buffers are broadcast in place (zero-copy tensors); over gloo
     (host-only backend, used by the CPU-side tests) they are staged through host memory.
+    int8_only: broadcast only the int8 path's state (receivers created with adopt=True, int8_only=True;
+    the FP64 path's packed T -- n^2 * 4 bytes -- is neither sent nor allocated on them).
     Returns the number of bytes broadcast."""
     import torch
+
+    from .gls import GLS_SHARE_INT8_ONLY
     rank = dist.get_rank()  # global rank, comparable with src
-    tensors = ctx.shared_tensors()
+    tensors = ctx.shared_tensors(GLS_SHARE_INT8_ONLY if int8_only else None)
     staged = bool(tensors) and tensors[0].is_cuda and dist.get_backend(group) == "gloo"
     nbytes = 0
     for t in tensors:
@@ -93,3 +97,92 @@ def shared_state_digest(ctx) -> list[int]:
         out.append(int(w.sum().item()))
         out.append(int((w * pos).sum().item()))
     return out
+
+
+class Comm:
+    """The collectives of the distributed create over torch.distributed: NCCL moves the library's device
+    buffers in place; gloo (host-only, used by the CPU-side and one-GPU tests) stages them through host
+    memory.  world 1 (no process group): every collective is the identity."""
+
+    def __init__(self, dist=None, group=None):
+        self.dist, self.group = dist, group
+        live = dist is not None and dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if live else 1
+        self.rank = dist.get_rank(group) if live else 0
+        self.host = live and self.world > 1 and dist.get_backend(group) == "gloo"
+
+    def _src(self, r):
+        return self.dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def _run(self, t, fn):
+        if self.world == 1:
+            return
+        if self.host and t.is_cuda:
+            h = t.cpu()
+            fn(h)
+            t.copy_(h)
+        else:
+            fn(t)
+
+    def bcast(self, t, src: int):
+        self._run(t, lambda x: self.dist.broadcast(x, src=self._src(src), group=self.group))
+
+    def allreduce(self, t, op: str):
+        o = {"max": self.dist.ReduceOp.MAX, "sum": self.dist.ReduceOp.SUM}[op] if self.world > 1 else None
+        self._run(t, lambda x: self.dist.all_reduce(x, op=o, group=self.group))
+
+    def allgather(self, t):
+        if self.world == 1:
+            return [t]
+        src = t.cpu() if self.host and t.is_cuda else t
+        out = [src.new_empty(src.shape) for _ in range(self.world)]
+        self.dist.all_gather(out, src, group=self.group)
+        return [x.to(t.device) for x in out]
+
+
+def dist_create(n: int, pL: int, pR: int, M, X_L, y, dist=None, nb: int = 1024, group=None, factor=None):
+    """The distributed create of NEXT-3 (include/gls.h gls_dist_*): this rank holds the
+    column blocks j of width nb with j % G == rank; one panel broadcast per block column; then the int8
+    state assembled by small all-gathers / all-reduces.  Returns this rank's int8-only Context (its shared
+    state bit-identical on every rank).  M, X_L, y: full arrays (host or device) -- each rank copies its
+    own column blocks of M.  Raises GLSError(GLS_ERR_NOT_SPD) on every rank when a pivot fails (the pivot
+    index in the exception's .pivot).  `factor` (tests): a stand-in for gls.DistFactor with the same
+    methods."""
+    import torch
+
+    from . import gls
+    comm = Comm(dist, group)
+    d = factor if factor is not None else gls.DistFactor(n, pL, pR, nb, comm.world, comm.rank, M, X_L, y)
+    dev = d.buffer(gls.GLS_DIST_W).device
+    status = torch.zeros(1, dtype=torch.int64, device=dev)
+    for k in range(d.nblocks):
+        owner = k % comm.world
+        if comm.rank == owner:
+            rc = d.step(gls.GLS_DIST_FACTOR, k)
+            status[0] = d.failed_pivot if rc == gls.GLS_ERR_NOT_SPD else -1
+        comm.bcast(status, owner)
+        piv = int(status.item())
+        if piv >= 0:
+            d.close()
+            err = gls.GLSError(gls.GLS_ERR_NOT_SPD, "M is not SPD: Cholesky pivot %d (distributed create)" % piv)
+            err.pivot = piv
+            raise err
+        comm.bcast(d.buffer(gls.GLS_DIST_PANEL, k), owner)
+        d.step(gls.GLS_DIST_UPDATE, k)
+    d.step(gls.GLS_DIST_PARTIALS)
+    parts = comm.allgather(d.buffer(gls.GLS_DIST_WPART).view(torch.float64))
+    W = parts[0].clone()
+    for p in parts[1:]:  # rank order on every rank: the same bits everywhere
+        W += p
+    d.buffer(gls.GLS_DIST_W).view(torch.float64).copy_(W)
+    comm.allreduce(d.buffer(gls.GLS_DIST_ROWMAX).view(torch.float64), "max")
+    d.step(gls.GLS_DIST_PACK)
+    comm.allreduce(d.buffer(gls.GLS_DIST_VMAX).view(torch.float64), "max")
+    d.step(gls.GLS_DIST_PACK2)
+    comm.allreduce(d.buffer(gls.GLS_DIST_T8), "sum")  # uint8 bytes, one nonzero contributor each
+    comm.allreduce(d.buffer(gls.GLS_DIST_V8), "sum")
+    if dev.type == "cuda":
+        torch.cuda.synchronize()
+    ctx = d.finish()
+    d.close()
+    return ctx

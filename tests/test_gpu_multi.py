@@ -36,13 +36,18 @@ def _rank_main(rank, world, init_file, out_dir, mode):
     dist.init_process_group("gloo", init_method="file://" + init_file, rank=rank, world_size=world)
     P = gen.make_problem(N, PL, PR, seed=SEED)
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    if mode == "bcast":
-        ctx = pkg.Context(N, PL, PR, d(P.M), d(P.XL), d(P.y)) if rank == 0 else pkg.Context(N, PL, PR, adopt=True)
+    if mode in ("bcast", "bcast8"):
+        i8 = mode == "bcast8"  # receivers hold only the int8 path's state; the root sends only that
+        ctx = (pkg.Context(N, PL, PR, d(P.M), d(P.XL), d(P.y)) if rank == 0
+               else pkg.Context(N, PL, PR, adopt=True, int8_only=i8))
         # the library's shared buffers broadcast from rank 0 (gloo: staged through host memory)
-        multi.replicate_shared(ctx, dist, src=0)
+        nbytes = multi.replicate_shared(ctx, dist, src=0, int8_only=i8)
+        full = sum(nb for _, nb in ctx.shared_view(0)) if rank == 0 else 0
+        np.save(os.path.join(out_dir, "nbytes%d.npy" % rank), np.array([nbytes, full]))
     else:
         ctx = pkg.Context(N, PL, PR, d(P.M), d(P.XL), d(P.y))
-    np.save(os.path.join(out_dir, "digest%d.npy" % rank), np.array(multi.shared_state_digest(ctx)))
+    np.save(os.path.join(out_dir, "digest%d.npy" % rank),
+            np.array(multi.shared_state_digest(ctx) if mode != "bcast8" else [0]))
     lo, hi = multi.snp_range(M_TOTAL, world, rank)
     X = torch.empty((hi - lo) * PR, N, dtype=torch.float64, device="cuda")
     pkg.gen_xr_device(SEED, N, lo * PR, (hi - lo) * PR, X)
@@ -56,7 +61,7 @@ def _rank_main(rank, world, init_file, out_dir, mode):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["bcast", "redundant"])
+@pytest.mark.parametrize("mode", ["bcast", "bcast8", "redundant"])
 def test_replicate_then_shard_two_processes(tmp_path, mode):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -72,6 +77,9 @@ def test_replicate_then_shard_two_processes(tmp_path, mode):
     for r in (0, 1):
         assert tuple(np.load(tmp_path / ("paths%d.npy" % r))) == (1, 0)  # int8 path on both ranks
     np.testing.assert_array_equal(np.load(tmp_path / "digest0.npy"), np.load(tmp_path / "digest1.npy"))
+    if mode == "bcast8":  # only T8, aux, V8, vscale and G travel: no packed FP64 T
+        sent, full = np.load(tmp_path / "nbytes0.npy")
+        assert sent == np.load(tmp_path / "nbytes1.npy")[0] and sent < 0.6 * full, (sent, full)
     # single-process reference over all m problems
     P = gen.make_problem(N, PL, PR, seed=SEED)
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()

@@ -26,7 +26,7 @@ class FakeCtx:
             self.bufs = [torch.zeros(s, dtype=torch.uint8) for s in sizes]
         self.committed = root
 
-    def shared_tensors(self):
+    def shared_tensors(self, flags=None):
         return self.bufs
 
     def commit_shared(self):
