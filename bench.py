@@ -82,8 +82,10 @@ def parse():
     ap.add_argument("--no-sub", action="store_true", help="skip the sub-records (FP64 path, OOC, weak scaling)")
     ap.add_argument("--scaling", default="auto", choices=["auto", "strong", "weak"],
                     help="auto: strong (the config's m split over the GPUs) when N > 1")
-    ap.add_argument("--replicate", default="redundant", choices=["redundant", "bcast"],
-                    help="N > 1: every rank factors M (paper, PAPER.md:812-814) or rank 0 + NCCL broadcast")
+    ap.add_argument("--replicate", default="redundant", choices=["redundant", "bcast", "dist"],
+                    help="N > 1: every rank factors M (paper, PAPER.md:812-814), rank 0 + NCCL broadcast, or the "
+                         "factorisation split over the ranks (NEXT-3, multi.dist_create)")
+    ap.add_argument("--dist-nb", type=int, default=1024, help="column-block width of --replicate dist")
     ap.add_argument("--codes", action="store_true",
                     help="config 4: stream X_R as int8 genotype codes (gls_solve_block_i8) instead of FP64")
     ap.add_argument("--seed", type=int, default=gen.DEFAULT_SEED)
@@ -236,6 +238,11 @@ class Job:
 
     def make_ctx(self, Mx, XLx, yx):
         cfg, pkg = self.cfg, self.pkg
+        if self.args.replicate == "dist":
+            # NEXT-3: the factorisation itself split over the ranks (column blocks of M and T, panel
+            # broadcasts); every rank ends with the same int8-only state
+            return self.multi.dist_create(cfg.n, cfg.pL, cfg.pR, Mx, XLx, yx, dist=self.dist if self.world > 1 else None,
+                                          nb=self.args.dist_nb)
         if self.world > 1 and self.args.replicate == "bcast":
             ctx = (pkg.Context(cfg.n, cfg.pL, cfg.pR, Mx, XLx, yx) if self.rank == 0
                    else pkg.Context(cfg.n, cfg.pL, cfg.pR, adopt=True))
@@ -402,7 +409,7 @@ def main():
 
     # ---- sub-records (fixed small step counts, so the default run stays within minutes)
     subs = {}
-    if not args.no_sub and r["paths"][0] > 0:
+    if not args.no_sub and r["paths"][0] > 0 and args.replicate != "dist":
         # the FP64 tensor-pipe path on the same workload: the metric's "FP64 tensor-pipe % of peak"
         r64 = job.run(2, 1, path=pkg.GLS_PATH_FP64)
         rl64 = fp64_roofline(r64, n, int(m_max), pR, None)
