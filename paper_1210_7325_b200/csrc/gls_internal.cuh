@@ -148,8 +148,11 @@ inline int oz_nv(int pl1) { return ((8 * pl1 + 31) / 32) * 32; }
 struct ColOwn {
   int64_t nb = (int64_t)1 << 40;
   int nranks = 1, rank = 0;
-  __host__ __device__ bool owned(int64_t j) const { return (j / nb) % nranks == rank; }
-  __host__ __device__ int64_t local(int64_t j) const { return ((j / nb) / nranks) * nb + j % nb; }
+  // (nranks == 1: no 64-bit divisions -- the setup kernels of the single-GPU create run at full speed)
+  __host__ __device__ bool owned(int64_t j) const { return nranks == 1 || (j / nb) % nranks == rank; }
+  __host__ __device__ int64_t local(int64_t j) const {
+    return nranks == 1 ? j : ((j / nb) / nranks) * nb + j % nb;
+  }
 };
 // Setup of the int8 path from T = L^{-1} (dense, column-major, ld) and W = [X~_L | y~], V = M^{-1}[X_L|y]:
 // row scales + aux, digit tiles T8, V digits.  scratch: (n + 31) / 32 * 32 doubles.
