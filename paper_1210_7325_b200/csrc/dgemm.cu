@@ -8,6 +8,12 @@
 // zero-fill for ragged edges, any leading dimension / transpose.  Shared tiles are [row][k] with a
 // 20-double row stride: the m8n8k4 fragment loads (lane (m, k) = (l/4, l%4)) are conflict-free.
 // Triangular operands skip all-zero K ranges through GemmFlags.
+#include <cuda.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+
 #include "gls_internal.cuh"
 
 namespace gls {
@@ -188,6 +194,297 @@ __global__ void dgemm_splitk_reduce(GemmParams p) {
   }
 }
 
+// ---------------------------------------------------------------- TMA-fed DMMA GEMM (op(A) = A)
+// The large products of gls_create (L21 = A21 T11^T, the SYRK, Y = L21 T11, T21 = -T22 Y) all read A
+// untransposed.  A persistent CTA per SM walks its output tiles (BM x BN = 128 x 64); warp 8 is a TMA
+// producer (one lane) filling an 8-stage ring of [BK = 16] x (A: 128 rows, B: 64 columns) tiles under
+// full / empty mbarriers, warps 0-7 (4 x 2, 32 x 32 each) issue mma.sync.m8n8k4.f64 (DMMA.8x8x4) from
+// LDS.128 fragment loads: every 16-byte load feeds two DMMA tiles.
+//   A (M-major in memory, m contiguous): smem [k][128 m], no swizzle; a lane's LDS.128 at (k, m pair
+//     2 l4, 2 l4 + 1) gives the A fragments of two row tiles -- tile t covers rows 16 (t >> 1) + 2 l4 +
+//     (t & 1) of the warp's 32 (a row permutation the epilogue undoes); 4 k rows 1 KB apart: 4 wavefronts
+//     per 512 bytes, conflict-free.
+//   B^T (BT, op(B) = B^T with B N x K, n contiguous): smem [k][64 n], the same pairing on the columns.
+//   B (K-major, op(B) = B with B K x N, k contiguous): smem [64 n][16 k] with the 128-byte swizzle; an
+//     LDS.128 gives two consecutive k of one column (chunk (2 kk + P) ^ (n & 7)); the k-steps use the
+//     matching k permutation (DMMA k index kk <-> k = 4 kk + 2 P + e) on both operands.
+// Ragged M / N / K edges come zero-filled from TMA.  Triangular K ranges skip whole 16-wide stages; the
+// skipped and the partially covered stages' extra elements are zeros of the triangular operand (every
+// call site's operand holds zeros there), so no element masking is needed.
+namespace tg {
+constexpr int BM = 128, BN = 64, BK = 16, CW = 8, THREADS = (CW + 1) * 32, STAGES = 8;
+constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+
+struct Params {
+  int64_t M, N, K;
+  double* C;
+  int64_t ldc;
+  double alpha, beta;
+  int flags;
+  int64_t tm, ntiles;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W_%=;\n}\n" ::"r"(
+          su32(b)),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(su32(dst)),
+      "l"(m), "r"(c0), "r"(c1), "r"(su32(b))
+      : "memory");
+}
+__device__ __forceinline__ void lds128(uint32_t a, double& x, double& y) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(a));
+}
+
+// K range of an output tile (the old kernel's triangular rules, at stage granularity)
+__device__ __forceinline__ void krange(const Params& p, int64_t r0, int64_t c0, int64_t& kb, int& nk) {
+  int64_t b = 0, e = p.K;
+  if (p.flags & GEMM_KMIN_COL) b = c0;
+  if (p.flags & GEMM_KMAX_ROW) e = min(e, r0 + BM);
+  if (p.flags & GEMM_KMAX_COL) e = min(e, c0 + BN);
+  b = (b / BK) * BK;
+  kb = b;
+  nk = e > b ? (int)((e - b + BK - 1) / BK) : 0;
+}
+
+template <bool BT>
+__global__ void __launch_bounds__(THREADS, 1) dgemm_tma_kernel(const __grid_constant__ CUtensorMap amap,
+                                                              const __grid_constant__ CUtensorMap bmap, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = (uint64_t*)(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == CW) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&amap) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&bmap) : "memory");
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        const int64_t r0 = (tile % p.tm) * BM, c0 = (tile / p.tm) * BN;
+        if ((p.flags & GEMM_LOWER_C) && c0 >= r0 + BM) continue;
+        int64_t kb;
+        int nk;
+        krange(p, r0, c0, kb, nk);
+        for (int kt = 0; kt < nk; ++kt) {
+          const int k0 = (int)(kb + (int64_t)kt * BK);
+          bar_wait(&empty[st], ph ^ 1);
+          bar_expect(&full[st], STAGE_BYTES);
+          tma2d(sA + st * A_BYTES, &amap, (int)r0, k0, &full[st]);
+          if (BT)
+            tma2d(sB + st * B_BYTES, &bmap, (int)c0, k0, &full[st]);
+          else
+            tma2d(sB + st * B_BYTES, &bmap, k0, (int)c0, &full[st]);
+          if (++st == STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+  // -------------------------------------------------------------- DMMA consumers
+  const int wm = warp & 3, wn = warp >> 2;
+  const int l4 = lane >> 2, kk = lane & 3;
+  const uint32_t a_base = su32(sA), b_base = su32(sB);
+  const uint32_t a_lane = (uint32_t)((wm * 32 + 2 * l4) * 8);
+  int st = 0;
+  uint32_t ph = 0;
+  for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    const int64_t r0 = (tile % p.tm) * BM, c0 = (tile / p.tm) * BN;
+    if ((p.flags & GEMM_LOWER_C) && c0 >= r0 + BM) continue;
+    int64_t kb;
+    int nk;
+    krange(p, r0, c0, kb, nk);
+    double acc[4][4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) acc[t][s][0] = acc[t][s][1] = 0.0;
+    for (int kt = 0; kt < nk; ++kt) {
+      bar_wait(&full[st], ph);
+      const uint32_t as = a_base + st * A_BYTES, bs = b_base + st * B_BYTES;
+      if (BT) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const int k = ks * 4 + kk;
+          double a[4], b[4];
+          lds128(as + k * (BM * 8) + a_lane, a[0], a[1]);
+          lds128(as + k * (BM * 8) + a_lane + 128, a[2], a[3]);
+          lds128(bs + k * (BN * 8) + (wn * 32 + 2 * l4) * 8, b[0], b[1]);
+          lds128(bs + k * (BN * 8) + (wn * 32 + 2 * l4) * 8 + 128, b[2], b[3]);
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) dmma(acc[t][s], a[t], b[s]);
+        }
+      } else {
+#pragma unroll
+        for (int P = 0; P < 2; ++P) {
+          double b[4][2];
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const int n = wn * 32 + 8 * s + l4;
+            lds128(bs + n * 128 + ((((2 * kk + P) ^ (n & 7)) & 7) << 4), b[s][0], b[s][1]);
+          }
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int k = 4 * kk + 2 * P + e;
+            double a[4];
+            lds128(as + k * (BM * 8) + a_lane, a[0], a[1]);
+            lds128(as + k * (BM * 8) + a_lane + 128, a[2], a[3]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+              for (int s = 0; s < 4; ++s) dmma(acc[t][s], a[t], b[s][e]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) bar_arrive(&empty[st]);
+      if (++st == STAGES) {
+        st = 0;
+        ph ^= 1;
+      }
+    }
+    // epilogue: lane holds C[m_d = l4][n_d = 2 kk + e] of each DMMA tile (t, s)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int64_t gm = r0 + wm * 32 + 16 * (t >> 1) + 2 * l4 + (t & 1);
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t gn = BT ? c0 + wn * 32 + 16 * (s >> 1) + 2 * (2 * kk + e) + (s & 1)
+                                : c0 + wn * 32 + 8 * s + 2 * kk + e;
+          if (gm < p.M && gn < p.N) {
+            double* cp = p.C + gm + gn * p.ldc;
+            double v = p.alpha * acc[t][s][e];
+            if (p.beta != 0.0) v += p.beta * *cp;
+            *cp = v;
+          }
+        }
+    }
+  }
+}
+}  // namespace tg
+
+typedef CUresult (*PFN_encodeTiled_g)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled_g encode_fn() {
+  static PFN_encodeTiled_g fn = nullptr;
+  if (!fn) {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult r;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r) == cudaSuccess &&
+        r == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled_g)q;
+  }
+  return fn;
+}
+
+// The TMA GEMM when it applies (op(A) = A; 16-byte aligned bases, even leading dimensions): true if
+// launched.  GLS_DGEMM_TMA=0 turns it off (A/B diagnostics).
+bool try_tma(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda, char opA,
+             const double* B, int64_t ldb, char opB, double beta, double* C, int64_t ldc, int flags, int max_ctas) {
+  static const int on = getenv("GLS_DGEMM_TMA") ? atoi(getenv("GLS_DGEMM_TMA")) : 1;
+  if (!on || opA != 'N' || K <= 0) return false;
+  if ((((uintptr_t)A | (uintptr_t)B) & 15) || (lda & 1) || (ldb & 1)) return false;
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return false;
+  PFN_encodeTiled_g enc = encode_fn();
+  if (!enc) return false;
+  const bool bt = opB == 'T';
+  CUtensorMap am, bm;
+  const cuuint32_t estr[2] = {1, 1};
+  {
+    cuuint64_t dim[2] = {(cuuint64_t)M, (cuuint64_t)K};
+    cuuint64_t str[1] = {(cuuint64_t)lda * 8};
+    cuuint32_t box[2] = {(cuuint32_t)tg::BM, (cuuint32_t)tg::BK};
+    if (enc(&am, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)A, dim, str, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return false;
+  }
+  {
+    cuuint64_t dim[2], str[1] = {(cuuint64_t)ldb * 8};
+    cuuint32_t box[2];
+    CUtensorMapSwizzle sw;
+    if (bt) {  // B stored N x K (n contiguous)
+      dim[0] = (cuuint64_t)N;
+      dim[1] = (cuuint64_t)K;
+      box[0] = tg::BN;
+      box[1] = tg::BK;
+      sw = CU_TENSOR_MAP_SWIZZLE_NONE;
+    } else {   // B stored K x N (k contiguous)
+      dim[0] = (cuuint64_t)K;
+      dim[1] = (cuuint64_t)N;
+      box[0] = tg::BK;
+      box[1] = tg::BN;
+      sw = CU_TENSOR_MAP_SWIZZLE_128B;
+    }
+    if (enc(&bm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)B, dim, str, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  tg::Params p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.C = C;
+  p.ldc = ldc;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.flags = flags;
+  p.tm = (M + tg::BM - 1) / tg::BM;
+  p.ntiles = p.tm * ((N + tg::BN - 1) / tg::BN);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = max_ctas > 0 ? std::max(1, max_ctas / 2) : sms;  // one CTA per SM (max_ctas counts two per SM)
+  if (grid > p.ntiles) grid = p.ntiles;
+  if (bt) {
+    if (first_use_on_device((const void*)tg::dgemm_tma_kernel<true>))
+      cudaFuncSetAttribute(tg::dgemm_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tg::SMEM);
+    tg::dgemm_tma_kernel<true><<<(unsigned)grid, tg::THREADS, tg::SMEM, s>>>(am, bm, p);
+  } else {
+    if (first_use_on_device((const void*)tg::dgemm_tma_kernel<false>))
+      cudaFuncSetAttribute(tg::dgemm_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tg::SMEM);
+    tg::dgemm_tma_kernel<false><<<(unsigned)grid, tg::THREADS, tg::SMEM, s>>>(am, bm, p);
+  }
+  return true;
+}
+
 template <bool TA, bool TB>
 void launch(cudaStream_t s, dim3 grid, const GemmParams& p) {
   if (first_use_on_device((const void*)dgemm_kernel<TA, TB>))
@@ -327,6 +624,10 @@ void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const 
       p.ws = ws;
       grid.z = sp;
     }
+  }
+  if (p.nsplit == 1 && try_tma(s, M, N, K, alpha, A, lda, opA, B, ldb, opB, beta, C, ldc, flags, max_ctas)) {
+    if (launch_counter) ++*launch_counter;
+    return;
   }
   if (max_ctas > 0 && p.nsplit == 1 && tiles > max_ctas) grid = dim3((unsigned)max_ctas);
   const bool ta = (opA == 'T'), tb = (opB == 'T');
