@@ -208,7 +208,7 @@ __global__ void dgemm_splitk_reduce(GemmParams p) {
 //   B (K-major, op(B) = B with B K x N, k contiguous): smem [64 n][16 k] with the 128-byte swizzle; an
 //     LDS.128 gives two consecutive k of one column (chunk (2 kk + P) ^ (n & 7)); the k-steps use the
 //     matching k permutation (DMMA k index kk <-> k = 4 kk + 2 P + e) on both operands.
-// Ragged M / N / K edges come zero-filled from TMA.  Triangular K ranges skip whole 16-wide stages; the
+// Ragged M / N edges only touch outputs that are not stored; the K tail is zeroed in registers.  Triangular K ranges skip whole 16-wide stages; the
 // skipped and the partially covered stages' extra elements are zeros of the triangular operand (every
 // call site's operand holds zeros there), so no element masking is needed.
 namespace tg {
@@ -262,6 +262,52 @@ __device__ __forceinline__ void krange(const Params& p, int64_t r0, int64_t c0, 
   b = (b / BK) * BK;
   kb = b;
   nk = e > b ? (int)((e - b + BK - 1) / BK) : 0;
+}
+
+// The fragments of one half-stage (8 K values): a[j][t] / b[j][s] for the two DMMA k-steps j.
+struct Frag {
+  double a[2][4], b[2][4];
+};
+// BT (B N-major): half h holds k-steps 2h, 2h+1 (k = 4 (2h + j) + kk).  !BT (B K-major): half P holds
+// k = 4 kk + 2 P + j.  Fragments of k >= kvalid are zeroed (K tail).
+template <bool BT>
+__device__ __forceinline__ void load_half(Frag& f, uint32_t as, uint32_t bs, uint32_t a_lane, int wn, int l4, int kk,
+                                          int h, int kvalid) {
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int k = BT ? 4 * (2 * h + j) + kk : 4 * kk + 2 * h + j;
+    lds128(as + k * (BM * 8) + a_lane, f.a[j][0], f.a[j][1]);
+    lds128(as + k * (BM * 8) + a_lane + 128, f.a[j][2], f.a[j][3]);
+    if (BT) {
+      lds128(bs + k * (BN * 8) + (wn * 32 + 2 * l4) * 8, f.b[j][0], f.b[j][1]);
+      lds128(bs + k * (BN * 8) + (wn * 32 + 2 * l4) * 8 + 128, f.b[j][2], f.b[j][3]);
+    }
+  }
+  if (!BT) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int n = wn * 32 + 8 * s + l4;
+      lds128(bs + n * 128 + ((((2 * kk + h) ^ (n & 7)) & 7) << 4), f.b[0][s], f.b[1][s]);
+    }
+  }
+  if (kvalid < BK) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int k = BT ? 4 * (2 * h + j) + kk : 4 * kk + 2 * h + j;
+      if (k >= kvalid) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) f.a[j][q] = f.b[j][q] = 0.0;
+      }
+    }
+  }
+}
+__device__ __forceinline__ void mma_half(double (&acc)[4][4][2], const Frag& f) {
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) dmma(acc[t][s], f.a[j][t], f.b[j][s]);
 }
 
 template <bool BT>
@@ -331,52 +377,39 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_tma_kernel(const __grid_cons
     for (int t = 0; t < 4; ++t)
 #pragma unroll
       for (int s = 0; s < 4; ++s) acc[t][s][0] = acc[t][s][1] = 0.0;
-    for (int kt = 0; kt < nk; ++kt) {
-      bar_wait(&full[st], ph);
-      const uint32_t as = a_base + st * A_BYTES, bs = b_base + st * B_BYTES;
-      if (BT) {
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const int k = ks * 4 + kk;
-          double a[4], b[4];
-          lds128(as + k * (BM * 8) + a_lane, a[0], a[1]);
-          lds128(as + k * (BM * 8) + a_lane + 128, a[2], a[3]);
-          lds128(bs + k * (BN * 8) + (wn * 32 + 2 * l4) * 8, b[0], b[1]);
-          lds128(bs + k * (BN * 8) + (wn * 32 + 2 * l4) * 8 + 128, b[2], b[3]);
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-#pragma unroll
-            for (int s = 0; s < 4; ++s) dmma(acc[t][s], a[t], b[s]);
-        }
-      } else {
-#pragma unroll
-        for (int P = 0; P < 2; ++P) {
-          double b[4][2];
-#pragma unroll
-          for (int s = 0; s < 4; ++s) {
-            const int n = wn * 32 + 8 * s + l4;
-            lds128(bs + n * 128 + ((((2 * kk + P) ^ (n & 7)) & 7) << 4), b[s][0], b[s][1]);
-          }
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int k = 4 * kk + 2 * P + e;
-            double a[4];
-            lds128(as + k * (BM * 8) + a_lane, a[0], a[1]);
-            lds128(as + k * (BM * 8) + a_lane + 128, a[2], a[3]);
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-#pragma unroll
-              for (int s = 0; s < 4; ++s) dmma(acc[t][s], a[t], b[s][e]);
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) bar_arrive(&empty[st]);
-      if (++st == STAGES) {
-        st = 0;
-        ph ^= 1;
-      }
+    // Software pipeline over half-stages (8 LDS.128 -> 32 DMMAs each): the fragments of half-stage h+1
+    // (the next stage's first half after waiting for it) are loaded while half-stage h's DMMAs issue.
+    Frag F0, F1;
+    int cur = st;
+    uint32_t cph = ph;
+    if (nk > 0) {
+      bar_wait(&full[cur], cph);
+      load_half<BT>(F0, a_base + cur * A_BYTES, b_base + cur * B_BYTES, a_lane, wn, l4, kk, 0,
+                    (int)min((int64_t)BK, p.K - kb));
     }
+    for (int kt = 0; kt < nk; ++kt) {
+      // the last stage of a K not divisible by 16: the rows of the box beyond K are not zero in shared
+      // memory (measured: a box cut along its outer dimension leaves them stale), so load_half zeroes
+      // the fragments of k >= K in registers (a select, not a product: stale bits may be NaN)
+      const int kvalid = (int)min((int64_t)BK, p.K - (kb + (int64_t)kt * BK));
+      load_half<BT>(F1, a_base + cur * A_BYTES, b_base + cur * B_BYTES, a_lane, wn, l4, kk, 1, kvalid);
+      mma_half(acc, F0);
+      const int done = cur;
+      if (++cur == STAGES) {
+        cur = 0;
+        cph ^= 1;
+      }
+      if (kt + 1 < nk) {
+        bar_wait(&full[cur], cph);
+        load_half<BT>(F0, a_base + cur * A_BYTES, b_base + cur * B_BYTES, a_lane, wn, l4, kk, 0,
+                      (int)min((int64_t)BK, p.K - (kb + (int64_t)(kt + 1) * BK)));
+      }
+      mma_half(acc, F1);
+      __syncwarp();
+      if (lane == 0) bar_arrive(&empty[done]);
+    }
+    st = cur;
+    ph = cph;
     // epilogue: lane holds C[m_d = l4][n_d = 2 kk + e] of each DMMA tile (t, s)
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
