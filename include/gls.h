@@ -203,7 +203,12 @@ int gls_release_cached_memory(void);
  *                        points (Alg. 8 lines 8 and 16; Alg. 7 lines 7 and 14), the first block's load,
  *                        blocks and bytes moved.
  * Results are bitwise identical between the two modes and to gls_solve_block on the same values (same
- * kernels, block-partition independent).  Synchronous: returns when every b is on the file.
+ * kernels, block-partition independent) whenever every block takes the same arithmetic path -- always for
+ * genotype codes (elem_bytes 1) and for integer-valued FP64 X_R.  Exception (reading A16): with
+ * GLS_PATH_AUTO the int8-or-FP64 choice is made per device conversion chunk, so for FP64 X_R that mixes
+ * integer and non-integer (dosage) columns, a problem's record can differ at rounding level (both paths
+ * are within the parity tolerance) depending on which chunk it falls in; GLS_PATH_FP64 restores
+ * partition-independent bits for such data.  Synchronous: returns when every b is on the file.
  * Errors: GLS_ERR_ARG (bad argument, unreadable/short X_R file, failed write), GLS_ERR_DIM, GLS_ERR_OOM
  * (pinned workspaces), and any error of the solve calls. */
 enum { GLS_OOC_SYNC = 0, GLS_OOC_ASYNC = 1 };
