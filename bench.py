@@ -586,13 +586,13 @@ def config3_subrecord(args, world, rank, pkg, multi, dist, torch):
 
 
 def file_ooc_subrecord(args, pkg, torch):
-    """NEXT-1 (§4): 2e5 config-4 SNPs as int8 genotype codes in a file on the box's local disk,
+    """NEXT-1 (§4): 1e6 config-4 SNPs as int8 genotype codes (10 GB) in a file on the box's local disk,
     solved with gls_solve_file in Alg. 7 (synchronous) and Alg. 8 (double-buffered) mode, each from a
     cold page cache; the raw O_DIRECT read rate of the same file is the I/O roofline."""
     import mmap
     import tempfile
     cfg = gen.CONFIGS[4]
-    n, pL, pR, m = cfg.n, cfg.pL, cfg.pR, 200_000
+    n, pL, pR, m = cfg.n, cfg.pL, cfg.pR, 1_000_000
     P = gen.config_problem(cfg, seed=args.seed)
     d = tempfile.mkdtemp(prefix="gls_ooc_", dir=os.environ.get("GLS_OOC_DIR", "/tmp"))
     xr, bf = os.path.join(d, "xr_i8.bin"), os.path.join(d, "b.bin")
