@@ -660,18 +660,25 @@ def ooc_subrecord(args, cfg, world, rank, pkg, multi, dist, torch):
     yd = torch.from_numpy(P.y).cuda()
     blk = ooc.host_block_groups(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count, pR)
     g0 = multi.weak_range(m, rank)[0]
+    # pinned pool per rank: 2 blocks (FP64 + codes: ~13.6 GB at n = 1e4), or 1 when the host is short
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 1 << 40
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    npool = 2 if 2 * blk * pR * n * 9 <= 0.4 * avail / local_world else 1
     tmp = torch.empty((blk * pR, n), dtype=torch.float64, device="cuda")
-    pool64 = torch.empty((2, blk * pR, n), dtype=torch.float64, pin_memory=True)
-    pool8 = torch.empty((2, blk * pR, n), dtype=torch.int8, pin_memory=True)
-    for k in range(2):
+    pool64 = torch.empty((npool, blk * pR, n), dtype=torch.float64, pin_memory=True)
+    pool8 = torch.empty((npool, blk * pR, n), dtype=torch.int8, pin_memory=True)
+    for k in range(npool):
         pkg.gen_xr_device(args.seed, n, (g0 + k * blk) * pR, blk * pR, tmp)
         pool64[k].copy_(tmp)
         pool8[k].copy_(tmp.to(torch.int8))
     del tmp
     b = torch.empty((m, p), dtype=torch.float64, pin_memory=True)
     st = torch.empty(m, dtype=torch.int32, pin_memory=True)
-    out = {"m_per_rank": m, "block_snps": blk, "pool_blocks": 2,
-           "snp_to_block": "block j -> pool block j mod 2", "steps": 1, "warmup": 1}
+    out = {"m_per_rank": m, "block_snps": blk, "pool_blocks": npool,
+           "snp_to_block": "block j -> pool block j mod %d" % npool, "steps": 1, "warmup": 1}
     peak8, _, _ = int8_peak()
     for name, pool, codes, esz in (("codes", pool8, True, 1), ("fp64", pool64, False, 8)):
         res = None
