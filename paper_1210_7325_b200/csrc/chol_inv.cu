@@ -307,6 +307,355 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_inv_node128(int n, double* 
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Blocked leaf of up to 128 rows on the FP64 tensor pipe (round 2).  The column sweeps above are
+// bound by shared-memory traffic (every pair step re-reads the whole trailing triangle and T block:
+// ~1.7 us per pair, 97 us for a 128-row node).  Here the block is factored 16 columns at a time,
+// right-looking (the same recursion as chol_inv_rec, unrolled at 16-row granularity):
+//   step k:  (L_kk, T_kk) = chol16(A_kk)                      one warp, registers + shuffles
+//            L_ik = A_ik T_kk^T                (i > k)          DMMA, 8-row strips
+//            A_ij -= L_ik L_jk^T               (i >= j > k)     DMMA, 16 x 16 blocks
+//            T_kj = -T_kk sum_{l=j}^{k-1} L_kl T_lj  (j < k)    DMMA, 16 x 8 strips (row block k of
+//                                                               T = L^{-1}, from [[L11,0],[L21,L22]]^-1)
+// Shared memory holds the block column-major (Mat(r, c) = S[c LD + r], LD = 132 = 4 mod 16 so both the
+// m8n8k4 row- and column-fragment patterns are conflict-free per half-warp); L fills the lower
+// triangle, the off-diagonal blocks of T are kept transposed in the strict upper blocks
+// (Mat(c, r) = T(r, c)), the diagonal blocks T_kk in Td.  A ragged block (nb % 16 != 0) is padded with
+// the identity, whose pivots are 1 and never fail the NotSPD test.
+// GLS_LEAF_PROF (diagnostics, tools/leaf_probe): clock64 per phase of chol_inv_leaf128, summed by thread 0
+// over launches into g_leaf_prof[0: load, 1: diag16, 2: panel, 3: trailing + T rows, 4: write back].
+#ifdef GLS_LEAF_PROF
+__device__ unsigned long long g_leaf_prof[8];
+#define LEAF_PROF_START() long long _lp_t = clock64()
+#define LEAF_PROF(q)                                      \
+  do {                                                    \
+    if (threadIdx.x == 0) {                               \
+      const long long _lp_n = clock64();                  \
+      atomicAdd(&g_leaf_prof[q], (unsigned long long)(_lp_n - _lp_t)); \
+      _lp_t = _lp_n;                                      \
+    }                                                     \
+  } while (0)
+#else
+#define LEAF_PROF_START()
+#define LEAF_PROF(q)
+#endif
+
+namespace blk {
+constexpr int NB = 128, B = 16, NBK = NB / B, LD = 132, TLD = 20, THREADS = 256, NW = THREADS / 32;
+constexpr size_t SMEM = (size_t)(NB * LD + NBK * B * TLD + NW * B * TLD) * sizeof(double);
+}  // namespace blk
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// chol16 + inverse of one 16 x 16 diagonal block by one warp (the critical path of the leaf).
+// Cholesky: lanes 0-15 hold row i = lane of the block (R[c], c <= i); column j: pivot d = L[j][j]
+// (lane j, shuffled), r = 1/sqrt(d), c_i = L[i][j] r (i > j) broadcast through shared memory (double
+// buffered, one __syncwarp per column), L[i][k] -= c_i c_k (j < k <= i).  Inverse: lane c solves
+// L t = e_c by right-looking forward substitution, t_i = (delta_ic + s_i) / L_ii, s_i' -= L[i'][i] t_i.
+// Writes L (zeros above the diagonal) into D and T = L^{-1} into Tk.  cb: 80 doubles of scratch.
+// (A first version that also swept T = [L | I] with shuffles took 18.8k cycles per block.)
+__device__ __forceinline__ void diag16(double* D, double* Tk, double* cb, double tol, int64_t gpiv,
+                                       CholStatus* st, int* failed) {
+  using namespace blk;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, i = lane & 15;
+  const bool lo = lane < 16;
+  const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+#ifdef GLS_LEAF_PROF
+  long long _d0 = clock64();
+#endif
+  double R[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) R[c] = (lo && c <= i) ? D[c * LD + i] : 0.0;
+  const bool fl0 = *(volatile int*)failed;
+  bool fl = fl0;
+  int jfail = 16;  // first failing pivot of this block (no branch in the sweep)
+  double* rinv = cb + 32;
+  // the pivot chain runs ahead of the shared-memory update: lane j+1 forms its updated diagonal
+  // L[j+1][j+1] - c_{j+1}^2 (the same operation the update below applies) right after c is known
+  // (and its rsqrt, the longest link, is issued before this column's shared-memory round trip)
+  double dn = __shfl_sync(FULL, R[0], 0);
+  bool badn = fl || !(dn > tol);
+  double rn = badn ? qnan : rsqrt(dn);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const double d = dn, r = rn;
+    const bool bad = badn;
+    jfail = (bad && !fl) ? j : jfail;
+    fl = bad;
+    const double ci = R[j] * r;
+    if (j < 15) {
+      dn = __shfl_sync(FULL, R[j + 1] - ci * ci, j + 1);
+      badn = bad || !(dn > tol);
+      rn = badn ? qnan : rsqrt(dn);
+    }
+    double* col = cb + 16 * (j & 1);
+    if (lo && i > j) col[i] = ci;
+    if (lane == j) {
+      R[j] = d * r;
+      rinv[j] = r;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 1; k < 16; ++k) {
+      if (k > j) {
+        const double ck = col[k];
+        if (lo && i >= k) R[k] -= ci * ck;
+      }
+    }
+    if (lo && i > j) R[j] = ci;
+  }
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    if (lo) D[c * LD + i] = (c <= i) ? R[c] : 0.0;
+  if (lane == 0 && !fl0 && jfail < 16) {
+    atomicMin(&st->fail, (unsigned long long)(gpiv + jfail));
+    *(volatile int*)failed = 1;
+  }
+  __syncwarp();
+#ifdef GLS_LEAF_PROF
+  long long _d1 = clock64();
+  if (threadIdx.x == 0) atomicAdd(&g_leaf_prof[5], (unsigned long long)(_d1 - _d0));
+#endif
+  // T = L^{-1}: lane c < 16 forms column c (t_i = 0 for i < c falls out of the recursion)
+  double sacc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) sacc[q] = 0.0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const double tq = ((q == i) ? 1.0 + sacc[q] : sacc[q]) * rinv[q];
+    sacc[q] = tq;  // sacc[q] now holds t_q
+#pragma unroll
+    for (int q2 = q + 1; q2 < 16; ++q2) sacc[q2] -= D[q * LD + q2] * tq;
+  }
+  if (lo) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Tk[i * TLD + q] = sacc[q];
+  }
+#ifdef GLS_LEAF_PROF
+  __syncwarp();
+  if (threadIdx.x == 0) atomicAdd(&g_leaf_prof[6], (unsigned long long)(clock64() - _d1));
+#endif
+}
+
+// L_rows = A_rows T_kk^T for one 8-row strip (both 8-column tiles), in place.
+__device__ __forceinline__ void panel_strip(double* S, const double* Tk, int k0, int r0) {
+  using namespace blk;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double a[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) a[kk] = S[(k0 + 4 * kk + t) * LD + r0 + g];
+  double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int ct = 0; ct < 2; ++ct) dmma884(c[ct], a[kk], Tk[(4 * kk + t) * TLD + 8 * ct + g]);
+#pragma unroll
+  for (int ct = 0; ct < 2; ++ct)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) S[(k0 + 8 * ct + 2 * t + e) * LD + r0 + g] = c[ct][e];
+}
+
+// Mat[bi.., bj..] -= L[bi.., k0..] L[bj.., k0..]^T for one 16 x 16 block (lower tiles only if bi == bj).
+__device__ __forceinline__ void update_block(double* S, int k0, int bi, int bj) {
+  using namespace blk;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double na[2][4], b[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      na[h][kk] = -S[(k0 + 4 * kk + t) * LD + bi + 8 * h + g];
+      b[h][kk] = S[(k0 + 4 * kk + t) * LD + bj + 8 * h + g];
+    }
+  double c[2][2][2];
+#pragma unroll
+  for (int ra = 0; ra < 2; ++ra)
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) c[ra][cb][e] = S[(bj + 8 * cb + 2 * t + e) * LD + bi + 8 * ra + g];
+  // k outermost: the three or four tile chains interleave
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int ra = 0; ra < 2; ++ra)
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb)
+        if (!(bi == bj && cb > ra)) dmma884(c[ra][cb], na[ra][kk], b[cb][kk]);
+#pragma unroll
+  for (int ra = 0; ra < 2; ++ra)
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb)
+      if (!(bi == bj && cb > ra))
+#pragma unroll
+        for (int e = 0; e < 2; ++e) S[(bj + 8 * cb + 2 * t + e) * LD + bi + 8 * ra + g] = c[ra][cb][e];
+}
+
+// Columns [n0, n0 + 8) of the off-diagonal block T_kj (j < k) of T = L^{-1}:
+//   W = sum_{l=j}^{k-1} L_kl T_lj,  T_kj = -T_kk W   (stored transposed at Mat(j0 + n0 + col, k0 + row)).
+__device__ __forceinline__ void trow_strip(double* S, const double* Td, double* W, int k, int j, int n0) {
+  using namespace blk;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int k0 = B * k, j0 = B * j;
+  const double* Tk = Td + k * B * TLD;
+  double w[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  {
+    const double* Tj = Td + j * B * TLD;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const double bv = Tj[(n0 + g) * TLD + 4 * kk + t];
+#pragma unroll
+      for (int ra = 0; ra < 2; ++ra) dmma884(w[ra], S[(j0 + 4 * kk + t) * LD + k0 + 8 * ra + g], bv);
+    }
+  }
+  for (int l = j + 1; l < k; ++l) {
+    const int l0 = B * l;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const double bv = S[(l0 + 4 * kk + t) * LD + j0 + n0 + g];
+#pragma unroll
+      for (int ra = 0; ra < 2; ++ra) dmma884(w[ra], S[(l0 + 4 * kk + t) * LD + k0 + 8 * ra + g], bv);
+    }
+  }
+#pragma unroll
+  for (int ra = 0; ra < 2; ++ra)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) W[(2 * t + e) * TLD + 8 * ra + g] = w[ra][e];
+  __syncwarp();
+  double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const double bv = W[g * TLD + 4 * kk + t];
+#pragma unroll
+    for (int ra = 0; ra < 2; ++ra) dmma884(c[ra], -Tk[(4 * kk + t) * TLD + 8 * ra + g], bv);
+  }
+#pragma unroll
+  for (int ra = 0; ra < 2; ++ra)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) S[(k0 + 8 * ra + g) * LD + j0 + n0 + 2 * t + e] = c[ra][e];
+  __syncwarp();
+}
+
+// Schedule (look-ahead): warp 0 carries the critical path -- the panel strips of block row k+1, the
+// update of the next diagonal block and chol16 of it -- while warps 1-7 do the rest of the panel, the
+// trailing update and row block k of T.  Two block-wide barriers per step.
+__global__ void __launch_bounds__(blk::THREADS) chol_inv_leaf128(int nb, double* A, double* T, int64_t ld,
+                                                                int64_t goff, CholStatus* st) {
+  using namespace blk;
+  extern __shared__ double leaf_smem[];
+  double* S = leaf_smem;                 // Mat(r, c) = S[c LD + r]
+  double* Td = S + NB * LD;              // T_kk(r, c) = Td[k B TLD + c TLD + r]
+  double* Wsc = Td + NBK * B * TLD;      // per-warp 16 x 8 scratch (column-major, TLD); warp 0: chol16's
+  __shared__ int failed;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nbk = (nb + B - 1) / B, np = nbk * B;
+  LEAF_PROF_START();
+  // every element's load in flight at once (cp.async; 16-byte pieces when A allows)
+  const bool vec = ((ld & 1) == 0) && ((((uintptr_t)A) | ((uintptr_t)T)) & 15) == 0;
+  for (int c = warp; c < np; c += NW) {
+    for (int r = 2 * lane; r < np; r += 64) {
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(S + c * LD + r);
+      if (vec && r >= c && r + 1 < nb) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(A + r + (int64_t)c * ld) : "memory");
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int re = r + e;
+          if (re >= c && re < nb) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d + 8 * e), "l"(A + re + (int64_t)c * ld)
+                         : "memory");
+          } else {
+            S[c * LD + re] = (re == c) ? 1.0 : 0.0;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  if (tid == 0) failed = 0;
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  LEAF_PROF(0);
+  const double tol = st->tol;
+  double* W = Wsc + warp * B * TLD;
+  if (warp == 0) diag16(S, Td, W, tol, goff, st, &failed);
+  __syncthreads();
+  LEAF_PROF(1);
+  for (int k = 0; k < nbk; ++k) {
+    const int k0 = k * B;
+    const double* Tk = Td + k * B * TLD;
+    // panel of step k: warp 0 the two strips of block row k+1, warps 1-7 the rest
+    const int nstrip = 2 * (nbk - 1 - k);
+    if (warp == 0) {
+      for (int u = 0; u < 2 && u < nstrip; ++u) panel_strip(S, Tk, k0, k0 + B + 8 * u);
+    } else {
+      for (int u = 2 + warp - 1; u < nstrip; u += NW - 1) panel_strip(S, Tk, k0, k0 + B + 8 * u);
+    }
+    __syncthreads();
+    LEAF_PROF(2);
+    if (warp == 0) {
+      if (k + 1 < nbk) {
+        update_block(S, k0, k0 + B, k0 + B);
+        __syncwarp();
+        diag16(S + (k0 + B) * LD + k0 + B, Td + (k + 1) * B * TLD, W, tol, goff + k0 + B, st, &failed);
+      }
+    } else {
+      // trailing update except the next diagonal block, then row block k of T
+      const int nt = nbk - 1 - k, nupd = nt * (nt + 1) / 2;
+      const int u0 = nupd > 0 ? 1 : 0;  // unit 0 is the next diagonal block (warp 0's) when there is one
+      for (int u = u0 + warp - 1; u < nupd + 2 * k; u += NW - 1) {
+        if (u < nupd) {
+          int i = 0, q = u;  // u -> (i, q), 0 <= q <= i < nt, row-major over the lower triangle
+          while (q > i) q -= ++i;
+          update_block(S, k0, k0 + B + B * i, k0 + B + B * q);
+        } else {
+          const int v = u - nupd;
+          trow_strip(S, Td, W, k, v >> 1, 8 * (v & 1));
+        }
+      }
+    }
+    __syncthreads();
+    LEAF_PROF(3);
+  }
+  // write back L (lower triangle of A) and T (zeros above the diagonal): a warp per column
+  for (int c = warp; c < nb; c += NW) {
+    const int bc = c / B;
+    for (int r = 2 * lane; r < nb; r += 64) {
+      double lv[2], tv[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int re = r + e, br = re / B;
+        lv[e] = S[c * LD + re];
+        tv[e] = 0.0;
+        if (br == bc) tv[e] = Td[br * B * TLD + (c - B * bc) * TLD + (re - B * br)];
+        else if (br > bc) tv[e] = S[re * LD + c];
+      }
+      double* pa = A + r + (int64_t)c * ld;
+      double* pt = T + r + (int64_t)c * ld;
+      if (vec && r + 1 < nb) {
+        if (r >= c) *(double2*)pa = make_double2(lv[0], lv[1]);
+        else if (r + 1 == c) pa[1] = lv[1];
+        *(double2*)pt = make_double2(tv[0], tv[1]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (r + e < nb) {
+            if (r + e >= c) pa[e] = lv[e];
+            pt[e] = tv[e];
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  LEAF_PROF(4);
+}
+
 // Streams of the recursion: the main stream s (the context's, high priority) carries the critical
 // path; at each depth a low-priority "side" stream takes the part of the trailing update the next
 // leaf does not need yet (look-ahead) and a high-priority "aux" stream the Y = L21 T11 product.  Each stream has
@@ -363,9 +712,17 @@ cudaEvent_t record(RecCtx& rc, cudaStream_t st) {
   return e;
 }
 
+// Leaf size of the recursion: 128 (chol_inv_leaf128, the blocked DMMA leaf; default) or 64 (the
+// column-sweep leaves and 128-row nodes of round 1; GLS_LEAF128=0, kept for A/B).
+int leaf_size() {
+  static const int v = (getenv("GLS_LEAF128") && atoi(getenv("GLS_LEAF128")) == 0) ? LEAF : blk::NB;
+  return v;
+}
+
 int64_t first_block(int64_t n) {  // size of the leading block of the split of an n x n node
-  const int64_t nblk = (n + LEAF - 1) / LEAF;
-  return LEAF * ((nblk + 1) / 2);
+  const int64_t lf = leaf_size();
+  const int64_t nblk = (n + lf - 1) / lf;
+  return lf * ((nblk + 1) / 2);
 }
 
 // Factor and invert the n x n node at A (T receives the inverse).  On entry the node's leading
@@ -374,6 +731,17 @@ int64_t first_block(int64_t n) {  // size of the leading block of the split of a
 void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64_t goff, cudaEvent_t rest_ready,
                   int depth) {
   cudaStream_t s = rc.s;
+  if (leaf_size() == blk::NB && n <= blk::NB) {
+    if (first_use_on_device((const void*)chol_inv_leaf128))
+      cudaFuncSetAttribute(chol_inv_leaf128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)blk::SMEM);
+    if (rest_ready) cudaStreamWaitEvent(s, rest_ready, 0);
+    wait_cols(rc, s, goff + n);
+    mark(s, depth, "wait-rest");
+    chol_inv_leaf128<<<1, blk::THREADS, blk::SMEM, s>>>((int)n, A, T, ld, goff, rc.st);
+    if (rc.lc) ++*rc.lc;
+    mark(s, depth, "leaf");
+    return;
+  }
   if (n <= LEAF) {
     constexpr int kLeafSmem = 2 * LEAF * LLD * sizeof(double);
     if (first_use_on_device((const void*)chol_inv_leaf))
@@ -464,7 +832,7 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least urgent
   int depth = 1;
-  for (int64_t k = n; k > LEAF && depth < kMaxDepth; k = first_block(k)) ++depth;
+  for (int64_t k = n; k > leaf_size() && depth < kMaxDepth; k = first_block(k)) ++depth;
   RecCtx rc{};
   rc.s = s;
   std::vector<cudaEvent_t> events;
