@@ -518,6 +518,114 @@ bool try_tma(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, cons
   return true;
 }
 
+// ---------------------------------------------------------------- small products (latency)
+// The recursion's deep levels multiply blocks of a few hundred rows: 128 x 64 tiles leave most SMs
+// idle and split-K adds a reduction launch (~20 us per product on the critical path).  Here a CTA
+// computes a 32 x 32 output tile; its 8 warps are 2 (16-row halves) x 4 (k-steps of each 16-wide K
+// slice), each with eight 8 x 8 DMMA accumulators, and the four partial tiles are summed in a fixed
+// order through shared memory at the end (deterministic).  Operands are staged by cp.async in a
+// 3-stage ring of [32 rows][BK = 16 (+4 pad)] tiles (conflict-free fragment loads).  op(A) = A only.
+namespace sg {
+constexpr int BM = 32, BN = 32, BK = 16, LDK = BK + 4, STAGES = 3, THREADS = 256;
+constexpr int A_T = BM * LDK, B_T = BN * LDK;
+constexpr int SMEM_DOUBLES = (STAGES * (A_T + B_T) > 4 * BM * BN) ? STAGES * (A_T + B_T) : 4 * BM * BN;
+}  // namespace sg
+
+template <bool TB>
+__global__ void __launch_bounds__(sg::THREADS) dgemm_small_kernel(GemmParams p) {
+  constexpr int BM = sg::BM, BN = sg::BN, BK = sg::BK, LDK = sg::LDK, STAGES = sg::STAGES, THREADS = sg::THREADS,
+                A_T = sg::A_T, B_T = sg::B_T, SMEM_DOUBLES = sg::SMEM_DOUBLES;
+  __shared__ __align__(16) double sm[SMEM_DOUBLES];
+  double* As = sm;
+  double* Bs = sm + STAGES * A_T;
+  const int64_t tm = (p.M + BM - 1) / BM;
+  const int64_t tile = blockIdx.x;
+  const int64_t r0 = (tile % tm) * BM, c0 = (tile / tm) * BN;
+  if ((p.flags & GEMM_LOWER_C) && c0 >= r0 + BM) return;
+  int64_t kb = 0, ke = p.K;
+  if (p.flags & GEMM_KMIN_COL) kb = c0;
+  if (p.flags & GEMM_KMAX_ROW) ke = min(ke, r0 + BM);
+  if (p.flags & GEMM_KMAX_COL) ke = min(ke, c0 + BN);
+  const int64_t kbeg = kb;
+  kb = (kb / BK) * BK;
+  const int nk = (ke > kb) ? (int)((ke - kb + BK - 1) / BK) : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wk = warp >> 1;  // rows [16 wm, 16 wm + 16), k-step wk of each BK slice
+  const int g = lane >> 2, t = lane & 3;
+  auto issue = [&](int kt, int stg) {
+    const int64_t k0 = kb + (int64_t)kt * BK;
+    double* as = As + stg * A_T;
+    double* bs = Bs + stg * B_T;
+#pragma unroll
+    for (int j = 0; j < (BM * BK) / THREADS; ++j) {  // 2
+      const int idx = tid + j * THREADS;
+      const int m = idx % BM, k = idx / BM;
+      const int64_t gm = r0 + m, gk = k0 + k;
+      const bool v = gm < p.M && gk < ke && gk >= kbeg;
+      cp_async8(as + m * LDK + k, v ? p.A + gm + gk * p.lda : p.A, v);
+    }
+#pragma unroll
+    for (int j = 0; j < (BN * BK) / THREADS; ++j) {  // 2
+      const int idx = tid + j * THREADS;
+      int n, k;
+      if (!TB) { k = idx % BK; n = idx / BK; } else { n = idx % BN; k = idx / BN; }
+      const int64_t gn = c0 + n, gk = k0 + k;
+      const bool v = gn < p.N && gk < ke && gk >= kbeg;
+      cp_async8(bs + n * LDK + k, v ? (TB ? p.B + gn + gk * p.ldb : p.B + gk + gn * p.ldb) : p.B, v);
+    }
+  };
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) issue(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nxt = kt + STAGES - 1;
+    if (nxt < nk) issue(nxt, nxt % STAGES);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * A_T + (16 * wm + g) * LDK + 4 * wk + t;
+    const double* bs = Bs + (kt % STAGES) * B_T + g * LDK + 4 * wk + t;
+    double a[2], b[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) a[i] = as[8 * i * LDK];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = bs[8 * j * LDK];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // partial tiles of the four k-step groups -> shared memory, summed in the order wk = 0, 1, 2, 3
+  double* red = sm;  // [wk][n][m] (32 x 32 per group)
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) red[wk * BM * BN + (8 * j + 2 * t + e) * BM + 16 * wm + 8 * i + g] = acc[i][j][e];
+  __syncthreads();
+  for (int o = tid; o < BM * BN; o += THREADS) {
+    const int m = o % BM, n = o / BM;
+    const int64_t gm = r0 + m, gn = c0 + n;
+    if (gm < p.M && gn < p.N) {
+      const double v = ((red[o] + red[BM * BN + o]) + red[2 * BM * BN + o]) + red[3 * BM * BN + o];
+      double* cp = p.C + gm + gn * p.ldc;
+      double r = p.alpha * v;
+      if (p.beta != 0.0) r += p.beta * *cp;
+      *cp = r;
+    }
+  }
+}
+
 template <bool TA, bool TB>
 void launch(cudaStream_t s, dim3 grid, const GemmParams& p) {
   if (first_use_on_device((const void*)dgemm_kernel<TA, TB>))
@@ -645,9 +753,18 @@ void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const 
 #endif
   GemmParams p{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, flags, 1, nullptr};
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
-  // small output, long K: split K so the launch fills the machine (the recursion's deep levels)
   const int64_t tiles = (int64_t)grid.x * grid.y;
   const int64_t ktiles = (K + BK - 1) / BK;
+  // small output: 32 x 32 tiles, no split-K launch (GLS_DGEMM_SMALL=0 restores the split-K path)
+  static const bool small_on = !(getenv("GLS_DGEMM_SMALL") && atoi(getenv("GLS_DGEMM_SMALL")) == 0);
+  if (small_on && opA == 'N' && tiles < 74 && max_ctas <= 0) {
+    const int64_t st = ((M + sg::BM - 1) / sg::BM) * ((N + sg::BN - 1) / sg::BN);
+    if (opB == 'T') dgemm_small_kernel<true><<<(unsigned)st, sg::THREADS, 0, s>>>(p);
+    else dgemm_small_kernel<false><<<(unsigned)st, sg::THREADS, 0, s>>>(p);
+    if (launch_counter) ++*launch_counter;
+    return;
+  }
+  // small output, long K: split K so the launch fills the machine (the recursion's deep levels)
   if (tiles < 74 && ktiles >= 8) {
     int sp = (int)((148 + tiles - 1) / tiles);
     if (sp > ktiles / 4) sp = (int)(ktiles / 4);

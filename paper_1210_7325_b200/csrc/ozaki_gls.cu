@@ -278,7 +278,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int i0 = 2 * t;
           const int nrb = vstep ? 1 : (i0 + 1 < kp.NBR ? 2 : 1);
           const int nc = vstep ? kp.NC : (i0 >> 2) + 1;
+#ifdef GLS_OZ_EXP_HALFB
+          // EXPERIMENT (wrong results; timing only): one B half per stage, shared by both row blocks
+          const uint32_t bbytes = vstep ? (uint32_t)kp.NV * (kKC / 2) : (uint32_t)kBHalf;
+#else
           const uint32_t bbytes = vstep ? (uint32_t)kp.NV * (kKC / 2) : (uint32_t)nrb * kBHalf;
+#endif
           for (int k = 0; k < nc; ++k) {
             const int c = chunk_at(t, nc, k);
             timed_wait(&empty[stage], ph ^ 1, pw);
@@ -292,7 +297,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (vstep) {
               tma_2d_g2s_pair(sb, &vmap, 0, c * kp.NV + (int)rank * (kp.NV / 2), fb);
             } else {
+#ifdef GLS_OZ_EXP_HALFB
+              for (int sl = 0; sl < 1; ++sl) {
+#else
               for (int sl = 0; sl < nrb; ++sl) {
+#endif
                 const int trow0 = (int)(oz_tile_offset(i0 + sl) * kBN) + (int)rank * (kBN / 2);
                 tma_2d_g2s_pair(sb + sl * kBHalf, &tmap, 0, trow0 + c * kBN, fb);
               }
@@ -321,7 +330,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // the 4 K=32 MMAs of stage st (K chunk k of the step) into accumulator region sl
       auto issue = [&](int st, int k, int sl, uint32_t idesc) {
         const uint64_t ad = sdesc_k128(a0 + st * kATile);
+#ifdef GLS_OZ_EXP_HALFB
+        const uint64_t bd = sdesc_k128(b0 + st * (2 * kBHalf));
+#else
         const uint64_t bd = sdesc_k128(b0 + st * (2 * kBHalf) + sl * kBHalf);
+#endif
 #pragma unroll
         for (int kk = 0; kk < kKC / 32; ++kk)
           mma_i8_pair(tbase + sl * 256, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idesc, (k | kk) != 0);
@@ -410,9 +423,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     };
     // z rows 16 h .. 16 h + 15 of the row block in TMEM region `sl`: the 7 digit sums combined exactly
     // in int64 (two partial sums), then one FP64 rounding each
+    // The region is released right after the last TMEM load completes (before the FP64 rounding), so
+    // the MMA issuer's wait for it does not include this warp's arithmetic.
     auto drain = [&](int sl, double (&z)[16]) {
       const uint32_t tr = tlane + sl * 256 + h * 16;
-#if GLS_OZ_DRAIN_RT == 2
+#if defined(GLS_OZ_EXP_NODRAIN)
+      // EXPERIMENT (wrong results; timing only): no TMEM traffic or arithmetic in the epilogue
+      release(sl);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) z[r] = 0.0;
+#elif GLS_OZ_DRAIN_RT == 2
       // two TMEM round trips: digits 0-3 (the high part), then digits 4-6
       long long hi[16];
       {
@@ -433,6 +453,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_ld16(tr + 5 * kR, d5);
         tmem_ld16(tr + 6 * kR, d6);
         tmem_wait_ld();
+        release(sl);
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
           const long long lo = (long long)d4[r] * 65536LL + (long long)d5[r] * 256LL + (long long)d6[r];
@@ -460,6 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int r = 0; r < 16; ++r) lo[r] = (long long)va[r] * 65536LL + (long long)vb[r] * 256LL;
       tmem_ld16(tr + 6 * kR, va);
       tmem_wait_ld();
+      release(sl);
 #pragma unroll
       for (int r = 0; r < 16; ++r) z[r] = fma((double)hi[r], 16777216.0, (double)(lo[r] + (long long)va[r]));
 #endif
@@ -505,7 +527,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // last MMAs still run
         double z[16];
         drain(0, z);
-        release(0);
         if (pe) prof_drain += clock64() - tw0;
         reduce(sig0, z);
         if (two) {
@@ -514,7 +535,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
           }
           drain(1, z);
-          release(1);
           reduce(sig1, z);
         }
         if (pe) prof_busy += clock64() - tw0;
