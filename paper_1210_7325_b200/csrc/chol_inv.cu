@@ -725,6 +725,14 @@ int64_t first_block(int64_t n) {  // size of the leading block of the split of a
   return lf * ((nblk + 1) / 2);
 }
 
+// levels of the recursion tree of an n x n node (a leaf is one level)
+int tree_depth(int64_t n) {
+  if (n <= leaf_size()) return 1;
+  const int64_t h1 = first_block(n);
+  const int a = tree_depth(h1), b = tree_depth(n - h1);
+  return 1 + (a > b ? a : b);
+}
+
 // Factor and invert the n x n node at A (T receives the inverse).  On entry the node's leading
 // first_block(n) x first_block(n) block is up to date in the order of the main stream; the rest of
 // the node (rows below it) is up to date once `rest_ready` has fired (nullptr: already).
@@ -792,7 +800,11 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
   cudaEvent_t e_rest = nullptr;
   cudaStream_t sd = rc.side[d];
   if (h2 > g) {
-    cudaStreamWaitEvent(sd, e_start, 0);
+    // the look-ahead products start after the main stream's two (GLS_SIDE_AFTER=1): persistent CTAs
+    // hold their SMs for the whole product, so started together they left L21top / SYRK11 -- the
+    // critical path -- a few SMs; the side work has the next leaf's whole recursion to hide behind
+    static const bool after = !(getenv("GLS_SIDE_AFTER") && atoi(getenv("GLS_SIDE_AFTER")) == 0);
+    cudaStreamWaitEvent(sd, after ? record(rc, s) : e_start, 0);
     dgemm(sd, h2 - g, h1, h1, 1.0, A21 + g, ld, 'N', T11, ld, 'T', 0.0, T21 + g, ld, GEMM_KMAX_COL, rc.lc,
           rc.ws_side[d], rc.off_ctas);
     cudaStreamWaitEvent(sd, e_top, 0);
@@ -831,8 +843,8 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
               int64_t* lc, const ColsReady* arriving) {
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least urgent
-  int depth = 1;
-  for (int64_t k = n; k > leaf_size() && depth < kMaxDepth; k = first_block(k)) ++depth;
+  int depth = tree_depth(n);
+  if (depth > kMaxDepth) depth = kMaxDepth;
   RecCtx rc{};
   rc.s = s;
   std::vector<cudaEvent_t> events;

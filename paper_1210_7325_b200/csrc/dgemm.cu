@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 
 #include "gls_internal.cuh"
@@ -223,6 +224,9 @@ struct Params {
   double alpha, beta;
   int flags;
   int64_t tm, ntiles;
+  int64_t tn, nvalid;  // tile columns; tiles actually computed (LOWER_C: those meeting the lower triangle)
+  int order;           // tile order (ORD_*): longest K range first
+  int snake;           // CTA b takes ordered tiles q G + b (q even) / q G + G - 1 - b (q odd)
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -251,6 +255,42 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, i
 }
 __device__ __forceinline__ void lds128(uint32_t a, double& x, double& y) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(a));
+}
+
+// Tile schedule.  A triangular operand makes the tiles' K ranges (their cost) linear in the tile's row
+// or column, and LOWER_C leaves only the tiles meeting the lower triangle; a plain round-robin over the
+// tile grid then gives some CTAs twice the work of others (measured: mid-size products of the
+// recursion at 10-17 TF/s).  The computed tiles are enumerated longest first and dealt to the
+// persistent CTAs in a snake order (round q: CTA b takes q G + b, or q G + G - 1 - b when q is odd),
+// which balances linear cost profiles.  Which tiles a CTA computes and in what order changes no bit of
+// any tile (each tile's K loop is fixed).
+enum { ORD_NATURAL = 0, ORD_COL_DESC = 1, ORD_COL_ASC = 2, ORD_ROW_DESC = 3, ORD_LOWER = 4 };
+__device__ __forceinline__ bool tile_at(const Params& p, int64_t q, int64_t& r0, int64_t& c0) {
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t idx = q * G + ((p.snake && (q & 1)) ? G - 1 - b : b);
+  if (idx >= p.nvalid) return false;
+  int64_t i, j;
+  switch (p.order) {
+    case ORD_COL_DESC: j = p.tn - 1 - idx / p.tm; i = idx % p.tm; break;
+    case ORD_COL_ASC: j = idx / p.tm; i = idx % p.tm; break;
+    case ORD_ROW_DESC: i = p.tm - 1 - idx / p.tn; j = idx % p.tn; break;
+    case ORD_LOWER: {  // row i holds the columns j with j BN < (i + 1) BM
+      int64_t rem = idx;
+      i = 0;
+      for (;; ++i) {
+        int64_t cnt = ((i + 1) * BM + BN - 1) / BN;
+        if (cnt > p.tn) cnt = p.tn;
+        if (rem < cnt) break;
+        rem -= cnt;
+      }
+      j = rem;
+      break;
+    }
+    default: i = idx % p.tm; j = idx / p.tm; break;
+  }
+  r0 = i * BM;
+  c0 = j * BN;
+  return true;
 }
 
 // K range of an output tile (the old kernel's triangular rules, at stage granularity)
@@ -335,9 +375,9 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_tma_kernel(const __grid_cons
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&bmap) : "memory");
       int st = 0;
       uint32_t ph = 0;
-      for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-        const int64_t r0 = (tile % p.tm) * BM, c0 = (tile / p.tm) * BN;
-        if ((p.flags & GEMM_LOWER_C) && c0 >= r0 + BM) continue;
+      int64_t r0, c0;
+      for (int64_t q = 0; tile_at(p, q, r0, c0); ++q) {
+        if ((p.flags & GEMM_LOWER_C) && c0 >= r0 + BM) continue;  // (natural order only)
         int64_t kb;
         int nk;
         krange(p, r0, c0, kb, nk);
@@ -366,8 +406,8 @@ __global__ void __launch_bounds__(THREADS, 1) dgemm_tma_kernel(const __grid_cons
   const uint32_t a_lane = (uint32_t)((wm * 32 + 2 * l4) * 8);
   int st = 0;
   uint32_t ph = 0;
-  for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-    const int64_t r0 = (tile % p.tm) * BM, c0 = (tile / p.tm) * BN;
+  int64_t r0, c0;
+  for (int64_t q = 0; tile_at(p, q, r0, c0); ++q) {
     if ((p.flags & GEMM_LOWER_C) && c0 >= r0 + BM) continue;
     int64_t kb;
     int nk;
@@ -500,12 +540,33 @@ bool try_tma(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, cons
   p.beta = beta;
   p.flags = flags;
   p.tm = (M + tg::BM - 1) / tg::BM;
-  p.ntiles = p.tm * ((N + tg::BN - 1) / tg::BN);
+  p.tn = (N + tg::BN - 1) / tg::BN;
+  p.ntiles = p.tm * p.tn;
+  // tile order: longest K range first (the flags the recursion uses come alone; anything else keeps
+  // the natural order)
+  static const int sched = getenv("GLS_DGEMM_SCHED") ? atoi(getenv("GLS_DGEMM_SCHED")) : 1;
+  p.order = tg::ORD_NATURAL;
+  p.nvalid = p.ntiles;
+  p.snake = 0;
+  if (flags == GEMM_LOWER_C) {
+    p.order = tg::ORD_LOWER;
+    p.nvalid = 0;
+    for (int64_t i = 0; i < p.tm; ++i) p.nvalid += std::min<int64_t>(p.tn, ((i + 1) * tg::BM + tg::BN - 1) / tg::BN);
+  } else if (sched) {
+    if (flags == GEMM_KMAX_COL) p.order = tg::ORD_COL_DESC;
+    else if (flags == GEMM_KMIN_COL) p.order = tg::ORD_COL_ASC;
+    else if (flags == GEMM_KMAX_ROW) p.order = tg::ORD_ROW_DESC;
+  }
+  if (sched) p.snake = p.order != tg::ORD_NATURAL && p.order != tg::ORD_LOWER ? 1 : 0;
+  if (!sched && flags == GEMM_LOWER_C) {  // A/B: the round-1 walk (skipped tiles stay in the round-robin)
+    p.order = tg::ORD_NATURAL;
+    p.nvalid = p.ntiles;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int64_t grid = max_ctas > 0 ? std::max(1, max_ctas / 2) : sms;  // one CTA per SM (max_ctas counts two per SM)
-  if (grid > p.ntiles) grid = p.ntiles;
+  if (grid > p.nvalid) grid = p.nvalid;
   if (bt) {
     if (first_use_on_device((const void*)tg::dgemm_tma_kernel<true>))
       cudaFuncSetAttribute(tg::dgemm_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tg::SMEM);
@@ -752,6 +813,10 @@ void dgemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, double alpha, const 
   }
 #endif
   GemmParams p{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, flags, 1, nullptr};
+  static const bool trace = getenv("GLS_TRACE_GEMM") != nullptr;  // diagnostics: one line per product
+  if (trace)
+    fprintf(stderr, "[gemm] %lld %lld %lld %c%c flags %d stream %p cap %d\n", (long long)M, (long long)N,
+            (long long)K, opA, opB, flags, (void*)s, max_ctas);
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
   const int64_t tiles = (int64_t)grid.x * grid.y;
   const int64_t ktiles = (K + BK - 1) / BK;

@@ -48,6 +48,11 @@
 #ifndef GLS_OZ_DRAIN_RT
 #define GLS_OZ_DRAIN_RT 2
 #endif
+// pR = 1 variants: drain a row-block half in ONE round trip (all 7 digit loads in flight), so the
+// region is released one TMEM latency earlier (A/B: see DESIGN.md §5.4)
+#ifndef GLS_OZ_DRAIN_ONE
+#define GLS_OZ_DRAIN_ONE 1
+#endif
 
 namespace gls {
 namespace {
@@ -62,6 +67,7 @@ constexpr int kATile = 128 * kKC;        // 16 KiB
 constexpr int kBTile = kBN * kKC;        // 28 KiB (whole packed digit tile)
 constexpr int kBHalf = kBTile / 2;       // 14 KiB staged per CTA of a pair
 constexpr int kEpiWarps = 8;
+constexpr bool kDrainOneTrip = GLS_OZ_DRAIN_ONE != 0;
 constexpr int kConvWarps = 2;  // convert-ahead warps: FP64 -> int8 of the NEXT chunk (see the kernel)
 constexpr int kThreads = (2 + kEpiWarps + kConvWarps) * 32;
 constexpr int kCvBuf = 8192;          // bytes per convert-ahead staging buffer (two per conv warp)
@@ -433,6 +439,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int r = 0; r < 16; ++r) z[r] = 0.0;
 #elif GLS_OZ_DRAIN_RT == 2
+      if constexpr (PR1 && kDrainOneTrip) {
+        // one TMEM round trip: all 7 digit loads in flight, one wait, release, then the arithmetic
+        // (the 1-accumulator Gram variants have the registers for it: 148, no spills)
+        int32_t d0[16], d1[16], d2[16], d3[16], d4[16], d5[16], d6[16];
+        tmem_ld16(tr, d0);
+        tmem_ld16(tr + 1 * kR, d1);
+        tmem_ld16(tr + 2 * kR, d2);
+        tmem_ld16(tr + 3 * kR, d3);
+        tmem_ld16(tr + 4 * kR, d4);
+        tmem_ld16(tr + 5 * kR, d5);
+        tmem_ld16(tr + 6 * kR, d6);
+        tmem_wait_ld();
+        release(sl);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const long long hi = (long long)d0[r] * 16777216LL + (long long)d1[r] * 65536LL +
+                               (long long)d2[r] * 256LL + (long long)d3[r];
+          const long long lo = (long long)d4[r] * 65536LL + (long long)d5[r] * 256LL + (long long)d6[r];
+          z[r] = fma((double)hi, 16777216.0, (double)lo);
+        }
+        return;
+      }
       // two TMEM round trips: digits 0-3 (the high part), then digits 4-6
       long long hi[16];
       {
