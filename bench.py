@@ -289,14 +289,18 @@ class Job:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(self.stream)
+        marks = []
         for _ in range(steps):
             step(True)
+            marks.append(torch.cuda.Event(enable_timing=True))
+            marks[-1].record(self.stream)
         e1.record(self.stream)
         torch.cuda.synchronize()
         if self.world > 1:
             dist.barrier()
         clk = clocks.stop() if clocks else None
         total_ms = e0.elapsed_time(e1)
+        each = [e0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, len(marks))]
         vals = multi.max_over_ranks([total_ms, statistics.mean(kern_ms),
                                      statistics.mean(t["int8_ms"] for t in timing),
                                      statistics.mean(t["fp64_ms"] for t in timing),
@@ -304,6 +308,7 @@ class Job:
                                      statistics.mean(create_ms)], dist, device="cuda")
         return {"ms_per_step": vals[0] / steps, "solve_block_ms": vals[1], "int8_ms": vals[2], "fp64_ms": vals[3],
                 "conv_ms": vals[4], "create_ms": vals[5], "paths": timing[-1]["paths"], "launches": launches[0],
+                "step_ms_rank": [round(x, 2) for x in each], "create_ms_rank": [round(x, 2) for x in create_ms],
                 "clocks": clk}
 
 
@@ -353,7 +358,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     # GLS_BENCH_DEVICE / GLS_BENCH_BACKEND: functional checks of the N > 1 code path with several ranks
-    # on one GPU over gloo (tools/gpu_*.sh); never used for a measurement
+    # on one GPU over gloo (tools/sessions/gpu_run13.sh); never used for a measurement
     local = int(os.environ.get("GLS_BENCH_DEVICE", multi.local_device()))
     torch.cuda.set_device(local)
     if world > 1:
@@ -550,7 +555,8 @@ def main():
                                "note": "SNPs / gls_solve_block time, gls_create excluded (SURVEY §8(d)'s timed "
                                        "region); value above includes gls_create every step"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": r["launches"],
-                "clocks": r["clocks"], "rank_deficient_rows": n_bad, "replication": replication, **subs}
+                "clocks": r["clocks"], "step_ms_rank0": r["step_ms_rank"], "create_ms_rank0": r["create_ms_rank"],
+                "rank_deficient_rows": n_bad, "replication": replication, **subs}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
