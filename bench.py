@@ -236,7 +236,7 @@ class Job:
         self.stream = torch.cuda.Stream()
         torch.cuda.set_stream(self.stream)
 
-    def make_ctx(self, Mx, XLx, yx):
+    def make_ctx(self, Mx, XLx, yx, async_create=False):
         cfg, pkg = self.cfg, self.pkg
         if self.args.replicate == "dist":
             # NEXT-3: the factorisation itself split over the ranks (column blocks of M and T, panel
@@ -248,7 +248,7 @@ class Job:
                    else pkg.Context(cfg.n, cfg.pL, cfg.pR, adopt=True))
             self.multi.replicate_shared(ctx, self.dist, src=0)
         else:
-            ctx = pkg.Context(cfg.n, cfg.pL, cfg.pR, Mx, XLx, yx)
+            ctx = pkg.Context(cfg.n, cfg.pL, cfg.pR, Mx, XLx, yx, async_create=async_create)
         return ctx
 
     def run(self, steps, warmup, path=None, clocks=None):
@@ -442,7 +442,10 @@ def main():
             sh = torch.empty(m_e, dtype=torch.int32, pin_memory=True)
 
             def one():
-                ctx = job.make_ctx(Mh, XLh, yh)
+                # gls_create_async: the first X_R chunks stream in while M is factored (the paper's
+                # first block load, otherwise exposed -- PAPER.md:723-728); the synchronous solve
+                # below resolves the create's outcome
+                ctx = job.make_ctx(Mh, XLh, yh, async_create=True)
                 ctx.set_stream_report(True)
                 solve(ctx, m_e, bh, sh)
                 rep = ctx.read_stream_report()
@@ -473,8 +476,9 @@ def main():
                "h2d_bytes_per_step": int((n * n + n * (pL + 1)) * 8 + m_i8 * pR * n),
                "d2h_bytes_per_step": int(m_i8 * p * 8 + m_i8 * 4),
                "m_per_rank": m_i8, "overlap": ov8,
-               "path": "C ABI gls_solve_block_i8: M, X_L, y (FP64) and X_R as int8 genotype codes in pinned "
-                       "host memory -> double-buffered H2D stream; b and status back to pinned host memory",
+               "path": "C ABI gls_create_async + gls_solve_block_i8: M, X_L, y (FP64) and X_R as int8 "
+                       "genotype codes in pinned host memory -> double-buffered H2D stream, its first chunks "
+                       "copied while M is factored; b and status back to pinned host memory",
                "bitwise_equal_to_device_run": same8}
         # FP64 X_R from host (8 bytes per genotype over PCIe): a SUBSET of the rank's SNPs (at most 250k,
         # 20 GB of pinned memory per rank at n = 1e4), 2 timed steps
@@ -494,7 +498,7 @@ def main():
                                   "h2d_bytes_per_step": int((n * n + n * (pL + 1) + m_f * pR * n) * 8),
                                   "d2h_bytes_per_step": int(m_f * p * 8 + m_f * 4), "overlap": ovf,
                                   "h2d_roofline_snps_per_s": H2D_GBS * 1e9 / (8.0 * n * pR),
-                                  "path": "C ABI gls_solve_block, FP64 X_R in pinned host memory",
+                                  "path": "C ABI gls_create_async + gls_solve_block, FP64 X_R in pinned host memory",
                                   "bitwise_equal_to_device_run": samef}
 
     if world > 1 and scaling == "strong" and not args.no_sub:

@@ -66,6 +66,22 @@ enum {
 int gls_create(int64_t n, int32_t pL, int32_t pR, const double* M, const double* X_L,
                const double* y, gls_ctx** out);
 
+/* gls_create_async -- gls_create without waiting for the factorisation (Alg. 8 lines 1-5 overlapped
+ * with the first async_read of line 7; §4.3 notes that the first block's load is
+ * otherwise not overlapped with computation).  Same arguments and the same
+ * resulting state, bit for bit.  Every step is enqueued on the context's stream and the call returns
+ * before it runs, so a following gls_solve_block* call can start streaming its host X_R block while
+ * M is still being factored (its H2D copies do not depend on the setup; its kernels do).
+ * Ownership: M, X_L, y are BORROWED until the first synchronising call on the context (a synchronous
+ * solve, gls_sync, gls_read_timing, gls_read_stream_report, gls_path_counts, gls_shared_view*,
+ * gls_destroy): the host copies read them in stream order.  Host pointers should be pinned.
+ * Errors: argument / dimension / allocation errors are returned here as by gls_create.  A non-SPD M
+ * is reported by the first synchronising call, which returns GLS_ERR_NOT_SPD (once) and puts the
+ * context in the failed state (gls_failed_pivot then holds the index); the b_out of solves enqueued
+ * before that call are undefined and must be discarded. */
+int gls_create_async(int64_t n, int32_t pL, int32_t pR, const double* M, const double* X_L,
+                     const double* y, gls_ctx** out);
+
 /* gls_solve_block -- solve m_blk consecutive problems (Alg. 5 line 3 and lines 7-11; Alg. 8 l.9-14).
  *   X_R   : n x (m_blk*pR) column-major, NOT modified (reading A9: the in-place X_R := L^{-1} X_R of
  *           the paper is never materialised).  Device pointer: read in place.  Host pointer:
@@ -163,7 +179,10 @@ int gls_read_timing(gls_ctx* ctx, double* ms_int8, double* ms_fp64, double* ms_c
  * summarises every chunk since the last read (in issue order), and resets:
  *   wall_ms          first chunk's H2D start -> last event
  *   h2d/compute/d2h  summed busy time of each engine
- *   first_load_ms    the first copy, which nothing can hide (§4.3 warm-up block)
+ *   first_load_ms    the part of the first copy the compute stream waited for: from the later of
+ *                    the copy's start and the end of the compute stream's earlier work (e.g. an
+ *                    asynchronous gls_create, which hides it) to the first chunk's compute
+ *                    (§4.3 warm-up block)
  *   exposed_h2d_ms   compute-stream idle time between chunks while the next X block was still in
  *                    flight (wait(current X_blk) exposed)
  *   exposed_other_ms the rest of the idle time between chunks (wait(previous b_blk), host gaps)

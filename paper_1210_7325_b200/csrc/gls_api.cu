@@ -93,6 +93,8 @@ struct gls_ctx {
   bool srep = false;
   struct ChunkRec {
     cudaEvent_t h0, h1, c0, c1, d0, d1;
+    cudaEvent_t cr;  // first chunk of a call: the compute stream done with its earlier work (e.g. an
+                     // asynchronous gls_create), before it waits for the chunk's data
     int64_t hbytes, dbytes;
   };
   std::vector<ChunkRec> srec;
@@ -110,6 +112,14 @@ struct gls_ctx {
   int32_t* sscratch = nullptr;
   int64_t scratch_groups = 0;
   int64_t launches = 0;
+  // gls_create_async: the factorisation is enqueued, not waited for; its NotSPD outcome (the device
+  // status, copied into the pinned hst by the stream) is resolved at the first synchronising call
+  bool create_pending = false;
+  CholStatus* hst = nullptr;            // pinned
+  cudaEvent_t ev_create = nullptr;      // after the whole setup and the status copy
+  // first-time workspace allocations: a stream with nothing queued, so allocating does not wait for
+  // the (possibly still running) factorisation on the context's stream
+  cudaStream_t alloc_stream = nullptr;
 };
 
 namespace {
@@ -182,9 +192,40 @@ cudaMemPool_t gls_device_pool(int device) {
   uint64_t keep = 32ull << 30;
   if (const char* e = getenv("GLS_POOL_KEEP_BYTES")) keep = strtoull(e, nullptr, 10);
   cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  // no hidden cross-stream waits: a workspace allocated on the idle alloc_stream while an
+  // asynchronous gls_create still runs must not be handed memory whose free is still pending on the
+  // context's stream (the allocation would then wait for the whole factorisation)
+  int no = 0;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
   cudaGetLastError();
   g_pool[device] = pool;
   return pool;
+}
+
+// Pinned host slots for the contexts' Cholesky status (CholStatus, 16 bytes each): cudaMallocHost
+// once per block of slots and never freed -- a cudaMallocHost / cudaFreeHost pair per context costs
+// driver round trips (cudaFreeHost may wait for the device) on every create / destroy.
+std::mutex g_slot_mu;
+std::vector<CholStatus*> g_free_slots;
+CholStatus* status_slot_get() {
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  if (g_free_slots.empty()) {
+    constexpr int kSlots = 256;
+    CholStatus* blk = nullptr;
+    if (cudaMallocHost((void**)&blk, kSlots * sizeof(CholStatus)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    for (int k = kSlots - 1; k >= 0; --k) g_free_slots.push_back(blk + k);
+  }
+  CholStatus* s = g_free_slots.back();
+  g_free_slots.pop_back();
+  return s;
+}
+void status_slot_put(CholStatus* s) {
+  if (!s) return;
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  g_free_slots.push_back(s);
 }
 
 cudaError_t gls_pool_alloc(void** p, size_t bytes, int device, cudaStream_t s) {
@@ -204,6 +245,15 @@ template <typename T>
 void dfree(gls_ctx* c, T*& p) {
   if (p) cudaFreeAsync(p, c->own_stream);
   p = nullptr;
+}
+// Workspace allocation usable from every stream on return, without waiting for work queued on the
+// context's streams (an asynchronous gls_create may still be running there): made on alloc_stream,
+// which carries nothing else.  Callers that replace an existing buffer synchronise the device first.
+template <typename T>
+cudaError_t walloc(gls_ctx* c, T** p, size_t bytes) {
+  cudaError_t e = gls_pool_alloc((void**)p, bytes, c->device, c->alloc_stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->alloc_stream);
+  return e;
 }
 
 int check_dims(int64_t n, int32_t pL, int32_t pR) {
@@ -228,6 +278,7 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR, bool fp64_state = tr
   CK(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->fb, cudaStreamNonBlocking));
+  CK(c, cudaStreamCreateWithFlags(&c->alloc_stream, cudaStreamNonBlocking));
   c->stream = c->own_stream;
   for (int k = 0; k < 2; ++k) {
     CK(c, cudaEventCreateWithFlags(&c->ev_oz[k], cudaEventDisableTiming));
@@ -283,7 +334,16 @@ void free_staging(gls_ctx* c) {
 }
 
 // Setup: Alg. 5 lines 1 (potrf), 2 + 4 (X~_L, y~), 5 (S_TL), 6 (b_T).
-int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
+void set_not_spd(gls_ctx* c, unsigned long long fail) {
+  c->failed_pivot = (int64_t)fail;
+  char buf[128];
+  snprintf(buf, sizeof buf, "M is not SPD: Cholesky pivot %lld <= 2^-52 * max diag", (long long)fail);
+  c->err = buf;
+}
+
+// async (gls_create_async): everything is enqueued on the context's stream and nothing is waited
+// for; the NotSPD outcome is resolved later by resolve_create.
+int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y, bool async = false) {
   const int64_t n = c->n;
   const int pL = c->pL;
   cudaStream_t s = c->stream;
@@ -291,7 +351,6 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   int* esc = nullptr;
   double* rmax = nullptr;  // row maxima of T (int8 setup scratch)
   CholStatus* st = nullptr;
-  CholStatus hst;
   int rc = GLS_OK;
   auto cleanup = [&]() {
     dfree(c, rmax);
@@ -329,6 +388,7 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   CKS(dalloc(c, &B, (size_t)n * (pL + 1) * sizeof(double)));
   CKS(dalloc(c, &W, (size_t)n * (pL + 1) * sizeof(double)));
   CKS(dalloc(c, &st, sizeof(CholStatus)));
+  if (!c->hst && !(c->hst = status_slot_get())) CKS(cudaErrorMemoryAllocation);  // status in and out
   if (c->oz_ok) {
     CKS(dalloc(c, &esc, (size_t)((n + kOzR - 1) / kOzR) * kOzR * sizeof(int)));
     CKS(dalloc(c, &rmax, (size_t)((n + kOzR - 1) / kOzR) * kOzR * sizeof(double)));
@@ -343,22 +403,28 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   if (m_host) {
     double mx = 0.0;
     for (int64_t k = 0; k < n; ++k) mx = std::fmax(mx, M[k + k * n]);
-    CholStatus h0;
-    h0.tol = std::ldexp(1.0, -52) * mx;
-    h0.fail = ULLONG_MAX;
-    CKS(cudaMemcpyAsync(st, &h0, sizeof h0, cudaMemcpyHostToDevice, s));
-    CKS(cudaStreamSynchronize(s));  // h0 lives on this stack frame; the allocations are in place too
+    c->hst->tol = std::ldexp(1.0, -52) * mx;
+    c->hst->fail = ULLONG_MAX;
+    CKS(cudaMemcpyAsync(st, c->hst, sizeof(CholStatus), cudaMemcpyHostToDevice, s));
+    {  // the h2d stream writes A: after its (stream-ordered) allocation
+      cudaEvent_t ea;
+      CKS(cudaEventCreateWithFlags(&ea, cudaEventDisableTiming));
+      col_ev.push_back(ea);
+      CKS(cudaEventRecord(ea, s));
+      CKS(cudaStreamWaitEvent(c->h2d, ea, 0));
+    }
+    const size_t ev0 = col_ev.size();
     const int64_t nch = (n + kUploadChunkCols - 1) / kUploadChunkCols;
-    col_ev.resize((size_t)nch);
+    col_ev.resize(ev0 + (size_t)nch);
     for (int64_t k = 0; k < nch; ++k) {
       const int64_t c0 = k * kUploadChunkCols, c1 = std::min(n, c0 + kUploadChunkCols);
-      CKS(cudaEventCreateWithFlags(&col_ev[(size_t)k], cudaEventDisableTiming));
+      CKS(cudaEventCreateWithFlags(&col_ev[ev0 + (size_t)k], cudaEventDisableTiming));
       CKS(cudaMemcpyAsync(A + c0 * n, M + c0 * n, (size_t)(c1 - c0) * n * sizeof(double), cudaMemcpyHostToDevice,
                           c->h2d));
-      CKS(cudaEventRecord(col_ev[(size_t)k], c->h2d));
+      CKS(cudaEventRecord(col_ev[ev0 + (size_t)k], c->h2d));
     }
     arriving.cols = kUploadChunkCols;
-    arriving.ready = col_ev.data();
+    arriving.ready = col_ev.data() + ev0;
     arriving.nchunks = nch;
     CKS(cudaMemsetAsync(T, 0, nn, s));
   } else {
@@ -371,18 +437,19 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
   if (m_host) CKS(cudaStreamWaitEvent(s, col_ev.back(), 0));  // M is the caller's again after return
   CKS(cudaGetLastError());
   mark("chol_inv");
-  CKS(cudaMemcpyAsync(&hst, st, sizeof hst, cudaMemcpyDeviceToHost, s));
-  CKS(cudaStreamSynchronize(s));
-  if (hst.fail != ULLONG_MAX) {
-    c->failed_pivot = (int64_t)hst.fail;
-    char buf[128];
-    snprintf(buf, sizeof buf, "M is not SPD: Cholesky pivot %lld <= 2^-52 * max diag",
-             (long long)hst.fail);
-    c->err = buf;
-    for (auto e : col_ev) cudaEventDestroy(e);
-    cleanup();
-    return GLS_ERR_NOT_SPD;
+  CKS(cudaMemcpyAsync(c->hst, st, sizeof(CholStatus), cudaMemcpyDeviceToHost, s));
+  if (!async) {
+    CKS(cudaStreamSynchronize(s));
+    if (c->hst->fail != ULLONG_MAX) {
+      set_not_spd(c, c->hst->fail);
+      for (auto e : col_ev) cudaEventDestroy(e);
+      cleanup();
+      return GLS_ERR_NOT_SPD;
+    }
   }
+  // (async: a failed factorisation leaves NaN / garbage in T; the setup below and any solve enqueued
+  // before resolve_create only compute on it -- no address depends on its values -- and their
+  // results are discarded when resolve_create reports GLS_ERR_NOT_SPD)
   // B = [X_L | y];  W = T B = [X~_L | y~];  G = W^T W  (S_TL and b_T)
   if (pL > 0) CKS(cudaMemcpyAsync(B, X_L, (size_t)n * pL * sizeof(double), cudaMemcpyDefault, s));
   CKS(cudaMemcpyAsync(B + (size_t)n * pL, y, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
@@ -405,24 +472,43 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y) {
     oz_setup(s, T, n, n, W, pL + 1, c->T8, c->aux, esc, B, c->V8, c->vscale, rmax, &c->launches);
   }
   CKS(cudaGetLastError());
-  CKS(cudaStreamSynchronize(s));
-  for (auto e : col_ev) cudaEventDestroy(e);
+  if (async) {
+    CKS(cudaEventCreateWithFlags(&c->ev_create, cudaEventDisableTiming));
+    CKS(cudaEventRecord(c->ev_create, s));
+    c->create_pending = true;
+  } else {
+    CKS(cudaStreamSynchronize(s));
+  }
+  for (auto e : col_ev) cudaEventDestroy(e);  // (pending events are released once they complete)
   mark("pack");
-  cleanup();
+  cleanup();  // stream-ordered frees on the context's stream
   mark("free");
 #undef CKS
   return GLS_OK;
 }
 
+// gls_create_async: wait for the enqueued setup; a failed factorisation puts the context in the
+// failed state and returns GLS_ERR_NOT_SPD (once -- later calls see GLS_ERR_STATE).
+int resolve_create(gls_ctx* c) {
+  if (!c->create_pending) return GLS_OK;
+  c->create_pending = false;
+  CK(c, cudaEventSynchronize(c->ev_create));
+  if (c->hst->fail != ULLONG_MAX) {
+    set_not_spd(c, c->hst->fail);
+    c->state = ST_FAILED;
+    return GLS_ERR_NOT_SPD;
+  }
+  return GLS_OK;
+}
+
 int ensure_scratch(gls_ctx* c, int64_t groups) {
   if (groups <= c->scratch_groups) return GLS_OK;
-  CK(c, cudaStreamSynchronize(c->stream));  // the old scratch may still be in use there
+  if (c->bscratch) CK(c, cudaStreamSynchronize(c->stream));  // the old scratch may still be in use there
   dfree(c, c->bscratch);
   dfree(c, c->sscratch);
   c->scratch_groups = 0;
-  CK(c, dalloc(c, &c->bscratch, (size_t)groups * c->p * sizeof(double)));
-  CK(c, dalloc(c, &c->sscratch, (size_t)groups * sizeof(int32_t)));
-  CK(c, cudaStreamSynchronize(c->own_stream));
+  CK(c, walloc(c, &c->bscratch, (size_t)groups * c->p * sizeof(double)));
+  CK(c, walloc(c, &c->sscratch, (size_t)groups * sizeof(int32_t)));
   c->scratch_groups = groups;
   return GLS_OK;
 }
@@ -431,16 +517,17 @@ int ensure_staging(gls_ctx* c, int64_t chunk_groups) {
   const int64_t cols = chunk_groups * c->pR;
   const int64_t ld = c->n + (c->n & 1);
   if (c->stage_cols >= cols && c->ld_stage == ld && c->bstage_groups >= chunk_groups) return GLS_OK;
-  CK(c, cudaDeviceSynchronize());
+  if (c->stage[0] || c->bstage[0]) CK(c, cudaDeviceSynchronize());  // old buffers may still be in use
   free_staging(c);
   for (int k = 0; k < 2; ++k) {
-    CK(c, dalloc(c, &c->stage[k], (size_t)ld * cols * sizeof(double)));
-    if (ld != c->n)  // the pad row of the odd-n staged copy must read as zero
-      CK(c, cudaMemsetAsync(c->stage[k], 0, (size_t)ld * cols * sizeof(double), c->own_stream));
-    CK(c, dalloc(c, &c->bstage[k], (size_t)chunk_groups * c->p * sizeof(double)));
-    CK(c, dalloc(c, &c->sstage[k], (size_t)chunk_groups * sizeof(int32_t)));
+    CK(c, walloc(c, &c->stage[k], (size_t)ld * cols * sizeof(double)));
+    if (ld != c->n) {  // the pad row of the odd-n staged copy must read as zero
+      CK(c, cudaMemsetAsync(c->stage[k], 0, (size_t)ld * cols * sizeof(double), c->alloc_stream));
+      CK(c, cudaStreamSynchronize(c->alloc_stream));
+    }
+    CK(c, walloc(c, &c->bstage[k], (size_t)chunk_groups * c->p * sizeof(double)));
+    CK(c, walloc(c, &c->sstage[k], (size_t)chunk_groups * sizeof(int32_t)));
   }
-  CK(c, cudaStreamSynchronize(c->own_stream));
   c->stage_cols = cols;
   c->ld_stage = ld;
   c->bstage_groups = chunk_groups;
@@ -516,12 +603,11 @@ int run_fp64(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b
 int ensure_x8(gls_ctx* c, int64_t cols) {
   const int64_t ld8 = (c->n + 15) & ~(int64_t)15;
   if (c->x8_cols >= cols && c->ld8 == ld8) return GLS_OK;
-  CK(c, cudaDeviceSynchronize());
+  if (c->x8[0]) CK(c, cudaDeviceSynchronize());
   dfree(c, c->x8[0]);
   dfree(c, c->x8[1]);
   c->x8_cols = 0;
-  for (int k = 0; k < 2; ++k) CK(c, dalloc(c, &c->x8[k], (size_t)ld8 * cols));
-  CK(c, cudaStreamSynchronize(c->own_stream));
+  for (int k = 0; k < 2; ++k) CK(c, walloc(c, &c->x8[k], (size_t)ld8 * cols));
   c->x8_cols = cols;
   c->ld8 = ld8;
   return GLS_OK;
@@ -531,11 +617,10 @@ int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* 
              const int* gate, const double* cv_X = nullptr, int64_t cv_ldx = 0, int64_t cv_cols = 0,
              int8_t* cv_X8 = nullptr, int* cv_flag = nullptr) {
   if (c->p > kOzPosvInKernelMaxP && c->sws_groups < groups) {
-    CK(c, cudaDeviceSynchronize());
+    if (c->sws) CK(c, cudaDeviceSynchronize());
     dfree(c, c->sws);
     c->sws_groups = 0;
-    CK(c, dalloc(c, &c->sws, (size_t)groups * c->pR * (c->p + 1) * sizeof(double)));
-    CK(c, cudaStreamSynchronize(c->own_stream));
+    CK(c, walloc(c, &c->sws, (size_t)groups * c->pR * (c->p + 1) * sizeof(double)));
     c->sws_groups = groups;
   }
   LaunchTimer lt(c, c->stream, 0);
@@ -645,12 +730,11 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
   int rc = ensure_x8(c, chunk_groups * pR);
   if (rc) return rc;
   if (c->cflags_cap < nchunks) {
-    CK(c, cudaDeviceSynchronize());
+    if (c->cflags) CK(c, cudaDeviceSynchronize());
     dfree(c, c->cflags);
     c->cflags_cap = 0;
     const int64_t cap = std::max<int64_t>(nchunks, 256);
-    CK(c, dalloc(c, &c->cflags, (size_t)cap * sizeof(int)));
-    CK(c, cudaStreamSynchronize(c->own_stream));
+    CK(c, walloc(c, &c->cflags, (size_t)cap * sizeof(int)));
     c->cflags_cap = cap;
   }
   // the flags of the previous block were last read by its FP64 launches, which the compute stream
@@ -727,6 +811,7 @@ int solve_streamed(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out, 
     rec.h1 = srep_mark(c, c->h2d);
     rec.hbytes = (int64_t)n * gc * pR * (int64_t)sizeof(double);
     CK(c, cudaEventRecord(c->ev_h2d[buf], c->h2d));
+    if (g0 == 0) rec.cr = srep_mark(c, c->stream);
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d[buf], 0));  // wait(current X_blk)
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_d2h[buf], 0));  // wait(previous b_blk) of this workspace
     rec.c0 = srep_mark(c, c->stream);
@@ -758,17 +843,16 @@ int solve_streamed(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out, 
 int ensure_stage8(gls_ctx* c, int64_t cols) {
   const int64_t ld8 = (c->n + 15) & ~(int64_t)15;
   if (c->stage8_cols >= cols && c->ld8 == ld8) return GLS_OK;
-  CK(c, cudaDeviceSynchronize());
+  if (c->stage8[0]) CK(c, cudaDeviceSynchronize());
   for (int k = 0; k < 2; ++k) {
     dfree(c, c->stage8[k]);
     dfree(c, c->raw8[k]);
   }
   c->stage8_cols = 0;
   for (int k = 0; k < 2; ++k) {
-    CK(c, dalloc(c, &c->stage8[k], (size_t)ld8 * cols));
-    if (ld8 != c->n) CK(c, dalloc(c, &c->raw8[k], (size_t)c->n * cols));
+    CK(c, walloc(c, &c->stage8[k], (size_t)ld8 * cols));
+    if (ld8 != c->n) CK(c, walloc(c, &c->raw8[k], (size_t)c->n * cols));
   }
-  CK(c, cudaStreamSynchronize(c->own_stream));
   c->stage8_cols = cols;
   c->ld8 = ld8;
   return GLS_OK;
@@ -788,14 +872,13 @@ int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, d
   if (!b_dev || (status_out && !s_dev)) {
     // the b / status staging of the double path, sized for these chunks
     if (c->bstage_groups < chunk_groups) {
-      CK(c, cudaDeviceSynchronize());
+      if (c->bstage[0]) CK(c, cudaDeviceSynchronize());
       for (int k = 0; k < 2; ++k) {
         dfree(c, c->bstage[k]);
         dfree(c, c->sstage[k]);
-        CK(c, dalloc(c, &c->bstage[k], (size_t)chunk_groups * p * sizeof(double)));
-        CK(c, dalloc(c, &c->sstage[k], (size_t)chunk_groups * sizeof(int32_t)));
+        CK(c, walloc(c, &c->bstage[k], (size_t)chunk_groups * p * sizeof(double)));
+        CK(c, walloc(c, &c->sstage[k], (size_t)chunk_groups * sizeof(int32_t)));
       }
-      CK(c, cudaStreamSynchronize(c->own_stream));
       c->bstage_groups = chunk_groups;
     }
   }
@@ -820,6 +903,7 @@ int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, d
     rec.h1 = srep_mark(c, c->h2d);
     rec.hbytes = (int64_t)n * gc * pR;
     CK(c, cudaEventRecord(c->ev_h2d[buf], c->h2d));
+    if (g0 == 0) rec.cr = srep_mark(c, c->stream);
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d[buf], 0));  // wait(current X_blk)
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_d2h[buf], 0));  // wait(previous b_blk) of this workspace
     rec.c0 = srep_mark(c, c->stream);
@@ -852,12 +936,14 @@ int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, d
   return GLS_OK;
 }
 
+// Every synchronising entry point ends here: all of the context's streams drained, and the outcome
+// of an asynchronous gls_create resolved (GLS_ERR_NOT_SPD once if the factorisation failed).
 int sync_all(gls_ctx* c) {
   CK(c, cudaStreamSynchronize(c->h2d));
   CK(c, cudaStreamSynchronize(c->fb));
   CK(c, cudaStreamSynchronize(c->stream));
   CK(c, cudaStreamSynchronize(c->d2h));
-  return GLS_OK;
+  return resolve_create(c);
 }
 
 }  // namespace
@@ -895,6 +981,24 @@ int gls_create(int64_t n, int32_t pL, int32_t pR, const double* M, const double*
   return GLS_OK;
 }
 
+int gls_create_async(int64_t n, int32_t pL, int32_t pR, const double* M, const double* X_L,
+                     const double* y, gls_ctx** out) {
+  if (!out) return GLS_ERR_ARG;
+  *out = nullptr;
+  if (!M || !y || (pL > 0 && !X_L)) return GLS_ERR_ARG;
+  int rc = check_dims(n, pL, pR);
+  if (rc) return rc;
+  gls_ctx* c = new gls_ctx();
+  *out = c;
+  rc = ctx_init(c, n, pL, pR);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  rc = ctx_setup(c, M, X_L, y, true);
+  if (rc) return rc;
+  c->state = ST_OK;  // tentatively: resolve_create (any synchronising call) may still fail it
+  return GLS_OK;
+}
+
 int gls_create_adopt(int64_t n, int32_t pL, int32_t pR, gls_ctx** out) {
   if (!out) return GLS_ERR_ARG;
   *out = nullptr;
@@ -927,6 +1031,11 @@ int gls_shared_view_ex(gls_ctx* c, int32_t flags, void** ptrs, int64_t* bytes, i
   if (c->state == ST_FAILED) return GLS_ERR_STATE;
   const bool fp64 = c->fp64_ok && !(flags & GLS_SHARE_INT8_ONLY);
   if (!fp64 && !c->oz_ok) return GLS_ERR_STATE;
+  if (c->create_pending) {  // the views are read by the caller's collectives: the setup must be done
+    DeviceGuard g(c->device);
+    const int rc = sync_all(c);
+    if (rc) return rc;
+  }
   int k = 0;
   if (fp64) {
     ptrs[k] = c->Tpk;
@@ -1119,7 +1228,9 @@ int gls_read_stream_report(gls_ctx* c, gls_stream_report* r) {
         end = std::max(end, d1);
       }
       if (j == 0) {
-        r->first_load_ms = c0 - h0;
+        // the part of the first load the compute stream waited for: from when it was free (after
+        // the work queued before this call, e.g. an asynchronous gls_create) or the copy's start
+        r->first_load_ms = std::max(0.0, c0 - std::max(h0, x.cr ? at(x.cr) : h0));
       } else {
         // the compute stream's idle time between chunk j-1 and chunk j: the part before chunk j's
         // data had arrived waited at wait(current X_blk), the rest at wait(previous b_blk)
@@ -1134,7 +1245,7 @@ int gls_read_stream_report(gls_ctx* c, gls_stream_report* r) {
     r->wall_ms = end;
     r->chunks = (int64_t)c->srec.size();
     for (auto& x : c->srec)
-      for (cudaEvent_t e : {x.h0, x.h1, x.c0, x.c1, x.d0, x.d1})
+      for (cudaEvent_t e : {x.h0, x.h1, x.c0, x.c1, x.d0, x.d1, x.cr})
         if (e) c->ev_pool.push_back(e);
     c->srec.clear();
   }
@@ -1227,6 +1338,9 @@ void gls_destroy(gls_ctx* c) {
     if (c->ev_oz[k]) cudaEventDestroy(c->ev_oz[k]);
     if (c->ev_fb[k]) cudaEventDestroy(c->ev_fb[k]);
   }
+  if (c->ev_create) cudaEventDestroy(c->ev_create);
+  status_slot_put(c->hst);
+  if (c->alloc_stream) cudaStreamDestroy(c->alloc_stream);
   if (c->fb) cudaStreamDestroy(c->fb);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   if (c->h2d) cudaStreamDestroy(c->h2d);

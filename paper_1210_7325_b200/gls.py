@@ -54,7 +54,7 @@ class StreamReport(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 ABI_SYMBOLS = (
-    "gls_create", "gls_solve_block", "gls_solve_block_ex", "gls_sync", "gls_set_stream",
+    "gls_create", "gls_create_async", "gls_solve_block", "gls_solve_block_ex", "gls_sync", "gls_set_stream",
     "gls_set_block_cols", "gls_destroy", "gls_failed_pivot", "gls_last_error",
     "gls_error_string", "gls_create_adopt", "gls_shared_view", "gls_commit_shared",
     "gls_kernel_launches", "gls_set_path", "gls_path_counts", "gls_solve_block_i8",
@@ -91,6 +91,8 @@ def load(build_if_missing: bool = True):
     vp, i64, i32, dp = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
     L.gls_create.argtypes = [i64, i32, i32, dp, dp, dp, ctypes.POINTER(vp)]
     L.gls_create.restype = ctypes.c_int
+    L.gls_create_async.argtypes = [i64, i32, i32, dp, dp, dp, ctypes.POINTER(vp)]
+    L.gls_create_async.restype = ctypes.c_int
     L.gls_create_adopt.argtypes = [i64, i32, i32, ctypes.POINTER(vp)]
     L.gls_create_adopt.restype = ctypes.c_int
     L.gls_solve_block.argtypes = [vp, dp, i64, dp]
@@ -235,10 +237,12 @@ def error_string(code: int) -> str:
 
 
 class Context:
-    """gls_ctx wrapper.  Context(n, pL, pR, M, X_L, y) runs gls_create on the current device."""
+    """gls_ctx wrapper.  Context(n, pL, pR, M, X_L, y) runs gls_create on the current device;
+    async_create=True runs gls_create_async (M, X_L, y are kept referenced until the first
+    synchronising call; a non-SPD M raises there)."""
 
     def __init__(self, n: int, pL: int, pR: int, M=None, X_L=None, y=None, adopt: bool = False,
-                 int8_only: bool = False, _handle=None):
+                 int8_only: bool = False, _handle=None, async_create: bool = False):
         L = load()
         self._lib = L
         self.n, self.pL, self.pR, self.p = n, pL, pR, pL + pR
@@ -254,9 +258,11 @@ class Context:
         elif adopt:
             rc = L.gls_create_adopt(n, pL, pR, ctypes.byref(h))
         else:
-            rc = L.gls_create(n, pL, pR, _ptr(M), _ptr(X_L) if pL > 0 else None, _ptr(y), ctypes.byref(h))
+            create = L.gls_create_async if async_create else L.gls_create
+            rc = create(n, pL, pR, _ptr(M), _ptr(X_L) if pL > 0 else None, _ptr(y), ctypes.byref(h))
         self._h = h
         self.failed_pivot = -1
+        self._borrowed = (M, X_L, y) if async_create else None  # read in stream order until synchronised
         if rc != GLS_OK:
             msg = error_string(rc)
             if h.value:
@@ -269,6 +275,8 @@ class Context:
     # -- helpers
     def _check(self, rc: int):
         if rc != GLS_OK:
+            if rc == GLS_ERR_NOT_SPD:  # an asynchronous create's factorisation failed
+                self.failed_pivot = self._lib.gls_failed_pivot(self._h)
             raise GLSError(rc, error_string(rc) + " -- " + self._lib.gls_last_error(self._h).decode())
 
     def solve_block(self, X_R, m_blk: int, b_out, status_out=None, async_: bool = False):

@@ -765,3 +765,70 @@ def test_gwfgls_rung_matches_oracle(glsmod, n, pL, pR, m):
         assert g.kernel_launches > 0
         with pytest.raises(glsmod.GLSError):
             g.solve(dev(XR), 0, torch.empty((1, pL + pR), dtype=torch.float64, device="cuda"))
+
+
+@pytest.mark.parametrize("n", [1100, 4100])
+def test_create_async_bitwise(glsmod, n):
+    """gls_create_async (Alg. 8 lines 1-5 overlapped with the first block's H2D): the same shared state
+    and the same b bit for bit as gls_create, with M / X_L / y pinned on the host and a host X_R block
+    (codes and FP64) streamed while the factorisation may still run; and against the oracle."""
+    from paper_1210_7325_b200 import multi
+    pL, pR, m = 3, 1, 700
+    P = gen.make_problem(n, pL, pR, seed=61)
+    XR = gen.make_XR(61, n, 0, m)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    Mh, XLh, yh = pin(P.M), pin(P.XL), pin(P.y)
+    G = pin(XR.astype(np.int8))
+    Xh = pin(XR)
+    with glsmod.Context(n, pL, pR, Mh, XLh, yh) as ref:
+        dig_ref = multi.shared_state_digest(ref)
+        b_ref = torch.empty((m, pL + pR), dtype=torch.float64, pin_memory=True)
+        ref.solve_block_i8(G, m, b_ref)
+        b_ref64 = torch.empty((m, pL + pR), dtype=torch.float64, pin_memory=True)
+        ref.solve_block(Xh, m, b_ref64)
+    for entry in ("i8", "f64", "sync"):
+        with glsmod.Context(n, pL, pR, Mh, XLh, yh, async_create=True) as ctx:
+            b = torch.empty((m, pL + pR), dtype=torch.float64, pin_memory=True)
+            st = torch.empty(m, dtype=torch.int32, pin_memory=True)
+            if entry == "i8":
+                ctx.solve_block_i8(G, m, b, st)         # synchronous: resolves the create at its end
+            elif entry == "f64":
+                ctx.solve_block(Xh, m, b, st, async_=True)
+                ctx.sync()
+            else:
+                ctx.sync()
+                ctx.solve_block(Xh, m, b, st)
+            np.testing.assert_array_equal(b.numpy(), (b_ref if entry == "i8" else b_ref64).numpy())
+            assert multi.shared_state_digest(ctx) == dig_ref
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, pR)
+    assert_parity(b_ref.numpy(), st.numpy(), b_or, st_or, label="create_async n=%d" % n)
+
+
+def test_create_async_not_spd(glsmod):
+    """A non-SPD M under gls_create_async: the create returns OK, the first synchronising call reports
+    GLS_ERR_NOT_SPD with the oracle's pivot, the context is failed afterwards, destroy is clean."""
+    import ctypes
+    n, piv = 1100, 777
+    P = gen.make_problem(n, 3, 1, seed=62)
+    M = P.M.copy()
+    M[piv, piv] = -1.0
+    with pytest.raises(oracle.NotSPD) as ei:
+        oracle.cholesky(M)
+    assert ei.value.pivot == piv
+    L = glsmod.load()
+    Mh = torch.from_numpy(M).pin_memory()
+    XLd, yd = dev(P.XL), dev(P.y)
+    G = torch.from_numpy(gen.make_XR(62, n, 0, 50).astype(np.int8)).pin_memory()
+    b = torch.empty((50, 4), dtype=torch.float64, pin_memory=True)
+    h = ctypes.c_void_p()
+    assert L.gls_create_async(n, 3, 1, Mh.data_ptr(), XLd.data_ptr(), yd.data_ptr(), ctypes.byref(h)) == 0
+    assert L.gls_solve_block_i8(h, G.data_ptr(), n, 50, b.data_ptr(), None, 1) == 0   # enqueued
+    assert L.gls_sync(h) == 3                                                          # GLS_ERR_NOT_SPD
+    assert L.gls_failed_pivot(h) == piv
+    assert L.gls_sync(h) == 0 and L.gls_solve_block_i8(h, G.data_ptr(), n, 50, b.data_ptr(), None, 0) == 6
+    L.gls_destroy(h)
+    # the same through the binding: the synchronous solve raises, with the pivot on the context
+    with glsmod.Context(n, 3, 1, Mh, XLd, yd, async_create=True) as ctx:
+        with pytest.raises(glsmod.GLSError) as eg:
+            ctx.solve_block_i8(G, 50, b)
+        assert eg.value.code == 3 and ctx.failed_pivot == piv
