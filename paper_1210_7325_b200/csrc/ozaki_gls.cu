@@ -264,6 +264,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // region-0 MMAs queue behind that tail.  Measured ~+1 % on configs 2 and 3 (for the 21-accumulator
   // variants only since their epilogue stopped being the bottleneck).
   constexpr bool kSplit = true;
+#ifndef GLS_OZ_HOLD
+#define GLS_OZ_HOLD (ST - 1)
+#endif
+  // stages the MMA issuer may hold for deferred region-1 MMAs: fewer leave more stages to prefetch into
+  // but widen the TMEM hand-over bubbles (A/B: profiles/r02_ab_hold.txt -- ST - 1 is fastest)
+  constexpr int kHold = GLS_OZ_HOLD;
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
@@ -365,7 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
             issue(stage, k, 0, idesc);
             if (k == nc - 1 && (kSplit || !two)) mma_commit_pair_mc(&tfull[0], 3);  // region 0 complete
-            const bool hold = two && (!r1 || (kSplit && k >= nc - (ST - 1)));
+            const bool hold = two && (!r1 || (kSplit && k >= nc - kHold));
             if (!hold) {
               if (two) issue(stage, k, 1, idesc);
               mma_commit_pair_mc(&empty[stage], 3);
@@ -374,8 +380,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 dstage = stage;
                 dk = k;
               }
-              const bool late = kSplit && k >= nc - (ST - 1);  // the tail: flush only when forced
-              if (ndef == ST - 1 || k == nc - 1 || (!late && mbar_test(&tempty[1], (u1 & 1) ^ 1))) {
+              const bool late = kSplit && k >= nc - kHold;  // the tail: flush only when forced
+              if (ndef == kHold || k == nc - 1 || (!late && mbar_test(&tempty[1], (u1 & 1) ^ 1))) {
                 if (!r1) {
                   timed_wait(&tempty[1], (u1++ & 1) ^ 1, pt);
                   tc_fence_after();
