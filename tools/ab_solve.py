@@ -1,5 +1,6 @@
 """A/B timing of the config-2 solve with a given libgls.so (diagnostics): only symbols every round-1
-build exports.  usage: python tools/ab_solve.py LIB [m] [config]"""
+build exports.  usage: python tools/ab_solve.py LIB [m] [config] [i8]   (i8: X_R as int8 genotype codes
+in HBM through gls_solve_block_i8 -- no conversion, no convert-ahead)"""
 import ctypes, os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -28,6 +29,13 @@ for c in range(0, m * pR, 65536):
     k = min(65536, m * pR - c)
     g.gen_xr_device(gen.DEFAULT_SEED, n, c, k, X[c:c + k])
 b = torch.empty((m, pL + pR), dtype=torch.float64, device="cuda")
+codes = len(sys.argv) > 4 and sys.argv[4] == "i8"
+if codes:
+    G = torch.empty((m * pR, n), dtype=torch.int8, device="cuda")
+    for c in range(0, m * pR, 65536):
+        G[c:c + 65536].copy_(X[c:c + 65536].to(torch.int8))
+    del X
+    lib.gls_solve_block_i8.argtypes = [vp, vp, i64, i64, vp, vp, ctypes.c_int]
 s = torch.cuda.Stream()
 for rep in range(4):
     h = vp()
@@ -37,7 +45,10 @@ for rep in range(4):
     t1 = time.perf_counter()
     lib.gls_set_stream(h, s.cuda_stream)
     lib.gls_set_timing(h, 1)
-    assert lib.gls_solve_block_ex(h, X.data_ptr(), m, b.data_ptr(), None, 0) == 0
+    if codes:
+        assert lib.gls_solve_block_i8(h, G.data_ptr(), n, m, b.data_ptr(), None, 0) == 0
+    else:
+        assert lib.gls_solve_block_ex(h, X.data_ptr(), m, b.data_ptr(), None, 0) == 0
     t2 = time.perf_counter()
     a, bb, c, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
     lib.gls_read_timing(h, ctypes.byref(a), ctypes.byref(bb), ctypes.byref(c), ctypes.byref(k))
