@@ -832,3 +832,29 @@ def test_create_async_not_spd(glsmod):
         with pytest.raises(glsmod.GLSError) as eg:
             ctx.solve_block_i8(G, 50, b)
         assert eg.value.code == 3 and ctx.failed_pivot == piv
+
+
+def test_create_bitwise_independent_of_schedule(glsmod):
+    """The create's shared state (T digits, packed T, aux, V digits, G) is bit-for-bit the same under
+    every scheduling switch of the factorisation: TMA GEMM tile order (cost-ordered snake vs
+    round-robin), look-ahead products after vs beside the main stream, the free-SM budget of the
+    off-critical-path products -- no result depends on which CTA or stream ran a tile first.  Each
+    setting runs in its own process (the switches are read once per process)."""
+    import json, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, json, numpy as np, torch; sys.path.insert(0, %r); import gen; "
+            "import paper_1210_7325_b200 as pkg; from paper_1210_7325_b200 import multi; out = {}\n"
+            "for n in (1500, 4097):\n"
+            "    P = gen.make_problem(n, 3, 1)\n"
+            "    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()\n"
+            "    with pkg.Context(n, 3, 1, d(P.M), d(P.XL), d(P.y)) as c: out[n] = multi.shared_state_digest(c)\n"
+            "print(json.dumps(out))" % root)
+    runs = {}
+    for name, env in [("default", {}), ("round_robin", {"GLS_DGEMM_SCHED": "0"}),
+                      ("side_concurrent", {"GLS_SIDE_AFTER": "0"}), ("free48", {"GLS_CHOL_FREE_SMS": "48"})]:
+        r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        runs[name] = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, dg in runs.items():
+        assert dg == runs["default"], name
