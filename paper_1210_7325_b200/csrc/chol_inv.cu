@@ -663,6 +663,7 @@ __global__ void __launch_bounds__(blk::THREADS) chol_inv_leaf128(int nb, double*
 constexpr int kMaxDepth = 24;
 constexpr int64_t kLookaheadMin = 1024;  // smallest trailing node split for look-ahead
 constexpr int kFreeSms = 16;             // SMs the off-critical-path GEMMs leave free
+constexpr int kFreeSmsY = 48;            // ... the aux-stream Y products
 struct RecCtx {
   cudaStream_t s;
   cudaStream_t side[kMaxDepth], aux[kMaxDepth];
@@ -673,6 +674,7 @@ struct RecCtx {
   CholStatus* st;
   int64_t* lc;
   int off_ctas;  // grid cap of the off-critical-path GEMMs (look-ahead and Y; 0: none)
+  int off_side, off_aux;  // per stream kind (A/B: GLS_CAP_SIDE / GLS_CAP_AUX, SMs)
   const ColsReady* arriving;  // nullable: A's columns still being uploaded
 };
 
@@ -806,14 +808,14 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
     static const bool after = !(getenv("GLS_SIDE_AFTER") && atoi(getenv("GLS_SIDE_AFTER")) == 0);
     cudaStreamWaitEvent(sd, after ? record(rc, s) : e_start, 0);
     dgemm(sd, h2 - g, h1, h1, 1.0, A21 + g, ld, 'N', T11, ld, 'T', 0.0, T21 + g, ld, GEMM_KMAX_COL, rc.lc,
-          rc.ws_side[d], rc.off_ctas);
+          rc.ws_side[d], rc.off_side);
     cudaStreamWaitEvent(sd, e_top, 0);
     wait_cols(rc, sd, goff + n);
     // rows [g, h2) of the lower triangle: columns [0, g) full, [g, h2) lower
     dgemm(sd, h2 - g, g, h1, -1.0, T21 + g, ld, 'N', T21, ld, 'T', 1.0, A22 + g, ld, 0, rc.lc, rc.ws_side[d],
-          rc.off_ctas);
+          rc.off_side);
     dgemm(sd, h2 - g, h2 - g, h1, -1.0, T21 + g, ld, 'N', T21 + g, ld, 'T', 1.0, A22 + g + g * ld, ld,
-          GEMM_LOWER_C, rc.lc, rc.ws_side[d], rc.off_ctas);
+          GEMM_LOWER_C, rc.lc, rc.ws_side[d], rc.off_side);
     e_rest = record(rc, sd);
   }
   // Y = L21 T11 -> A21's place, on the aux stream (after every read of A21 and every write of L21)
@@ -821,7 +823,7 @@ void chol_inv_rec(RecCtx& rc, int64_t n, double* A, double* T, int64_t ld, int64
   cudaStreamWaitEvent(sa, record(rc, s), 0);
   if (e_rest) cudaStreamWaitEvent(sa, e_rest, 0);
   dgemm(sa, h2, h1, h1, 1.0, T21, ld, 'N', T11, ld, 'N', 0.0, A21, ld, GEMM_KMIN_COL, rc.lc, rc.ws_aux[d],
-        rc.off_ctas);
+        rc.off_aux);
   cudaEvent_t e_y = record(rc, sa);
   chol_inv_rec(rc, h2, A22, T22, ld, goff + h1, e_rest, depth + 1);
   // T21 = -T22 Y  (overwrites L21: Y, and with it every reader of L21, must be complete)
@@ -861,6 +863,13 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev0);
     static const int freeq = getenv("GLS_CHOL_FREE_SMS") ? atoi(getenv("GLS_CHOL_FREE_SMS")) : kFreeSms;
     rc.off_ctas = freeq > 0 && sms > freeq ? 2 * (sms - freeq) : 0;  // 2 CTAs per SM
+    static const int cap_side = getenv("GLS_CAP_SIDE") ? atoi(getenv("GLS_CAP_SIDE")) : 0;
+    static const int cap_aux = getenv("GLS_CAP_AUX") ? atoi(getenv("GLS_CAP_AUX")) : 0;
+    // Y (aux) leaves 48 SMs: it often runs beside a look-ahead product of a deeper level, and two capped
+    // persistent products together had taken every SM from the main stream (A/B over side / aux caps:
+    // profiles/r02_create_caps_ab.txt -- 132 / 100 SMs best, 25.8 vs 26.2 ms at n = 1e4)
+    rc.off_side = cap_side > 0 ? 2 * cap_side : rc.off_ctas;
+    rc.off_aux = cap_aux > 0 ? 2 * cap_aux : (freeq > 0 && sms > kFreeSmsY ? 2 * (sms - kFreeSmsY) : 0);
   }
   // split-K workspaces (main + side and aux per depth) from the stream-ordered pool
   double* ws = nullptr;
