@@ -502,7 +502,10 @@ cudaError_t launch_variant(cudaStream_t s, const CUtensorMap& map, const KParams
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::bytes);
     if (e != cudaSuccess) return e;
   }
-  const int64_t grid = kp.num_panels < num_sms ? kp.num_panels : num_sms;
+  int64_t grid = kp.num_panels < num_sms ? kp.num_panels : num_sms;
+  // GLS_FP64_CTAS (tests): a smaller persistent grid -- another panel schedule, the same bits
+  static const int ctas_cap = getenv("GLS_FP64_CTAS") ? atoi(getenv("GLS_FP64_CTAS")) : 0;
+  if (ctas_cap > 0 && ctas_cap < grid) grid = ctas_cap;
   fused_trsm_gls_kernel<NW, FULL, ALIGNED><<<(unsigned)grid, kThreads, C::bytes, s>>>(map, kp);
   return cudaGetLastError();
 }

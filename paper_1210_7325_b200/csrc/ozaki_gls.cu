@@ -988,7 +988,11 @@ cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& xmap, const CUt
     cudaGetLastError();
     max_pairs_dev[dev] = mp;
   }
-  const int max_pairs = max_pairs_dev[dev] > 0 ? max_pairs_dev[dev] : num_sms / 2;
+  int max_pairs = max_pairs_dev[dev] > 0 ? max_pairs_dev[dev] : num_sms / 2;
+  // GLS_OZ_PAIRS (tests): fewer CTA pairs than the machine holds -- a different tile-to-pair schedule and
+  // different timing, under which the results must not change by a bit
+  static const int pairs_cap = getenv("GLS_OZ_PAIRS") ? atoi(getenv("GLS_OZ_PAIRS")) : 0;
+  if (pairs_cap > 0 && pairs_cap < max_pairs) max_pairs = pairs_cap;
   const int need = (kp.num_tiles + 1) / 2;
   const int np = need < max_pairs ? need : max_pairs;
   kern<<<2 * np, kThreads, smem, s>>>(xmap, tmap, vmap, kp);

@@ -858,3 +858,46 @@ def test_create_bitwise_independent_of_schedule(glsmod):
         runs[name] = json.loads(r.stdout.strip().splitlines()[-1])
     for name, dg in runs.items():
         assert dg == runs["default"], name
+
+
+def test_hot_kernels_bitwise_under_perturbation(glsmod):
+    """Race evidence without a race detector (compute-sanitizer is closed on this pool): the int8
+    tcgen05 kernel (mbarrier rings, TMEM hand-over between the MMA issuer and the epilogue, the CTA
+    pair's remote arrivals, the convert-ahead warps) and the FP64 DMMA kernel give the same bits when
+    their timing is perturbed -- fewer CTA pairs / CTAs (another tile schedule), in-kernel clock
+    counters on (GLS_OZ_PROF), and a concurrent GEMM load on another stream competing for the SMs.
+    A missing wait or a premature release would show up as a changed bit in some run."""
+    import json, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    # n >= 4096 so the convert-ahead warps run; 3 chunks of tiles plus a ragged tail
+    code = ("import sys, hashlib, numpy as np, torch; sys.path.insert(0, %r); import gen; "
+            "import paper_1210_7325_b200 as pkg\n"
+            "n, m = 4100, 3 * 18944 + 77\n"
+            "P = gen.make_problem(n, 3, 1, seed=71)\n"
+            "d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()\n"
+            "X = torch.empty((m, n), dtype=torch.float64, device='cuda')\n"
+            "pkg.gen_xr_device(71, n, 0, m, X)\n"
+            "load = sys.argv[1] == 'load'\n"
+            "if load:\n"
+            "    s2 = torch.cuda.Stream(); a = torch.randn(8192, 8192, device='cuda')\n"
+            "out = []\n"
+            "with pkg.Context(n, 3, 1, d(P.M), d(P.XL), d(P.y)) as c:\n"
+            "    for path in (pkg.GLS_PATH_AUTO, pkg.GLS_PATH_FP64):\n"
+            "        c.set_path(path)\n"
+            "        b = torch.empty((m, 4), dtype=torch.float64, device='cuda')\n"
+            "        if load:\n"
+            "            with torch.cuda.stream(s2):\n"
+            "                for _ in range(30): a = a @ a; a /= a.abs().max()\n"
+            "        c.solve_block(X, m, b)\n"
+            "        out.append(hashlib.sha256(b.cpu().numpy().tobytes()).hexdigest())\n"
+            "print(' '.join(out))" % root)
+    runs = {}
+    for name, env, arg in [("default", {}, "-"), ("pairs7", {"GLS_OZ_PAIRS": "7", "GLS_FP64_CTAS": "13"}, "-"),
+                           ("prof", {"GLS_OZ_PROF": "1"}, "-"), ("load", {}, "load"),
+                           ("pairs33_load", {"GLS_OZ_PAIRS": "33", "GLS_FP64_CTAS": "61"}, "load")]:
+        r = subprocess.run([sys.executable, "-c", code, arg], env={**os.environ, **env}, capture_output=True,
+                           text=True, timeout=900)
+        assert r.returncode == 0, (name, r.stderr[-2000:])
+        runs[name] = r.stdout.strip().splitlines()[-1].split()
+    for name, h in runs.items():
+        assert h == runs["default"], (name, h, runs["default"])
