@@ -901,3 +901,32 @@ def test_hot_kernels_bitwise_under_perturbation(glsmod):
         runs[name] = r.stdout.strip().splitlines()[-1].split()
     for name, h in runs.items():
         assert h == runs["default"], (name, h, runs["default"])
+
+
+def test_large_n_planted_beta(glsmod):
+    """Maximum-size check far above the configs: n = 49 999 (odd, so every tile, chunk and 16-byte
+    pitch is ragged; 1563 row blocks of the int8 digit tiles, int32 digit sums up to 127 * 2 * n),
+    noise-free y = X_L beta.  No oracle can factor this M in a test's time, so the pin is the
+    planted-beta identity b_i = (beta, 0) (PAPER.md:28-39 with y in span(X_L)), on both arithmetic
+    paths: the int8 tcgen05 path on three chunks of SNPs plus a ragged tail, the FP64 DMMA path on a
+    subset."""
+    n, pL, pR = 49_999, 3, 1
+    m = 2 * 18944 + 333
+    P = gen.make_problem(n, pL, pR, seed=81, noise=0.0)
+    Xd = torch.empty((m * pR, n), dtype=torch.float64, device="cuda")
+    glsmod.gen_xr_device(81, n, 0, m * pR, Xd)
+    ref = np.concatenate([P.beta_L, [0.0]])
+    scale = np.max(np.abs(P.beta_L))
+    with glsmod.Context(n, pL, pR, dev(P.M), dev(P.XL), dev(P.y)) as ctx:
+        for path, mm in ((glsmod.GLS_PATH_AUTO, m), (glsmod.GLS_PATH_FP64, 2000)):
+            ctx.set_path(path)
+            b = torch.empty((mm, pL + pR), dtype=torch.float64, device="cuda")
+            st = torch.empty(mm, dtype=torch.int32, device="cuda")
+            ctx.solve_block(Xd, mm, b, st)
+            counts = ctx.path_counts()
+            b, st = b.cpu().numpy(), st.cpu().numpy()
+            assert np.all(st == 0)
+            err = float(np.max(np.abs(b - ref)) / scale)
+            assert err <= 1e-9, (path, err)
+            if path == glsmod.GLS_PATH_AUTO:
+                assert counts[0] > 0, counts  # the int8 kernel did the work
