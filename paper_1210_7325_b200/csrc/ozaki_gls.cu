@@ -72,6 +72,10 @@ constexpr int kConvWarps = 2;  // convert-ahead warps: FP64 -> int8 of the NEXT 
 constexpr int kThreads = (2 + kEpiWarps + kConvWarps) * 32;
 constexpr int kCvBuf = 8192;          // bytes per convert-ahead staging buffer (two per conv warp)
 constexpr int kCvRows = kCvBuf / 8;   // X rows per piece
+#ifndef GLS_OZ_CV_HINT
+#define GLS_OZ_CV_HINT 1
+#endif
+constexpr bool kCvHint = GLS_OZ_CV_HINT != 0;  // L2 evict_first hints on the convert-ahead traffic
 constexpr uint32_t kTmemCols = 512;
 // TMEM column pair of double w in the epilogue hand-over scratch: columns MMAs never write
 __device__ __forceinline__ uint32_t xcol(int w) { return w < 16 ? 224 + 2 * w : 480 + 2 * (w - 16); }
@@ -667,6 +671,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int64_t units = kp.cv_cols * ppc;
     uint8_t* const buf0 = cvbuf + (size_t)cw * 2 * kCvBuf;
     uint64_t* const bar0 = cvbar + 2 * cw;
+    // the FP64 source is read once and the int8 copy is next read a launch later: both L2::evict_first,
+    // so this stream does not push the pinned X panels and the digit tiles out of L2
+    const uint64_t pol_once = policy_evict_first();
     auto piece = [&](int64_t u, int64_t& c, int64_t& r0, int& rows) {
       c = u / ppc;
       r0 = (u - c * ppc) * kCvRows;
@@ -680,7 +687,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (lane == 0) {
         if (bytes) {
           mbar_arrive_expect_tx(&bar0[b], bytes);
-          bulk_g2s(buf0 + b * kCvBuf, kp.cv_X + c * kp.cv_ldx + r0, bytes, &bar0[b]);
+          if (kCvHint)
+            bulk_g2s_hint(buf0 + b * kCvBuf, kp.cv_X + c * kp.cv_ldx + r0, bytes, &bar0[b], pol_once);
+          else
+            bulk_g2s(buf0 + b * kCvBuf, kp.cv_X + c * kp.cv_ldx + r0, bytes, &bar0[b]);
         } else {
           mbar_arrive(&bar0[b]);  // a one-row piece: nothing to copy
         }
@@ -704,7 +714,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int r = 2 * lane + 64 * k;
         if (r + 2 <= rows) {
           const double2 v = *(const double2*)(sv + r);
-          *(uint16_t*)(dst + r) = (uint16_t)(to_i8_bits(v.x, bad) | to_i8_bits(v.y, bad) << 8);
+          const uint16_t w = (uint16_t)(to_i8_bits(v.x, bad) | to_i8_bits(v.y, bad) << 8);
+          if (kCvHint)
+            st_u16_hint(dst + r, w, pol_once);
+          else
+            *(uint16_t*)(dst + r) = w;
         } else if (r < rows) {  // the column's odd last row: not in the bulk copy
           dst[r] = (int8_t)to_i8_bits(__ldg(kp.cv_X + c * kp.cv_ldx + r0 + r), bad);
         }
