@@ -910,6 +910,10 @@ def test_large_n_planted_beta(glsmod):
     planted-beta identity b_i = (beta, 0) (PAPER.md:28-39 with y in span(X_L)), on both arithmetic
     paths: the int8 tcgen05 path on three chunks of SNPs plus a ragged tail, the FP64 DMMA path on a
     subset."""
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()          # earlier tests' cached blocks (config 3 held 160 GB)
+    glsmod.release_cached_memory()
     n, pL, pR = 49_999, 3, 1
     m = 2 * 18944 + 333
     P = gen.make_problem(n, pL, pR, seed=81, noise=0.0)
