@@ -13,6 +13,7 @@
 // NotSPD (reading A5): a pivot d_j <= 2^-52 * max_k M_kk records min(j) in st->fail.
 #include <climits>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "gls_internal.cuh"
@@ -702,11 +703,34 @@ void mark(cudaStream_t s, int depth, const char* what) {
   g_marks->push_back({e, depth, what});
 }
 
+// Ordering events come from a process-wide pool per device (a create records ~300; creating and
+// destroying them every time costs driver calls on the create's host path).  Every wait on an event is
+// enqueued within the create that recorded it, so handing it to the next create is safe.
+std::mutex g_ev_mu;
+std::vector<cudaEvent_t> g_ev_pool[64];
 cudaEvent_t new_event(RecCtx& rc) {
-  cudaEvent_t e;
-  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  cudaEvent_t e = nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_ev_mu);
+    if (!g_ev_pool[dev].empty()) {
+      e = g_ev_pool[dev].back();
+      g_ev_pool[dev].pop_back();
+    }
+  }
+  if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   rc.events->push_back(e);
   return e;
+}
+void return_events(std::vector<cudaEvent_t>& events) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> lk(g_ev_mu);
+  for (cudaEvent_t e : events) g_ev_pool[dev].push_back(e);
+  events.clear();
 }
 cudaEvent_t record(RecCtx& rc, cudaStream_t st) {
   cudaEvent_t e = new_event(rc);
@@ -938,7 +962,7 @@ void chol_inv(cudaStream_t s, int64_t n, double* A, double* T, int64_t ld, CholS
     cudaStreamWaitEvent(s, record(rc, rc.aux[d]), 0);
   }
   if (ws) cudaFreeAsync(ws, s);  // after the join
-  for (cudaEvent_t e : events) cudaEventDestroy(e);
+  return_events(events);
 }
 
 }  // namespace gls
