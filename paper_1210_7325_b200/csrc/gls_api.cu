@@ -15,6 +15,9 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+#include <nvtx3/nvToolsExtCudaRt.h>
+
 #include "../../include/gls.h"
 #include "gls_internal.cuh"
 
@@ -134,6 +137,30 @@ struct DeviceGuard {
     int cur = -1;
     if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
   }
+};
+
+// NVTX (header-only v3; a no-op unless a tool such as Nsight Systems is attached): ranges in the "gls"
+// domain around the API calls and, in the Alg. 8 streams, around each chunk's H2D / compute / D2H
+// enqueue, and names on the context's streams, so a timeline shows Alg. 8's overlap directly.
+nvtxDomainHandle_t nvtx_domain() {
+  static nvtxDomainHandle_t d = nvtxDomainCreateA("gls");
+  return d;
+}
+struct NvtxRange {
+  explicit NvtxRange(const char* name) {
+    nvtxEventAttributes_t a = {};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = name;
+    nvtxDomainRangePushEx(nvtx_domain(), &a);
+  }
+  void end() {
+    if (open_) nvtxDomainRangePop(nvtx_domain());
+    open_ = false;
+  }
+  ~NvtxRange() { end(); }
+  bool open_ = true;
 };
 
 int fail_cuda(gls_ctx* c, cudaError_t e, const char* what) {
@@ -280,6 +307,11 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR, bool fp64_state = tr
   CK(c, cudaStreamCreateWithFlags(&c->fb, cudaStreamNonBlocking));
   CK(c, cudaStreamCreateWithFlags(&c->alloc_stream, cudaStreamNonBlocking));
   c->stream = c->own_stream;
+  nvtxNameCudaStreamA(c->own_stream, "gls compute");
+  nvtxNameCudaStreamA(c->h2d, "gls h2d (Alg. 8 async_read)");
+  nvtxNameCudaStreamA(c->d2h, "gls d2h (Alg. 8 async_write)");
+  nvtxNameCudaStreamA(c->fb, "gls fp64 fallback");
+  nvtxNameCudaStreamA(c->alloc_stream, "gls alloc");
   for (int k = 0; k < 2; ++k) {
     CK(c, cudaEventCreateWithFlags(&c->ev_oz[k], cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_fb[k], cudaEventDisableTiming));
@@ -800,6 +832,7 @@ int solve_streamed(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out, 
     const int buf = (int)(c->seq++ & 1);
     const double* src = X_R + (size_t)g0 * pR * n;
     gls_ctx::ChunkRec rec{};
+    NvtxRange nr_read("Alg. 8 async_read(X_blk)");
     CK(c, cudaStreamWaitEvent(c->h2d, c->ev_comp[buf], 0));
     rec.h0 = srep_mark(c, c->h2d);
     if (ld == n)
@@ -811,6 +844,8 @@ int solve_streamed(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out, 
     rec.h1 = srep_mark(c, c->h2d);
     rec.hbytes = (int64_t)n * gc * pR * (int64_t)sizeof(double);
     CK(c, cudaEventRecord(c->ev_h2d[buf], c->h2d));
+    nr_read.end();
+    NvtxRange nr_comp("Alg. 8 wait(X_blk), trsm + assembly + posv");
     if (g0 == 0) rec.cr = srep_mark(c, c->stream);
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d[buf], 0));  // wait(current X_blk)
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_d2h[buf], 0));  // wait(previous b_blk) of this workspace
@@ -821,6 +856,8 @@ int solve_streamed(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_out, 
     if (rc) return rc;
     rec.c1 = srep_mark(c, c->stream);
     CK(c, cudaEventRecord(c->ev_comp[buf], c->stream));
+    nr_comp.end();
+    NvtxRange nr_write("Alg. 8 async_write(b_blk)");
     if (!b_dev || (status_out && !s_dev)) {
       CK(c, cudaStreamWaitEvent(c->d2h, c->ev_comp[buf], 0));
       rec.d0 = srep_mark(c, c->d2h);
@@ -888,6 +925,7 @@ int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, d
   for (int64_t g0 = 0, gc = 0; g0 < m_blk; g0 += gc) {
     gc = std::min<int64_t>(m_blk - g0, g0 == 0 ? first : chunk_groups);
     const int buf = (int)(c->seq++ & 1);
+    NvtxRange nr_read("Alg. 8 async_read(X_blk)");
     CK(c, cudaStreamWaitEvent(c->h2d, c->ev_comp[buf], 0));
     // contiguous rows whose length is not a multiple of 16 bytes (the TMA row pitch): one linear copy
     // (a pitched copy of short rows runs at a fraction of the link rate), repacked on the device
@@ -903,6 +941,8 @@ int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, d
     rec.h1 = srep_mark(c, c->h2d);
     rec.hbytes = (int64_t)n * gc * pR;
     CK(c, cudaEventRecord(c->ev_h2d[buf], c->h2d));
+    nr_read.end();
+    NvtxRange nr_comp("Alg. 8 wait(X_blk), trsm + assembly + posv");
     if (g0 == 0) rec.cr = srep_mark(c, c->stream);
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d[buf], 0));  // wait(current X_blk)
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_d2h[buf], 0));  // wait(previous b_blk) of this workspace
@@ -917,6 +957,8 @@ int solve_streamed_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, d
     if (rc) return rc;
     rec.c1 = srep_mark(c, c->stream);
     CK(c, cudaEventRecord(c->ev_comp[buf], c->stream));
+    nr_comp.end();
+    NvtxRange nr_write("Alg. 8 async_write(b_blk)");
     if (!b_dev || (status_out && !s_dev)) {
       CK(c, cudaStreamWaitEvent(c->d2h, c->ev_comp[buf], 0));
       rec.d0 = srep_mark(c, c->d2h);
@@ -970,6 +1012,7 @@ int gls_create(int64_t n, int32_t pL, int32_t pR, const double* M, const double*
   if (!M || !y || (pL > 0 && !X_L)) return GLS_ERR_ARG;
   int rc = check_dims(n, pL, pR);
   if (rc) return rc;
+  NvtxRange nr("gls_create");
   gls_ctx* c = new gls_ctx();
   *out = c;
   rc = ctx_init(c, n, pL, pR);
@@ -988,6 +1031,7 @@ int gls_create_async(int64_t n, int32_t pL, int32_t pR, const double* M, const d
   if (!M || !y || (pL > 0 && !X_L)) return GLS_ERR_ARG;
   int rc = check_dims(n, pL, pR);
   if (rc) return rc;
+  NvtxRange nr("gls_create_async");
   gls_ctx* c = new gls_ctx();
   *out = c;
   rc = ctx_init(c, n, pL, pR);
@@ -1078,6 +1122,7 @@ int gls_solve_block_ex(gls_ctx* c, const double* X_R, int64_t m_blk, double* b_o
   if (c->state != ST_OK) return GLS_ERR_STATE;
   if (!X_R || !b_out || (async != 0 && async != 1)) return GLS_ERR_ARG;
   if (m_blk < 1) return GLS_ERR_DIM;
+  NvtxRange nr("gls_solve_block");
   DeviceGuard g(c->device);
   c->err.clear();
   const bool x_dev = is_device_ptr(X_R);
@@ -1120,6 +1165,7 @@ int gls_solve_block_i8(gls_ctx* c, const int8_t* G, int64_t ldg, int64_t m_blk, 
     c->err = "gls_solve_block_i8 needs n <= 131071 (exact int32 digit products)";
     return GLS_ERR_DIM;
   }
+  NvtxRange nr("gls_solve_block_i8");
   DeviceGuard g(c->device);
   c->err.clear();
   const bool x_dev = is_device_ptr(G);
