@@ -934,3 +934,25 @@ def test_large_n_planted_beta(glsmod):
             assert err <= 1e-9, (path, err)
             if path == glsmod.GLS_PATH_AUTO:
                 assert counts[0] > 0, counts  # the int8 kernel did the work
+
+
+def test_strong_shards_bitwise_for_every_world_size(glsmod):
+    """b bitwise independent of the number of GPUs.  The strong-scaling split of the bench
+    (rank r of G owns problems [floor(r m / G), floor((r+1) m / G)), each rank with its own create --
+    the redundant factorisation) is replayed on this GPU for G = 2, 4, 8: every
+    shard's b, from its own context, equals the rows of the single-GPU run bit for bit (shard edges
+    fall inside conversion chunks, waves and tiles)."""
+    from paper_1210_7325_b200 import multi
+    n, pL, pR = 10_000, 3, 1
+    m = 3 * 18944 + 1234
+    P = gen.make_problem(n, pL, pR, seed=91)
+    Xd = torch.empty((m * pR, n), dtype=torch.float64, device="cuda")
+    glsmod.gen_xr_device(91, n, 0, m * pR, Xd)
+    b_full, st_full, _ = run_gpu(glsmod, P, Xd, m, pR)
+    for G in (2, 4, 8):
+        parts = []
+        for r in range(G):
+            lo, hi = multi.snp_range(m, G, r)
+            b_r, _, _ = run_gpu(glsmod, P, Xd[lo * pR:hi * pR], hi - lo, pR)
+            parts.append(b_r)
+        np.testing.assert_array_equal(np.concatenate(parts), b_full, err_msg="G=%d" % G)
