@@ -17,6 +17,7 @@ bounded sample of the same workload and prints the same JSON line with "impl": "
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -96,15 +97,22 @@ def parse():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region.
+
+    nvidia-smi is launched by `launch()` before the warm-up steps: its start-up (NVML init, first
+    query) holds driver locks long enough to stall the host's launches for tens of ms, which showed
+    up as 25-77 ms outlier steps when it started with the timed region.  Every row is time-stamped
+    on arrival; `start()` / `stop()` bracket the timed region and only rows inside it are kept."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []          # (perf_counter at arrival, fields)
         self._stop = threading.Event()
         self._t = None
+        self._t0 = self._t1 = None
 
     def _run(self):
         try:
@@ -117,27 +125,41 @@ class ClockSampler:
             line = p.stdout.readline()
             if not line:
                 break
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
         p.terminate()
 
-    def start(self):
+    def launch(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
 
+    def start(self):
+        if self._t is None:
+            self.launch()
+        self._t0 = time.perf_counter()
+
     def stop(self):
+        self._t1 = time.perf_counter()
+        # one more sampling interval, so a timed region shorter than it still has a sample
+        deadline = self._t1 + 0.5
+        while time.perf_counter() < deadline and not any(t >= self._t0 for t, _ in self.rows):
+            time.sleep(0.05)
         self._stop.set()
         if self._t:
             self._t.join(timeout=2)
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        inside = [r for t, r in self.rows if self._t0 <= t <= self._t1]
+        if not inside:
+            inside = [r for t, r in self.rows if t >= self._t0][:1]
+        sm = [float(r[0]) for r in inside if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in inside if len(r) > 1 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in inside:
             for k, nm in enumerate(names):
                 if len(r) > 3 + k and r[3 + k].lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "sampler": "nvidia-smi -lms 200 launched before the warm-up; rows inside the timed region"}
 
 
 # ----------------------------------------------------------------------------- oracle arm
@@ -257,11 +279,14 @@ class Job:
         torch, dist, multi = self.torch, self.dist, self.multi
         kern_ms, create_ms, timing, launches = [], [], [], [0]
 
+        hostlog = os.environ.get("GLS_BENCH_HOSTLOG") == "1"   # diagnostics: host time of each call
+
         def step(timed):
             tc = time.perf_counter()
             ctx = self.make_ctx(self.Md, self.XLd, self.yd)
+            th = [tc, time.perf_counter()]
             if timed:
-                create_ms.append(1e3 * (time.perf_counter() - tc))
+                create_ms.append(1e3 * (th[1] - tc))
             if path is not None:
                 ctx.set_path(path)
             ctx.set_stream(self.stream.cuda_stream)
@@ -269,18 +294,29 @@ class Job:
             k0 = torch.cuda.Event(enable_timing=True)
             k1 = torch.cuda.Event(enable_timing=True)
             k0.record(self.stream)
+            th.append(time.perf_counter())
             if self.m > 0:
                 ctx.solve_block(self.Xd, self.m, self.b, self.st, async_=True)
             k1.record(self.stream)
+            th.append(time.perf_counter())
             ctx.sync()
+            th.append(time.perf_counter())
             if timed:
                 launches[0] += ctx.kernel_launches
                 k1.synchronize()
                 kern_ms.append(k0.elapsed_time(k1))
                 timing.append(ctx.read_timing())
                 timing[-1]["paths"] = ctx.path_counts()
+            th.append(time.perf_counter())
             ctx.close()
+            th.append(time.perf_counter())
+            if hostlog:
+                names = ("create", "setup", "enqueue", "sync", "read", "close")
+                print("[host] " + " ".join("%s %.2f" % (nm, 1e3 * (th[i + 1] - th[i])) for i, nm in enumerate(names)),
+                      file=sys.stderr, flush=True)
 
+        if clocks:
+            clocks.launch()     # nvidia-smi's start-up lands in the warm-up, not in a timed step
         for _ in range(warmup):
             step(False)
         if clocks:
@@ -371,6 +407,11 @@ def main():
         else:
             dist.init_process_group(backend)
     pkg.load()
+    # No cyclic-GC pauses inside timed regions: after torch's imports a full collection walks ~170k
+    # objects (~75 ms), and one landing in a step stalls the host between that step's synchronising
+    # calls -- seen as single 55-93 ms outlier steps (create or close).  Collect once here, then off.
+    gc.collect()
+    gc.disable()
 
     cfg = gen.CONFIGS[args.config]
     if args.config == 4:
@@ -773,9 +814,10 @@ def run_ooc(args, cfg, world, rank, local):
         ctx.close()
         return launches
 
+    clocks = ClockSampler(local)
+    clocks.launch()
     for _ in range(max(1, args.warmup)):
         step()
-    clocks = ClockSampler(local)
     clocks.start()
     if world > 1:
         dist.barrier()

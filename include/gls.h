@@ -112,7 +112,10 @@ int gls_set_stream(gls_ctx* ctx, void* stream);
  * size); rounded to whole problems.  Default: 64 * (number of SMs) columns. */
 int gls_set_block_cols(gls_ctx* ctx, int64_t cols);
 
-/* gls_destroy -- free everything (NULL is a no-op).  Waits for outstanding work first. */
+/* gls_destroy -- free everything (NULL is a no-op).  Waits for outstanding work first.  The
+ * context's CUDA streams and events go back, idle, to a per-device cache that the next context on
+ * that device takes them from (creating and destroying them per context stalled the host for tens of
+ * ms now and then; GLS_RES_CACHE=0 turns the cache off). */
 void gls_destroy(gls_ctx* ctx);
 
 /* Diagnostics. */

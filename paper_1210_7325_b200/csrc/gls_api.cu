@@ -38,8 +38,16 @@ namespace {
 enum CtxState { ST_OK = 0, ST_FAILED = 1, ST_ADOPT = 2 };
 }
 
+// The streams and fixed events a context owns; taken from / given back to a per-device cache
+// (res_take / res_give) instead of being created and destroyed with every context.
+struct CtxRes {
+  cudaStream_t own = nullptr, h2d = nullptr, d2h = nullptr, fb = nullptr, alloc = nullptr;
+  cudaEvent_t ev[12] = {};  // ev_oz[2], ev_fb[2], ev_h2d[2], ev_comp[2], ev_d2h[2], ev_create, misc
+};
+
 struct gls_ctx {
   int device = 0;
+  CtxRes res;
   int64_t n = 0;
   int pL = 0, pR = 0, p = 0, NW = 1;
   int64_t NB = 0;
@@ -255,6 +263,93 @@ void status_slot_put(CholStatus* s) {
   g_free_slots.push_back(s);
 }
 
+// Per-device cache of context streams / events.  Creating and destroying five streams and ~40
+// events per context made the driver stall the host for 25-90 ms every ~9 create / destroy cycles
+// once the process had seen heavy pinned-memory traffic (bench steps: a 27-63 ms gls_destroy, then
+// a 53-93 ms gls_create whose traced phases were normal; profiles/r02_step_outliers.txt).  A
+// context now takes its streams and fixed events from here and gives them back idle (every stream
+// synchronised) on destroy; timing events likewise.  GLS_RES_CACHE=0 restores create / destroy.
+std::mutex g_res_mu;
+std::vector<CtxRes> g_res[kMaxDevices];
+std::vector<cudaEvent_t> g_tev[kMaxDevices];  // timing-enabled events (gls_set_timing, stream reports)
+bool res_cache_on() {
+  static const bool v = !(getenv("GLS_RES_CACHE") && atoi(getenv("GLS_RES_CACHE")) == 0);
+  return v;
+}
+bool res_take(int dev, CtxRes* r) {
+  if (!res_cache_on() || dev < 0 || dev >= kMaxDevices) return false;
+  std::lock_guard<std::mutex> lk(g_res_mu);
+  if (g_res[dev].empty()) return false;
+  *r = g_res[dev].back();
+  g_res[dev].pop_back();
+  return true;
+}
+void res_give(int dev, CtxRes& r) {
+  for (cudaStream_t st : {r.own, r.h2d, r.d2h, r.fb, r.alloc})
+    if (st) cudaStreamSynchronize(st);
+  const bool whole = r.own && r.h2d && r.d2h && r.fb && r.alloc &&
+                     std::all_of(std::begin(r.ev), std::end(r.ev), [](cudaEvent_t e) { return e != nullptr; });
+  if (res_cache_on() && whole && dev >= 0 && dev < kMaxDevices) {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    g_res[dev].push_back(r);
+  } else {
+    for (cudaEvent_t e : r.ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaStream_t st : {r.own, r.h2d, r.d2h, r.fb, r.alloc})
+      if (st) cudaStreamDestroy(st);
+  }
+  r = CtxRes{};
+}
+cudaEvent_t tev_take(int dev) {
+  if (res_cache_on() && dev >= 0 && dev < kMaxDevices) {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    if (!g_tev[dev].empty()) {
+      cudaEvent_t e = g_tev[dev].back();
+      g_tev[dev].pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return e;
+}
+void tev_give(int dev, cudaEvent_t e) {
+  if (!e) return;
+  if (res_cache_on() && dev >= 0 && dev < kMaxDevices) {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    g_tev[dev].push_back(e);
+  } else {
+    cudaEventDestroy(e);
+  }
+}
+
+// ordering-only events (no timing) for the host-M upload of a create; every wait on one is enqueued
+// within the create that recorded it, so handing it to the next create is safe
+std::vector<cudaEvent_t> g_sev[kMaxDevices];
+cudaError_t sev_take(int dev, cudaEvent_t* e) {
+  if (res_cache_on() && dev >= 0 && dev < kMaxDevices) {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    if (!g_sev[dev].empty()) {
+      *e = g_sev[dev].back();
+      g_sev[dev].pop_back();
+      return cudaSuccess;
+    }
+  }
+  return cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+}
+void sev_give(int dev, cudaEvent_t e) {
+  if (!e) return;
+  if (res_cache_on() && dev >= 0 && dev < kMaxDevices) {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    g_sev[dev].push_back(e);
+  } else {
+    cudaEventDestroy(e);
+  }
+}
+
 cudaError_t gls_pool_alloc(void** p, size_t bytes, int device, cudaStream_t s) {
   cudaMemPool_t pool = gls_device_pool(device);
   if (!pool) return cudaErrorMemoryAllocation;
@@ -301,24 +396,33 @@ int ctx_init(gls_ctx* c, int64_t n, int32_t pL, int32_t pR, bool fp64_state = tr
   CK(c, cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   int prio_lo = 0, prio_hi = 0;  // the context's stream is high priority: in gls_create it carries the
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);  // critical path of the factorisation
-  CK(c, cudaStreamCreateWithPriority(&c->own_stream, cudaStreamNonBlocking, prio_hi));
-  CK(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
-  CK(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
-  CK(c, cudaStreamCreateWithFlags(&c->fb, cudaStreamNonBlocking));
-  CK(c, cudaStreamCreateWithFlags(&c->alloc_stream, cudaStreamNonBlocking));
+  CtxRes& r = c->res;
+  if (!res_take(c->device, &r)) {
+    CK(c, cudaStreamCreateWithPriority(&r.own, cudaStreamNonBlocking, prio_hi));
+    CK(c, cudaStreamCreateWithFlags(&r.h2d, cudaStreamNonBlocking));
+    CK(c, cudaStreamCreateWithFlags(&r.d2h, cudaStreamNonBlocking));
+    CK(c, cudaStreamCreateWithFlags(&r.fb, cudaStreamNonBlocking));
+    CK(c, cudaStreamCreateWithFlags(&r.alloc, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : r.ev) CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    nvtxNameCudaStreamA(r.own, "gls compute");
+    nvtxNameCudaStreamA(r.h2d, "gls h2d (Alg. 8 async_read)");
+    nvtxNameCudaStreamA(r.d2h, "gls d2h (Alg. 8 async_write)");
+    nvtxNameCudaStreamA(r.fb, "gls fp64 fallback");
+    nvtxNameCudaStreamA(r.alloc, "gls alloc");
+  }
+  c->own_stream = r.own;
+  c->h2d = r.h2d;
+  c->d2h = r.d2h;
+  c->fb = r.fb;
+  c->alloc_stream = r.alloc;
   c->stream = c->own_stream;
-  nvtxNameCudaStreamA(c->own_stream, "gls compute");
-  nvtxNameCudaStreamA(c->h2d, "gls h2d (Alg. 8 async_read)");
-  nvtxNameCudaStreamA(c->d2h, "gls d2h (Alg. 8 async_write)");
-  nvtxNameCudaStreamA(c->fb, "gls fp64 fallback");
-  nvtxNameCudaStreamA(c->alloc_stream, "gls alloc");
   for (int k = 0; k < 2; ++k) {
-    CK(c, cudaEventCreateWithFlags(&c->ev_oz[k], cudaEventDisableTiming));
-    CK(c, cudaEventCreateWithFlags(&c->ev_fb[k], cudaEventDisableTiming));
+    c->ev_oz[k] = r.ev[0 + k];
+    c->ev_fb[k] = r.ev[2 + k];
+    c->ev_h2d[k] = r.ev[4 + k];
+    c->ev_comp[k] = r.ev[6 + k];
+    c->ev_d2h[k] = r.ev[8 + k];
     CK(c, cudaEventRecord(c->ev_fb[k], c->own_stream));
-    CK(c, cudaEventCreateWithFlags(&c->ev_h2d[k], cudaEventDisableTiming));
-    CK(c, cudaEventCreateWithFlags(&c->ev_comp[k], cudaEventDisableTiming));
-    CK(c, cudaEventCreateWithFlags(&c->ev_d2h[k], cudaEventDisableTiming));
   }
   const PanelGeom pg = panel_geom(pR);
   c->oz_ok = n <= kOzMaxN;
@@ -426,6 +530,14 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y, b
     CKS(dalloc(c, &rmax, (size_t)((n + kOzR - 1) / kOzR) * kOzR * sizeof(double)));
   }
   mark("alloc");
+  if (trace) {  // the private pool's footprint: growth here means the allocations above mapped memory
+    uint64_t res = 0, used = 0;
+    if (cudaMemPool_t pool = gls::gls_device_pool(c->device)) {
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    fprintf(stderr, "[gls] pool reserved %.3f GB used %.3f GB\n", res / 1e9, used / 1e9);
+  }
   // A host M is uploaded in column chunks on the h2d stream while the factorisation runs: the
   // recursion works left to right and waits for the chunks each kernel touches, so only the first
   // chunk's copy is exposed.  The NotSPD tolerance (max of the diagonal) is then taken on the host.
@@ -439,8 +551,8 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y, b
     c->hst->fail = ULLONG_MAX;
     CKS(cudaMemcpyAsync(st, c->hst, sizeof(CholStatus), cudaMemcpyHostToDevice, s));
     {  // the h2d stream writes A: after its (stream-ordered) allocation
-      cudaEvent_t ea;
-      CKS(cudaEventCreateWithFlags(&ea, cudaEventDisableTiming));
+      cudaEvent_t ea = nullptr;
+      CKS(sev_take(c->device, &ea));
       col_ev.push_back(ea);
       CKS(cudaEventRecord(ea, s));
       CKS(cudaStreamWaitEvent(c->h2d, ea, 0));
@@ -450,7 +562,7 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y, b
     col_ev.resize(ev0 + (size_t)nch);
     for (int64_t k = 0; k < nch; ++k) {
       const int64_t c0 = k * kUploadChunkCols, c1 = std::min(n, c0 + kUploadChunkCols);
-      CKS(cudaEventCreateWithFlags(&col_ev[ev0 + (size_t)k], cudaEventDisableTiming));
+      CKS(sev_take(c->device, &col_ev[ev0 + (size_t)k]));
       CKS(cudaMemcpyAsync(A + c0 * n, M + c0 * n, (size_t)(c1 - c0) * n * sizeof(double), cudaMemcpyHostToDevice,
                           c->h2d));
       CKS(cudaEventRecord(col_ev[ev0 + (size_t)k], c->h2d));
@@ -474,7 +586,7 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y, b
     CKS(cudaStreamSynchronize(s));
     if (c->hst->fail != ULLONG_MAX) {
       set_not_spd(c, c->hst->fail);
-      for (auto e : col_ev) cudaEventDestroy(e);
+      for (auto e : col_ev) sev_give(c->device, e);
       cleanup();
       return GLS_ERR_NOT_SPD;
     }
@@ -505,13 +617,13 @@ int ctx_setup(gls_ctx* c, const double* M, const double* X_L, const double* y, b
   }
   CKS(cudaGetLastError());
   if (async) {
-    CKS(cudaEventCreateWithFlags(&c->ev_create, cudaEventDisableTiming));
+    c->ev_create = c->res.ev[10];
     CKS(cudaEventRecord(c->ev_create, s));
     c->create_pending = true;
   } else {
     CKS(cudaStreamSynchronize(s));
   }
-  for (auto e : col_ev) cudaEventDestroy(e);  // (pending events are released once they complete)
+  for (auto e : col_ev) sev_give(c->device, e);  // (a pending event may be re-recorded: waits already enqueued keep their record)
   mark("pack");
   cleanup();  // stream-ordered frees on the context's stream
   mark("free");
@@ -572,12 +684,7 @@ cudaEvent_t pool_event(gls_ctx* c) {
     c->ev_pool.pop_back();
     return e;
   }
-  cudaEvent_t e = nullptr;
-  if (cudaEventCreate(&e) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  return e;
+  return tev_take(c->device);
 }
 // Brackets one launch on `s` with an event pair when timing is on (diagnostics for bench.py).
 struct LaunchTimer {
@@ -1315,11 +1422,9 @@ int gls_set_stream(gls_ctx* c, void* stream) {
   // work still pending on the old stream uses the context's scratch buffers (x8, cflags, bscratch,
   // staging): order the new stream after it, so reuse on the new stream cannot race with it
   DeviceGuard g(c->device);
-  cudaEvent_t e = nullptr;
-  CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t e = c->res.ev[11];
   cudaError_t err = cudaEventRecord(e, c->stream);
   if (err == cudaSuccess) err = cudaStreamWaitEvent(next, e, 0);
-  cudaEventDestroy(e);
   if (err != cudaSuccess) return fail_cuda(c, err, "gls_set_stream");
   c->stream = next;
   return GLS_OK;
@@ -1371,26 +1476,16 @@ void gls_destroy(gls_ctx* c) {
     dfree(c, c->stage8[k]);
     dfree(c, c->raw8[k]);
   }
-  for (auto& x : c->tl) {
-    cudaEventDestroy(x.a);
-    cudaEventDestroy(x.b);
-  }
-  for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
-  for (int k = 0; k < 2; ++k) {
-    if (c->ev_h2d[k]) cudaEventDestroy(c->ev_h2d[k]);
-    if (c->ev_comp[k]) cudaEventDestroy(c->ev_comp[k]);
-    if (c->ev_d2h[k]) cudaEventDestroy(c->ev_d2h[k]);
-    if (c->ev_oz[k]) cudaEventDestroy(c->ev_oz[k]);
-    if (c->ev_fb[k]) cudaEventDestroy(c->ev_fb[k]);
+  for (auto& x : c->tl) {
+    tev_give(c->device, x.a);
+    tev_give(c->device, x.b);
   }
-  if (c->ev_create) cudaEventDestroy(c->ev_create);
+  for (auto e : c->ev_pool) tev_give(c->device, e);
+  for (auto& x : c->srec)
+    for (cudaEvent_t e : {x.h0, x.h1, x.c0, x.c1, x.d0, x.d1, x.cr}) tev_give(c->device, e);
   status_slot_put(c->hst);
-  if (c->alloc_stream) cudaStreamDestroy(c->alloc_stream);
-  if (c->fb) cudaStreamDestroy(c->fb);
-  if (c->own_stream) cudaStreamDestroy(c->own_stream);
-  if (c->h2d) cudaStreamDestroy(c->h2d);
-  if (c->d2h) cudaStreamDestroy(c->d2h);
+  res_give(c->device, c->res);  // idle streams and events back to the device's cache
   cudaGetLastError();
   delete c;
 }
