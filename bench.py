@@ -411,7 +411,8 @@ def main():
     # objects (~75 ms), and one landing in a step stalls the host between that step's synchronising
     # calls -- seen as single 55-93 ms outlier steps (create or close).  Collect once here, then off.
     gc.collect()
-    gc.disable()
+    if os.environ.get("GLS_BENCH_GC") != "1":   # diagnostics: keep the collector on
+        gc.disable()
 
     cfg = gen.CONFIGS[args.config]
     if args.config == 4:
@@ -496,7 +497,8 @@ def main():
                 ctx.close()
                 return rep
 
-            one()
+            for _ in range(max(1, min(args.warmup, 3))):   # the first steps still page in pinned buffers
+                one()
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
