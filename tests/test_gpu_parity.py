@@ -519,6 +519,50 @@ def test_repeated_create_destroy_is_deterministic(glsmod):
     np.testing.assert_array_equal(outs[0], outs[2])
 
 
+def test_cached_streams_across_overlapping_contexts(glsmod):
+    """Contexts take their CUDA streams and events from a per-device cache and give them back on
+    destroy.  A rolling window of three live contexts -- async solves still in flight when an older
+    context is destroyed and a new one takes its streams, async creates from pinned host M, a user
+    stream, timing and stream-report events -- must give every context exactly the bits of a context
+    used alone."""
+    cases = []
+    for n, pL, pR, m, seed in ((1100, 3, 1, 700, 71), (1500, 2, 2, 300, 72)):
+        P = gen.make_problem(n, pL, pR, seed=seed)
+        XR = gen.make_XR(seed, n, 0, m * pR)
+        b_ref, _, _ = run_gpu(glsmod, P, dev(XR), m, pR)
+        cases.append((P, pR, m, dev(XR), torch.from_numpy(XR).to(torch.int8).pin_memory(), b_ref))
+    user = torch.cuda.Stream()
+    live = []
+
+    def finish(entry):
+        ctx, b, b_ref = entry
+        ctx.sync()
+        np.testing.assert_array_equal(b.cpu().numpy() if b.is_cuda else b.numpy(), b_ref)
+        ctx.close()
+
+    for it in range(12):
+        P, pR, m, Xd, G8, b_ref = cases[it % 2]
+        if it % 3 == 1:   # async create from pinned host buffers, then the host int8 stream
+            ctx = glsmod.Context(P.n, P.pL, pR, torch.from_numpy(P.M).pin_memory(),
+                                 torch.from_numpy(np.ascontiguousarray(P.XL)).pin_memory(),
+                                 torch.from_numpy(P.y).pin_memory(), async_create=True)
+            ctx.set_stream_report(True)
+            b = torch.empty((m, P.pL + pR), dtype=torch.float64, pin_memory=True)
+            ctx.solve_block_i8(G8, m, b, None, async_=True)
+        else:             # device buffers, async solve, every other one on a user stream
+            ctx = glsmod.Context(P.n, P.pL, pR, dev(P.M), dev(P.XL), dev(P.y))
+            if it % 2 == 0:
+                ctx.set_stream(user.cuda_stream)
+            ctx.set_timing(True)
+            b = torch.empty((m, P.pL + pR), dtype=torch.float64, device="cuda")
+            ctx.solve_block(Xd, m, b, None, async_=True)
+        live.append((ctx, b, b_ref))
+        if len(live) == 3:
+            finish(live.pop(0))   # destroyed while the two younger contexts still have work queued
+    for entry in live:
+        finish(entry)
+
+
 def test_int8_genotype_entry_matches_double_entry(glsmod):
     """gls_solve_block_i8 (genotype codes) gives the same bits as gls_solve_block on the same
     values: device in place (ldg % 16 == 0), device with an odd leading dimension (staged),
