@@ -70,11 +70,13 @@ namespace {
 
 void dist_free(gls_dist* d) {
   if (!d) return;
-  if (d->s) cudaStreamSynchronize(d->s);
+  // the buffers are also read and written by the caller's collectives on other streams
+  cudaDeviceSynchronize();
   for (void* p : {(void*)d->A, (void*)d->R, (void*)d->panel, (void*)d->tmp, (void*)d->B, (void*)d->Bloc,
                   (void*)d->Wpart, (void*)d->W, (void*)d->V, (void*)d->rowmax, (void*)d->vmax, (void*)d->esc,
                   (void*)d->ws, (void*)d->st})
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, d->s);  // back to the library's stream-ordered pool (no unmapping)
+  if (d->s) cudaStreamSynchronize(d->s);
   if (d->ctx) gls_destroy(d->ctx);
   if (d->s) cudaStreamDestroy(d->s);
   cudaGetLastError();
@@ -136,13 +138,18 @@ extern "C" int gls_dist_create(int64_t n, int32_t pL, int32_t pR, int64_t nb, in
   const int64_t NBR = (n + kOzR - 1) / kOzR;
   const size_t nl = (size_t)(d->nloc > 0 ? d->nloc : 1);
   const int pl1 = d->pl1;
-  if (cudaMalloc(&d->A, (size_t)n * nl * 8) || cudaMalloc(&d->R, (size_t)n * nl * 8) ||
-      cudaMalloc(&d->panel, (size_t)n * nb * 8) || cudaMalloc(&d->tmp, (size_t)nb * nl * 8) ||
-      cudaMalloc(&d->B, (size_t)n * pl1 * 8) || cudaMalloc(&d->Bloc, nl * pl1 * 8) ||
-      cudaMalloc(&d->Wpart, (size_t)n * pl1 * 8) || cudaMalloc(&d->W, (size_t)n * pl1 * 8) ||
-      cudaMalloc(&d->V, (size_t)n * pl1 * 8) || cudaMalloc(&d->rowmax, (size_t)NBR * kOzR * 8) ||
-      cudaMalloc(&d->vmax, (size_t)pl1 * 8) || cudaMalloc(&d->esc, (size_t)NBR * kOzR * sizeof(int)) ||
-      cudaMalloc(&d->ws, kSplitKWsDoubles * 8) || cudaMalloc(&d->st, sizeof(CholStatus)))
+  // from the library's stream-ordered pool (cached across creates: cudaMalloc / cudaFree of these
+  // ~2 n^2 / G * 8 bytes mapped and unmapped pages on every create), usable from any stream after
+  // the synchronisation below
+  auto palloc = [&](auto** p, size_t bytes) { return gls_pool_alloc((void**)p, bytes, d->device, d->s); };
+  if (palloc(&d->A, (size_t)n * nl * 8) || palloc(&d->R, (size_t)n * nl * 8) ||
+      palloc(&d->panel, (size_t)n * nb * 8) || palloc(&d->tmp, (size_t)nb * nl * 8) ||
+      palloc(&d->B, (size_t)n * pl1 * 8) || palloc(&d->Bloc, nl * pl1 * 8) ||
+      palloc(&d->Wpart, (size_t)n * pl1 * 8) || palloc(&d->W, (size_t)n * pl1 * 8) ||
+      palloc(&d->V, (size_t)n * pl1 * 8) || palloc(&d->rowmax, (size_t)NBR * kOzR * 8) ||
+      palloc(&d->vmax, (size_t)pl1 * 8) || palloc(&d->esc, (size_t)NBR * kOzR * sizeof(int)) ||
+      palloc(&d->ws, kSplitKWsDoubles * 8) || palloc(&d->st, sizeof(CholStatus)) ||
+      cudaStreamSynchronize(d->s))
     return fail(GLS_ERR_OOM);
   cudaStream_t s = d->s;
   // owned column blocks of M (contiguous n x w column ranges of the column-major M)
