@@ -153,10 +153,13 @@ struct gls_gwfgls {
 namespace {
 void gw_free(gls_gwfgls* g) {
   if (!g) return;
-  if (g->s) cudaStreamSynchronize(g->s);
+  cudaDeviceSynchronize();  // (a user stream may still read the buffers)
   for (double* p : {g->Minv, g->XL, g->WL, g->y, g->WR, g->ws})
-    if (p) cudaFree(p);
-  if (g->s) cudaStreamDestroy(g->s);
+    if (p) cudaFreeAsync(p, g->s);  // back to the library's stream-ordered pool
+  if (g->s) {
+    cudaStreamSynchronize(g->s);
+    cudaStreamDestroy(g->s);
+  }
   delete g;
 }
 }  // namespace
@@ -176,22 +179,23 @@ extern "C" int gls_gwfgls_create(int64_t n, int32_t pL, int32_t pR, const double
   CholStatus* st = nullptr;
   CholStatus hst;
   auto fail = [&](int rc) {
-    if (A) cudaFree(A);
-    if (T) cudaFree(T);
-    if (st) cudaFree(st);
+    for (void* q : {(void*)A, (void*)T, (void*)st})
+      if (q) cudaFreeAsync(q, g->s);
     cudaGetLastError();
     gw_free(g);
     return rc;
   };
   if (cudaGetDevice(&g->device) != cudaSuccess || cudaStreamCreateWithFlags(&g->s, cudaStreamNonBlocking) != cudaSuccess)
     return fail(GLS_ERR_CUDA);
-  if (cudaMalloc(&A, nn) != cudaSuccess || cudaMalloc(&T, nn) != cudaSuccess || cudaMalloc(&g->Minv, nn) != cudaSuccess ||
-      cudaMalloc(&g->XL, (size_t)n * (pL > 0 ? pL : 1) * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&g->WL, (size_t)n * (pL > 0 ? pL : 1) * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&g->y, (size_t)n * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&g->WR, (size_t)n * kGwChunkCols * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&g->ws, kSplitKWsDoubles * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&st, sizeof(CholStatus)) != cudaSuccess)
+  // device buffers from the library's stream-ordered pool (cached across creates, no page mapping)
+  auto palloc = [&](auto** q, size_t bytes) { return gls_pool_alloc((void**)q, bytes, g->device, g->s); };
+  if (palloc(&A, nn) != cudaSuccess || palloc(&T, nn) != cudaSuccess || palloc(&g->Minv, nn) != cudaSuccess ||
+      palloc(&g->XL, (size_t)n * (pL > 0 ? pL : 1) * sizeof(double)) != cudaSuccess ||
+      palloc(&g->WL, (size_t)n * (pL > 0 ? pL : 1) * sizeof(double)) != cudaSuccess ||
+      palloc(&g->y, (size_t)n * sizeof(double)) != cudaSuccess ||
+      palloc(&g->WR, (size_t)n * kGwChunkCols * sizeof(double)) != cudaSuccess ||
+      palloc(&g->ws, kSplitKWsDoubles * sizeof(double)) != cudaSuccess ||
+      palloc(&st, sizeof(CholStatus)) != cudaSuccess)
     return fail(GLS_ERR_OOM);
   cudaStream_t s = g->s;
   if (cudaMemcpyAsync(A, M, nn, cudaMemcpyDefault, s) != cudaSuccess || cudaMemsetAsync(T, 0, nn, s) != cudaSuccess ||
@@ -210,9 +214,12 @@ extern "C" int gls_gwfgls_create(int64_t n, int32_t pL, int32_t pR, const double
   // line 2: W_L = M^{-1} X_L
   if (pL > 0) dgemm(s, n, pL, n, 1.0, g->Minv, n, 'N', g->XL, n, 'N', 0.0, g->WL, n, 0, &g->launches, g->ws);
   if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess) return fail(GLS_ERR_CUDA);
-  cudaFree(A);
-  cudaFree(T);
-  cudaFree(st);
+  cudaFreeAsync(A, s);
+  cudaFreeAsync(T, s);
+  cudaFreeAsync(st, s);
+  A = T = nullptr;
+  st = nullptr;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return fail(GLS_ERR_CUDA);  // buffers usable from any stream
   *out = g;
   return GLS_OK;
 }
