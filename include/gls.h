@@ -146,11 +146,12 @@ int gls_shared_view_ex(gls_ctx* ctx, int32_t flags, void** ptrs, int64_t* bytes,
 int64_t gls_kernel_launches(const gls_ctx* ctx);
 
 /* Arithmetic path of the trsm (Alg. 5 line 3).  Both give FP64-accurate b.
- *   GLS_PATH_AUTO (default): blocks whose X_R values are all integers in [-128, 127] (SNP
- *     genotypes) run on the int8 tensor cores with T = L^{-1} split into seven
+ *   GLS_PATH_AUTO (default): problems whose pR columns of X_R hold only integers in [-128, 127]
+ *     (SNP genotypes) run on the int8 tensor cores with T = L^{-1} split into seven
  *     base-256 digits per element (exact int32 digit products, one rounding of T to 55 bits per
- *     row, reading A15); any other block runs on the FP64 tensor pipe.  Decided per device chunk
- *     of the block, on the device (no host synchronisation).  Only for n <= 131071.
+ *     row, reading A15); every other problem runs on the FP64 tensor pipe.  Decided per problem, on
+ *     the device (no host synchronisation), so a problem's bits depend only on its own values --
+ *     never on its neighbours or the block partition.  Only for n <= 131071.
  *   GLS_PATH_FP64: every block on the FP64 tensor pipe (DMMA).
  * The environment variable GLS_PATH=fp64 sets the default of new contexts. */
 enum { GLS_PATH_AUTO = 0, GLS_PATH_FP64 = 1 };
@@ -225,12 +226,8 @@ int gls_release_cached_memory(void);
  *                        points (Alg. 8 lines 8 and 16; Alg. 7 lines 7 and 14), the first block's load,
  *                        blocks and bytes moved.
  * Results are bitwise identical between the two modes and to gls_solve_block on the same values (same
- * kernels, block-partition independent) whenever every block takes the same arithmetic path -- always for
- * genotype codes (elem_bytes 1) and for integer-valued FP64 X_R.  Exception (reading A16): with
- * GLS_PATH_AUTO the int8-or-FP64 choice is made per device conversion chunk, so for FP64 X_R that mixes
- * integer and non-integer (dosage) columns, a problem's record can differ at rounding level (both paths
- * are within the parity tolerance) depending on which chunk it falls in; GLS_PATH_FP64 restores
- * partition-independent bits for such data.  Synchronous: returns when every b is on the file.
+ * kernels, block-partition independent; the int8-or-FP64 choice is made per problem, reading A16).
+ * Synchronous: returns when every b is on the file.
  * Errors: GLS_ERR_ARG (bad argument, unreadable/short X_R file, failed write), GLS_ERR_DIM, GLS_ERR_OOM
  * (pinned workspaces), and any error of the solve calls. */
 enum { GLS_OOC_SYNC = 0, GLS_OOC_ASYNC = 1 };

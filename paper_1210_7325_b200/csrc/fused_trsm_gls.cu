@@ -91,6 +91,7 @@ struct KParams {
   double* b_out;
   int32_t* status_out;
   const int* gate;  // nullable: when set, run only if *gate != 0 (int8 path rejected the block)
+  const int* pflag;  // nullable: solve and store only problems g with pflag[g] != 0; skip other panels
   unsigned long long* ran;  // nullable: block 0 adds 1 when the kernel does its work
   int64_t m_blk;
   int64_t num_panels;
@@ -156,6 +157,16 @@ __device__ __forceinline__ void mma_frag(double (&acc)[4][4][2], const Frag& f) 
       for (int s = 0; s < 4; ++s) dmma(acc[t][s], f.a[t][e], f.b[s][e]);
 }
 
+// Per-problem path choice: a panel without a flagged problem is left to the int8 kernel (the producer and
+// every consumer decide alike from the same flags, so their stage counters stay in step).
+__device__ __forceinline__ bool panel_wanted(const KParams& kp, int64_t panel) {
+  if (!kp.pflag) return true;
+  const int64_t g1 = (panel + 1) * kp.gpp < kp.m_blk ? (panel + 1) * kp.gpp : kp.m_blk;
+  for (int64_t g = panel * kp.gpp; g < g1; ++g)
+    if (kp.pflag[g]) return true;
+  return false;
+}
+
 template <int NW, bool FULL, bool ALIGNED>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_trsm_gls_kernel(const __grid_constant__ CUtensorMap xmap, const KParams kp) {
@@ -197,6 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t rbc = 0;  // running row-block counter (W buffer = rbc & 1, its use = rbc >> 1)
       const uint32_t xbytes = (uint32_t)(kKT * kp.cpp * 8);
       for (int64_t panel = blockIdx.x; panel < kp.num_panels; panel += gridDim.x) {
+        if (!panel_wanted(kp, panel)) continue;
         const int col0 = (int)(panel * kp.cpp);
         for (int i = 0; i < NB; ++i, ++rbc) {
           const double* Trb = kp.Tpk + tpk_tile_offset(i) * kTileDoubles;
@@ -266,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t rbc = 0;
   Frag F0, F1;
   for (int64_t panel = blockIdx.x; panel < kp.num_panels; panel += gridDim.x) {
+    if (!panel_wanted(kp, panel)) continue;
     for (int i = 0; i < NB; ++i, ++rbc) {
 #pragma unroll
       for (int t = 0; t < 4; ++t)
@@ -364,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int gl = threadIdx.x;  // one thread per problem of the panel
     const int64_t gidx = panel * kp.gpp + gl;
-    if (gl < kp.gpp && gidx < kp.m_blk) {
+    if (gl < kp.gpp && gidx < kp.m_blk && !(kp.pflag && !kp.pflag[gidx])) {
       const int pL = kp.pL, pR = kp.pR, p = kp.p;
       const int gmw = gl / kp.gw, gg = gl % kp.gw;
       const double* rd = sR + (size_t)gmw * C::kRedDoubles;
@@ -561,6 +574,7 @@ cudaError_t launch_fused_trsm_gls(cudaStream_t s, const SolveArgs& a, int num_sm
   kp.b_out = a.b_out;
   kp.status_out = a.status_out;
   kp.gate = gate;
+  kp.pflag = a.pflag;
   kp.ran = ran;
   kp.m_blk = a.m_blk;
   kp.num_panels = (a.m_blk + pg.gpp - 1) / pg.gpp;

@@ -81,8 +81,10 @@ struct gls_ctx {
   int64_t sws_groups = 0;
   int8_t* x8[2] = {nullptr, nullptr};
   int* flags = nullptr;                  // 2 ints, then (8-byte aligned) 2 work counters
-  int* cflags = nullptr;                 // per conversion chunk of a block: "not int8" flags
+  int* cflags = nullptr;                 // per conversion chunk of a block: its problems on the FP64 path
   int64_t cflags_cap = 0;
+  int* pflags = nullptr;                 // per problem of a block: 1 = holds a value int8 cannot take
+  int64_t pflags_cap = 0;
   unsigned long long* ran = nullptr;     // [0] int8 kernel launches that ran, [1] FP64 ones
   cudaEvent_t ev_oz[2] = {}, ev_fb[2] = {};
   cudaStream_t fb = nullptr;  // gated FP64 fallback launches (off the int8 kernel's stream)
@@ -713,7 +715,7 @@ cudaEvent_t srep_mark(gls_ctx* c, cudaStream_t s) {
 }
 
 int run_fp64(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt,
-             const int* gate, cudaStream_t strm = nullptr) {
+             const int* gate, cudaStream_t strm = nullptr, const int* pflag = nullptr) {
   if (!strm) strm = c->stream;
   LaunchTimer lt(c, strm, 1);
   SolveArgs a;
@@ -729,6 +731,7 @@ int run_fp64(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b
   a.G = c->G;
   a.b_out = b;
   a.status_out = stt;
+  a.pflag = pflag;
   std::string msg;
   cudaError_t e = launch_fused_trsm_gls(strm, a, c->num_sms, &msg, &c->launches, gate, c->ran + 1);
   if (e != cudaSuccess) {
@@ -754,7 +757,8 @@ int ensure_x8(gls_ctx* c, int64_t cols) {
 
 int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* b, int32_t* stt,
              const int* gate, const double* cv_X = nullptr, int64_t cv_ldx = 0, int64_t cv_cols = 0,
-             int8_t* cv_X8 = nullptr, int* cv_flag = nullptr) {
+             int8_t* cv_X8 = nullptr, int* cv_flag = nullptr, const int* pflag = nullptr,
+             int* cv_pflag = nullptr) {
   if (c->p > kOzPosvInKernelMaxP && c->sws_groups < groups) {
     if (c->sws) CK(c, cudaDeviceSynchronize());
     dfree(c, c->sws);
@@ -786,6 +790,9 @@ int run_int8(gls_ctx* c, const int8_t* X8, int64_t ld8, int64_t groups, double* 
   a.cv_X8 = cv_X8;
   a.cv_ld8 = ld8;
   a.cv_flag = cv_flag;
+  a.pflag = pflag;
+  a.gate_all = groups;
+  a.cv_pflag = cv_pflag;
   std::string msg;
   cudaError_t e = launch_ozaki_gls(c->stream, a, c->num_sms, &msg, &c->launches);
   if (e != cudaSuccess) {
@@ -838,9 +845,12 @@ int run_kernel_int8_only(gls_ctx* c, const double* X, int64_t ldx, int64_t group
 // Path AUTO: chunks of up to 8 waves of int8 tiles (1, 2, .. 8, 8, ..).  Chunk 0 is converted to int8
 // by a standalone pass; every later chunk j+1 is converted by the convert-ahead warps of the int8
 // kernel of chunk j, concurrently with its tensor-core work, into the other of the two int8
-// workspaces (flagging values that are not integers in [-128, 127] in cflags[j+1]).  For each chunk
-// the int8 kernel and the FP64 kernel are both launched, each gated on the device by the chunk's
-// flag, so exactly one of them does the work and the host never waits.
+// workspaces.  The path is chosen per problem: a problem whose pR columns hold a value that is not an
+// integer in [-128, 127] is flagged (pflags[g] = 1, counted in cflags[j]) and solved by the FP64 kernel,
+// every other problem by the int8 kernel -- so a problem's bits depend on its own values only, not on
+// its neighbours or the block partition.  For each chunk both kernels are launched, gated on the device
+// by the chunk's count (int8: skipped when every problem is flagged; FP64: when none is; it also skips
+// panels without a flagged problem), each storing only its own problems, and the host never waits.
 int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt) {
   if (!c->fp64_ok) return run_kernel_int8_only(c, X, ldx, groups, b, stt);
   if (c->path == GLS_PATH_FP64 || !c->oz_ok) return run_fp64(c, X, ldx, groups, b, stt, nullptr);
@@ -876,15 +886,25 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
     CK(c, walloc(c, &c->cflags, (size_t)cap * sizeof(int)));
     c->cflags_cap = cap;
   }
+  if (c->pflags_cap < groups) {
+    if (c->pflags) CK(c, cudaDeviceSynchronize());
+    dfree(c, c->pflags);
+    c->pflags_cap = 0;
+    const int64_t cap = std::max<int64_t>(groups, 65536);
+    CK(c, walloc(c, &c->pflags, (size_t)cap * sizeof(int)));
+    c->pflags_cap = cap;
+  }
+  int* const pf = c->pflags;
   // the flags of the previous block were last read by its FP64 launches, which the compute stream
   // waited for at the end of that block
   CK(c, cudaMemsetAsync(c->cflags, 0, (size_t)nchunks * sizeof(int), c->stream));
+  CK(c, cudaMemsetAsync(pf, 0, (size_t)groups * sizeof(int), c->stream));
   unsigned long long* work = (unsigned long long*)(c->flags + 2);
   CK(c, cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->stream));
   {
     LaunchTimer lt(c, c->stream, 2);
     oz_convert(c->stream, X, ldx, c->n, (bnd[1] - bnd[0]) * pR, c->x8[0], c->ld8, c->cflags, work, c->num_sms,
-               &c->launches);
+               &c->launches, pf, pR);
     CK(c, cudaGetLastError());
   }
   for (int64_t j = 0; j < nchunks; ++j) {
@@ -894,7 +914,7 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
       CK(c, cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->stream));
       LaunchTimer lt(c, c->stream, 2);
       oz_convert(c->stream, X + (size_t)g0 * pR * ldx, ldx, c->n, gc * pR, c->x8[buf], c->ld8, c->cflags + j,
-                 work, c->num_sms, &c->launches);
+                 work, c->num_sms, &c->launches, pf + g0, pR);
       CK(c, cudaGetLastError());
     }
     // cflags[j] is final here (written by chunk j-1's kernel or a standalone pass)
@@ -904,13 +924,13 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
     int32_t* sj = stt ? stt + g0 : nullptr;
     if (ahead && j + 1 < nchunks)
       rc = run_int8(c, c->x8[buf], c->ld8, gc, bj, sj, c->cflags + j, X + (size_t)bnd[j + 1] * pR * ldx, ldx,
-                    (bnd[j + 2] - bnd[j + 1]) * pR, c->x8[buf ^ 1], c->cflags + j + 1);
+                    (bnd[j + 2] - bnd[j + 1]) * pR, c->x8[buf ^ 1], c->cflags + j + 1, pf + g0, pf + bnd[j + 1]);
     else
-      rc = run_int8(c, c->x8[buf], c->ld8, gc, bj, sj, c->cflags + j);
+      rc = run_int8(c, c->x8[buf], c->ld8, gc, bj, sj, c->cflags + j, nullptr, 0, 0, nullptr, nullptr, pf + g0);
     if (rc) return rc;
     // the gated FP64 kernel runs on its own stream, so when it has nothing to do its launch never
     // holds back the next int8 kernel
-    rc = run_fp64(c, X + (size_t)g0 * pR * ldx, ldx, gc, bj, sj, c->cflags + j, c->fb);
+    rc = run_fp64(c, X + (size_t)g0 * pR * ldx, ldx, gc, bj, sj, c->cflags + j, c->fb, pf + g0);
     if (rc) return rc;
   }
   // the block is complete on the compute stream only when its fallback launches are
@@ -1471,6 +1491,7 @@ void gls_destroy(gls_ctx* c) {
   dfree(c, c->sws);
   dfree(c, c->flags);
   dfree(c, c->cflags);
+  dfree(c, c->pflags);
   dfree(c, c->ran);
   for (int k = 0; k < 2; ++k) {
     dfree(c, c->stage8[k]);

@@ -114,6 +114,9 @@ struct SolveArgs {
   const double* G;      // (pL+1) x (pL+1): S_TL = G[0:pL,0:pL], b_T = G[0:pL, pL]
   double* b_out;        // device
   int32_t* status_out;  // device or nullptr
+  // nullable per-problem path flags (int8 conversion): when set, only problems g with pflag[g] != 0 are
+  // solved and stored (the int8 kernel stores the others), and panels without one are skipped
+  const int* pflag = nullptr;
 };
 // Returns cudaSuccess or the launch error; msg receives a description on failure.
 // gate (nullable, device): when non-null the kernel returns at once unless *gate != 0 (it is the
@@ -169,9 +172,12 @@ void oz_vmax(cudaStream_t s, const double* V, int64_t n, int pl1, ColOwn own, do
 void oz_vdigits(cudaStream_t s, const double* V, int64_t n, int pl1, ColOwn own, const double* vmax, int* ev,
                 double* vscale, int8_t* V8, int64_t* lc);
 // X (double) -> X8 (int8, ld8 % 16 == 0); *flag |= 1 if some value is not an integer in [-128,127].
+// With pflag (zeroed, one int per problem of pR columns): pflag[g] = 1 for every problem holding such
+// a value and *flag counts those problems instead.
 // work: a zeroed unsigned long long (the pass's work-stealing counter).
 void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t cols, int8_t* X8,
-                int64_t ld8, int* flag, unsigned long long* work, int num_sms, int64_t* launch_counter);
+                int64_t ld8, int* flag, unsigned long long* work, int num_sms, int64_t* launch_counter,
+                int* pflag = nullptr, int pR = 1);
 struct OzArgs {
   const int8_t* X8;     // column-major, ld8 (multiple of 16), device
   int64_t ld8;
@@ -196,6 +202,12 @@ struct OzArgs {
   int8_t* cv_X8 = nullptr;
   int64_t cv_ld8 = 0;
   int* cv_flag = nullptr;
+  // nullable per-problem path flags (see oz_convert): with pflag, *gate counts the launch's flagged
+  // problems, the kernel runs unless all gate_all are flagged and stores none of the flagged ones;
+  // cv_pflag receives the convert-ahead chunk's flags (first-time flags counted in *cv_flag)
+  const int* pflag = nullptr;
+  int64_t gate_all = 0;
+  int* cv_pflag = nullptr;
 };
 constexpr int kOzPosvInKernelMaxP = 8;  // p above this: posv in a separate kernel (oz s_ws)
 constexpr int64_t kConvertAheadMinN = 4096;  // n below this: standalone FP64 -> int8 pass per chunk

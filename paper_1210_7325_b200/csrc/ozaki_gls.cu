@@ -111,6 +111,13 @@ struct OzParams {
   int8_t* cv_X8;
   int64_t cv_ld8;
   int* cv_flag;
+  // per-problem path choice (nullable pflag): pflag[g] != 0 -- problem g holds a value that is not an
+  // integer in [-128, 127] and is solved by the FP64 kernel; *gate then counts the flagged problems and
+  // this kernel skips only when all gate_all of them are; it stores no result of a flagged problem.
+  // cv_pflag: the same flags for the convert-ahead job's chunk (first-time flags add 1 to *cv_flag).
+  const int* pflag;
+  int64_t gate_all;
+  int* cv_pflag;
 };
 
 // FP64 value -> int8 code, flagging (bad = 1) anything that is not an integer in [-128, 127]
@@ -231,7 +238,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   // A gated launch (this chunk is not integer: the FP64 kernel solves it) still runs its
   // convert-ahead job -- the next chunk depends on it -- but no tile.
-  const bool gated = kp.gate && *(volatile const int*)kp.gate != 0;  // uniform across the grid
+  const int nflag = kp.gate ? *(volatile const int*)kp.gate : 0;  // uniform across the grid
+  const bool gated = kp.pflag ? nflag >= kp.gate_all : nflag != 0;
+  const bool masked = kp.pflag && nflag != 0;  // some problems of this launch belong to the FP64 kernel
   if (!gated && kp.ran && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(kp.ran, 1ull);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -611,7 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int w = 0; w < NA; ++w) acc[w] += tmem_ld_f64(tlane + xcol(w));
         const int64_t col = (int64_t)tile * cpt + q * kp.cpw + lane;
-        const bool owner = lane < kp.cpw && a_in == 0 && col < kp.cols;
+        const bool owner = lane < kp.cpw && a_in == 0 && col < kp.cols && !(masked && kp.pflag[col / kp.pR]);
         const int p = kp.p, pL = kp.pL, pR = kp.pR;
         double S[400];
         double rhs[20];
@@ -709,19 +718,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       piece(u, c, r0, rows);
       const double* sv = (const double*)(buf0 + b * kCvBuf);
       int8_t* dst = kp.cv_X8 + c * kp.cv_ld8 + r0;
+      int pb = 0;  // this piece holds a value the int8 path cannot take
 #pragma unroll 4
       for (int k = 0; k < kCvRows / 64; ++k) {  // lane holds rows 2 lane + 64 k, +1
         const int r = 2 * lane + 64 * k;
         if (r + 2 <= rows) {
           const double2 v = *(const double2*)(sv + r);
-          const uint16_t w = (uint16_t)(to_i8_bits(v.x, bad) | to_i8_bits(v.y, bad) << 8);
+          const uint16_t w = (uint16_t)(to_i8_bits(v.x, pb) | to_i8_bits(v.y, pb) << 8);
           if (kCvHint)
             st_u16_hint(dst + r, w, pol_once);
           else
             *(uint16_t*)(dst + r) = w;
         } else if (r < rows) {  // the column's odd last row: not in the bulk copy
-          dst[r] = (int8_t)to_i8_bits(__ldg(kp.cv_X + c * kp.cv_ldx + r0 + r), bad);
+          dst[r] = (int8_t)to_i8_bits(__ldg(kp.cv_X + c * kp.cv_ldx + r0 + r), pb);
         }
+      }
+      if (kp.cv_pflag) {  // flag the piece's problem; its first flag counts it in *cv_flag
+        if (__any_sync(0xffffffffu, pb) && lane == 0 && atomicExch(kp.cv_pflag + c / kp.pR, 1) == 0)
+          atomicAdd(kp.cv_flag, 1);
+      } else {
+        bad |= pb;
       }
       __syncwarp();
       fence_proxy_async();  // this warp's reads of the buffer before the copy that overwrites it
@@ -909,7 +925,8 @@ constexpr int kConvSmem = 8192;
 __global__ void __launch_bounds__(kConvThreads, 4) oz_x_to_i8_kernel(const double* __restrict__ X, int64_t ldx,
                                                                      int64_t n, int64_t cols, int8_t* __restrict__ X8,
                                                                      int64_t ld8, int* __restrict__ flag,
-                                                                     unsigned long long* __restrict__ work) {
+                                                                     unsigned long long* __restrict__ work,
+                                                                     int* __restrict__ pflag, int pR) {
   __shared__ unsigned long long unit;
   const int64_t nunits = (cols + kConvCols - 1) / kConvCols;
   const uint32_t per_col = (uint32_t)((n + 255) >> 8);  // 256-row pieces per column
@@ -946,13 +963,20 @@ __global__ void __launch_bounds__(kConvThreads, 4) oz_x_to_i8_kernel(const doubl
         const int64_t r = (int64_t)(q - c * per_col) * 256;
         const double* src = X + (c0 + c) * ldx + r;
         int8_t* dst = X8 + (c0 + c) * ld8 + r;
+        int pb = 0;  // this piece holds a value the int8 path cannot take
         if (r + 256 <= n) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             *(uint16_t*)(dst + 2 * lane + 64 * k) =
-                (uint16_t)(to_i8_bits(v[j][k].x, bad) | to_i8_bits(v[j][k].y, bad) << 8);
+                (uint16_t)(to_i8_bits(v[j][k].x, pb) | to_i8_bits(v[j][k].y, pb) << 8);
         } else {  // the ragged end of the column
-          for (int64_t e = lane; r + e < n; e += 32) dst[e] = (int8_t)to_i8_bits(__ldcs(src + e), bad);
+          for (int64_t e = lane; r + e < n; e += 32) dst[e] = (int8_t)to_i8_bits(__ldcs(src + e), pb);
+        }
+        if (pflag) {  // flag the piece's problem; its first flag counts it in *flag
+          if (__any_sync(0xffffffffu, pb) && lane == 0 && atomicExch(pflag + (c0 + c) / pR, 1) == 0)
+            atomicAdd(flag, 1);
+        } else {
+          bad |= pb;
         }
       }
     }
@@ -1017,11 +1041,15 @@ cudaError_t launch_oz_variant(cudaStream_t s, const CUtensorMap& xmap, const CUt
 // [S_BL, S_BR]], [b_T; b_B] with S_TL, b_T from G, then the same posv_store as in the kernel.
 __global__ void __launch_bounds__(128) oz_posv_kernel(const double* __restrict__ rec, const double* __restrict__ G,
                                                       int pL, int pR, int64_t m_blk, const int* gate,
+                                                      const int* __restrict__ pflag, int64_t gate_all,
                                                       double* __restrict__ b_out, int32_t* __restrict__ st) {
-  if (gate && *(volatile const int*)gate != 0) return;
+  const int nflag = gate ? *(volatile const int*)gate : 0;
+  if (pflag ? nflag >= gate_all : nflag != 0) return;
+  const bool masked = pflag && nflag != 0;
   const int p = pL + pR, pl1 = pL + 1;
   const int64_t rs = (int64_t)pR * (pL + pR + 1);
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < m_blk; g += (int64_t)gridDim.x * blockDim.x) {
+    if (masked && pflag[g]) continue;  // the FP64 kernel solves this problem
     double S[400];
     double rhs[20];
     for (int a2 = 0; a2 < pL; ++a2) {
@@ -1109,7 +1137,7 @@ void oz_repack_rows(cudaStream_t s, const int8_t* src, int64_t n, int64_t rows, 
 }
 
 void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t cols, int8_t* X8,
-                int64_t ld8, int* flag, unsigned long long* work, int num_sms, int64_t* lc) {
+                int64_t ld8, int* flag, unsigned long long* work, int num_sms, int64_t* lc, int* pflag, int pR) {
   const int64_t nunits = (cols + kConvCols - 1) / kConvCols;
   int64_t blocks = (int64_t)num_sms * 4;
   if (blocks > nunits) blocks = nunits;
@@ -1117,7 +1145,8 @@ void oz_convert(cudaStream_t s, const double* X, int64_t ldx, int64_t n, int64_t
   // Used for the first chunk of a block (later chunks are converted by the solve kernel's
   // convert-ahead warps).  kConvSmem of (unused) dynamic shared memory keeps these blocks off SMs
   // that hold an int8 solve CTA: placed beside one, plain loads convert at ~1 GB/s per SM.
-  oz_x_to_i8_kernel<<<(unsigned)blocks, kConvThreads, kConvSmem, s>>>(X, ldx, n, cols, X8, ld8, flag, work);
+  oz_x_to_i8_kernel<<<(unsigned)blocks, kConvThreads, kConvSmem, s>>>(X, ldx, n, cols, X8, ld8, flag, work,
+                                                                      pflag, pR);
   if (lc) ++*lc;
 }
 
@@ -1171,6 +1200,9 @@ cudaError_t launch_ozaki_gls(cudaStream_t s, const OzArgs& a, int num_sms, std::
   kp.cv_X8 = a.cv_X8;
   kp.cv_ld8 = a.cv_ld8;
   kp.cv_flag = a.cv_flag;
+  kp.pflag = a.pflag;
+  kp.gate_all = a.gate_all;
+  kp.cv_pflag = a.cv_pflag;
   kp.cols = cols;
   kp.m_blk = a.m_blk;
   const int64_t cpt = 4 * (int64_t)cpw;
@@ -1227,7 +1259,8 @@ cudaError_t launch_ozaki_gls(cudaStream_t s, const OzArgs& a, int num_sms, std::
   if (lc) ++*lc;
   if (e == cudaSuccess && a.s_ws) {
     const int64_t blocks = (a.m_blk + 127) / 128 < 4 * num_sms ? (a.m_blk + 127) / 128 : 4 * num_sms;
-    oz_posv_kernel<<<(unsigned)blocks, 128, 0, s>>>(a.s_ws, a.G, a.pL, a.pR, a.m_blk, a.gate, a.b_out,
+    oz_posv_kernel<<<(unsigned)blocks, 128, 0, s>>>(a.s_ws, a.G, a.pL, a.pR, a.m_blk, a.gate, a.pflag, a.gate_all,
+                                                    a.b_out,
                                                     a.status_out);
     e = cudaGetLastError();
     if (lc) ++*lc;

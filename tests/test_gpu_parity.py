@@ -109,7 +109,9 @@ def test_ragged_shapes(glsmod, n, pL, pR, m, sex):
 
 def test_non_integer_block_falls_back_to_fp64(glsmod):
     """Imputed dosages (non-integer X_R) are not int8-representable: AUTO must run the FP64 kernel
-    for that block, decided on the device, and still match the oracle."""
+    for them, decided on the device, and still match the oracle.  The path is chosen per problem: a
+    single non-integer value sends only its own problem to the FP64 kernel -- that row equals the FP64
+    path's bit for bit, every other row the all-integer int8 run's."""
     n, pL, pR, m = 700, 3, 1, 300
     P = gen.make_problem(n, pL, pR, seed=21)
     XR = gen.make_XR(21, n, 0, m)
@@ -121,6 +123,7 @@ def test_non_integer_block_falls_back_to_fp64(glsmod):
     assert_parity(b, st, b_or, st_or, label="dosage fallback")
     # edge values of the int8 test: out of range, the int8 extremes, -0.0, a fraction in the last
     # row of the last column
+    b_int, _, _ = run_gpu(glsmod, P, dev(gen.make_XR(21, n, 0, m)), m, pR)
     for (i, r, v, fallback) in ((5, 17, 200.0, True), (5, 17, -128.0, False), (5, 17, 127.0, False),
                                 (5, 17, 128.0, True), (m - 1, n - 1, 1.5, True), (0, 0, -0.0, False),
                                 (3, 3, 1e-300, True), (3, 3, float("inf"), True)):
@@ -128,7 +131,12 @@ def test_non_integer_block_falls_back_to_fp64(glsmod):
         XR2[i, r] = v
         counts = []
         b2, st2, _ = run_gpu(glsmod, P, dev(XR2), m, pR, counts=counts)
-        assert counts == ([0, 1] if fallback else [1, 0]), (i, r, v, counts)
+        assert counts == ([1, 1] if fallback else [1, 0]), (i, r, v, counts)
+        others = np.arange(m) != i
+        np.testing.assert_array_equal(b2[others], b_int[others])
+        if fallback:
+            b64, _, _ = run_gpu(glsmod, P, dev(XR2), m, pR, path=glsmod.GLS_PATH_FP64)
+            np.testing.assert_array_equal(b2[i], b64[i])
         if np.isfinite(v):
             b_or2, st_or2 = oracle.solve(P.M, P.XL, P.y, XR2, pR)
             assert_parity(b2, st2, b_or2, st_or2, label="value %g" % v)
@@ -146,9 +154,49 @@ def test_mixed_chunks_pick_paths_independently(glsmod):
     b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR, pR)
     counts = []
     b, st, _ = run_gpu(glsmod, P, dev(XR), m, pR, counts=counts)
-    # the chunks holding only genotypes ran on int8, the one holding the dosage on FP64
-    assert counts[0] >= 1 and counts[1] == 1, counts
+    # every chunk ran on int8; the dosage's chunk also ran the FP64 kernel, for that one problem
+    assert counts[0] >= 2 and counts[1] == 1, counts
     assert_parity(b, st, b_or, st_or, label="mixed chunks")
+    XRi = XR.copy()
+    XRi[chunk + 123, 9] = 0.0
+    b_int, _, _ = run_gpu(glsmod, P, dev(XRi), m, pR)
+    others = np.arange(m) != chunk + 123
+    np.testing.assert_array_equal(b[others], b_int[others])
+
+
+def test_path_choice_is_per_problem_and_partition_independent(glsmod):
+    """SPEC's invariant that b is bitwise independent of the block partition holds for mixed data too:
+    non-integer problems scattered over a block (some in the same tile as integer ones, pR = 2 groups
+    with one bad column) give the same bits whether the block is solved in one call, split at ragged
+    points, or streamed from host memory in small host chunks; flagged rows equal the FP64 path's."""
+    n, pL, pR, m = 1200, 3, 2, 5000
+    P = gen.make_problem(n, pL, pR, seed=77)
+    XR = gen.make_XR(77, n, 0, m * pR)
+    bad_groups = [0, 1, 130, 131, 2047, 2048, m - 1]
+    for g in bad_groups:
+        XR[g * pR + (g % 2), (37 * g) % n] += 0.5
+    Xd = dev(XR)
+    b_one, st_one, _ = run_gpu(glsmod, P, Xd, m, pR)
+    b64, _, _ = run_gpu(glsmod, P, Xd, m, pR, path=glsmod.GLS_PATH_FP64)
+    np.testing.assert_array_equal(b_one[bad_groups], b64[bad_groups])
+    b_int, _, _ = run_gpu(glsmod, P, dev(np.rint(XR)), m, pR)
+    good = np.setdiff1d(np.arange(m), bad_groups)
+    np.testing.assert_array_equal(b_one[good], b_int[good])
+    with glsmod.Context(n, pL, pR, dev(P.M), dev(P.XL), dev(P.y)) as ctx:
+        for cuts in ((1, 2047), (131, 4999), (777, 2048, 3001)):
+            b = torch.empty((m, pL + pR), dtype=torch.float64, device="cuda")
+            edges = [0, *cuts, m]
+            for g0, g1 in zip(edges[:-1], edges[1:]):
+                ctx.solve_block(Xd[g0 * pR:g1 * pR], g1 - g0, b[g0:g1])
+            np.testing.assert_array_equal(b.cpu().numpy(), b_one)
+        Xh = torch.from_numpy(XR).pin_memory()
+        bh = torch.empty((m, pL + pR), dtype=torch.float64, pin_memory=True)
+        ctx.set_block_cols(640)
+        ctx.solve_block(Xh, m, bh)
+        np.testing.assert_array_equal(bh.numpy(), b_one)
+    b_or, st_or = oracle.solve(P.M, P.XL, P.y, XR[np.repeat(np.array(bad_groups) * pR, pR) +
+                                                  np.tile(np.arange(pR), len(bad_groups))], pR)
+    assert_parity(b_one[bad_groups], st_one[bad_groups], b_or, st_or, label="per-problem FP64 rows")
 
 
 @pytest.mark.parametrize("n", [4096, 4097])
@@ -177,9 +225,13 @@ def test_convert_ahead_chunks(glsmod, n):
         Xd2[col, n - 1] = value
         counts = []
         b2, st2, _ = run_gpu(glsmod, P, Xd2, m, pR, counts=counts)
-        assert counts == [counts0[0] - 1, 1], (col, value, counts, counts0)
+        assert counts == [counts0[0], 1], (col, value, counts, counts0)
         b64, st64, _ = run_gpu(glsmod, P, Xd2, m, pR, path=glsmod.GLS_PATH_FP64)
         assert_parity(b2, st2, b64, st64, label="int8 vs FP64 path, value %g" % value)
+        # per-problem path: only the touched problem ran on FP64 (its bits are the FP64 path's)
+        others = np.arange(m) != col
+        np.testing.assert_array_equal(b2[others], b[others])
+        np.testing.assert_array_equal(b2[col], b64[col])
         del Xd2
     # oracle on SNPs around the chunk boundaries and the ragged end
     pick = sorted({0, 1, m - 1, m - 2} | {x + d for x in (w, 3 * w, 4 * w, 5 * w) for d in (-1, 0)})
