@@ -92,6 +92,8 @@ struct KParams {
   int32_t* status_out;
   const int* gate;  // nullable: when set, run only if *gate != 0 (int8 path rejected the block)
   const int* pflag;  // nullable: solve and store only problems g with pflag[g] != 0; skip other panels
+  const int* m_dev;  // nullable: only the first min(m_blk, *m_dev) problems (a compacted block)
+  int gate_lo, gate_hi;  // with gate: run only if gate_lo < *gate <= gate_hi
   unsigned long long* ran;  // nullable: block 0 adds 1 when the kernel does its work
   int64_t m_blk;
   int64_t num_panels;
@@ -159,7 +161,8 @@ __device__ __forceinline__ void mma_frag(double (&acc)[4][4][2], const Frag& f) 
 
 // Per-problem path choice: a panel without a flagged problem is left to the int8 kernel (the producer and
 // every consumer decide alike from the same flags, so their stage counters stay in step).
-__device__ __forceinline__ bool panel_wanted(const KParams& kp, int64_t panel) {
+__device__ __forceinline__ bool panel_wanted(const KParams& kp, int64_t panel, int64_t m_eff) {
+  if (panel * kp.gpp >= m_eff) return false;
   if (!kp.pflag) return true;
   const int64_t g1 = (panel + 1) * kp.gpp < kp.m_blk ? (panel + 1) * kp.gpp : kp.m_blk;
   for (int64_t g = panel * kp.gpp; g < g1; ++g)
@@ -170,7 +173,12 @@ __device__ __forceinline__ bool panel_wanted(const KParams& kp, int64_t panel) {
 template <int NW, bool FULL, bool ALIGNED>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_trsm_gls_kernel(const __grid_constant__ CUtensorMap xmap, const KParams kp) {
-  if (kp.gate && *(volatile const int*)kp.gate == 0) return;  // uniform across the grid
+  if (kp.gate) {  // uniform across the grid
+    const int g = *(volatile const int*)kp.gate;
+    if (g <= kp.gate_lo || g > kp.gate_hi) return;
+  }
+  const int64_t m_eff = kp.m_dev && *(volatile const int*)kp.m_dev < kp.m_blk ? *(volatile const int*)kp.m_dev
+                                                                              : kp.m_blk;
   if (kp.ran && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(kp.ran, 1ull);
   using C = KCfg<NW, FULL>;
   extern __shared__ uint8_t smem_raw[];
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t rbc = 0;  // running row-block counter (W buffer = rbc & 1, its use = rbc >> 1)
       const uint32_t xbytes = (uint32_t)(kKT * kp.cpp * 8);
       for (int64_t panel = blockIdx.x; panel < kp.num_panels; panel += gridDim.x) {
-        if (!panel_wanted(kp, panel)) continue;
+        if (!panel_wanted(kp, panel, m_eff)) continue;
         const int col0 = (int)(panel * kp.cpp);
         for (int i = 0; i < NB; ++i, ++rbc) {
           const double* Trb = kp.Tpk + tpk_tile_offset(i) * kTileDoubles;
@@ -278,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t rbc = 0;
   Frag F0, F1;
   for (int64_t panel = blockIdx.x; panel < kp.num_panels; panel += gridDim.x) {
-    if (!panel_wanted(kp, panel)) continue;
+    if (!panel_wanted(kp, panel, m_eff)) continue;
     for (int i = 0; i < NB; ++i, ++rbc) {
 #pragma unroll
       for (int t = 0; t < 4; ++t)
@@ -377,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int gl = threadIdx.x;  // one thread per problem of the panel
     const int64_t gidx = panel * kp.gpp + gl;
-    if (gl < kp.gpp && gidx < kp.m_blk && !(kp.pflag && !kp.pflag[gidx])) {
+    if (gl < kp.gpp && gidx < m_eff && !(kp.pflag && !kp.pflag[gidx])) {
       const int pL = kp.pL, pR = kp.pR, p = kp.p;
       const int gmw = gl / kp.gw, gg = gl % kp.gw;
       const double* rd = sR + (size_t)gmw * C::kRedDoubles;
@@ -540,6 +548,96 @@ void pack_W(cudaStream_t s, const double* W, int64_t ld, int64_t n, int ncolsW, 
   if (lc) ++*lc;
 }
 
+// ---------------------------------------------------------------- compacted FP64 fallback (reading A16)
+// After a block's int8 launches, its flagged problems (usually few) are gathered into a dense block,
+// solved there by full panels (many SMs at once instead of one partly used panel per flagged problem,
+// each a long one-CTA trsm) and their records scattered back; the per-column arithmetic does not depend
+// on a column's panel position, so the bits are those of an in-place FP64 solve.  fb_index_kernel
+// writes the block's flagged count to *count (0 when none); the others run only if 0 < *count <= cap.
+__device__ __forceinline__ int gated_count(const int* count, int cap) {
+  const int c = *(volatile const int*)count;
+  return (c > 0 && c <= cap) ? c : 0;
+}
+// flagged problem indices in ascending order: one CTA, a block-wide scan per 1024 problems
+__global__ void __launch_bounds__(1024) fb_index_kernel(const int* __restrict__ pflag, int64_t groups,
+                                                        const int* __restrict__ ccount, int nchunks, int cap,
+                                                        int* __restrict__ idx, int* __restrict__ count) {
+  __shared__ int wsum[32];
+  __shared__ int base_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int j = 0; j < nchunks; ++j) t += ccount[j];  // the chunks' flagged counts
+    base_s = t;
+  }
+  __syncthreads();
+  const int total = base_s;
+  __syncthreads();
+  if (total == 0 || total > cap) {  // nothing to gather (none, or the in-place path takes them)
+    if (threadIdx.x == 0) *count = total;
+    return;
+  }
+  if (threadIdx.x == 0) base_s = 0;
+  __syncthreads();
+  for (int64_t g0 = 0; g0 < groups; g0 += 1024) {
+    const int64_t g = g0 + threadIdx.x;
+    const int f = (g < groups && pflag[g]) ? 1 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    const int wpre = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {  // inclusive scan of the 32 warp counts
+      int v = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    const int base = base_s;
+    if (f) idx[base + (warp ? wsum[warp - 1] : 0) + wpre] = (int)g;
+    __syncthreads();
+    if (threadIdx.x == 0) base_s = base + wsum[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = total;
+}
+// the flagged problems' pR columns (all ldx rows) -> the dense block Xc (same leading dimension)
+__global__ void fb_gather_kernel(const double* __restrict__ X, int64_t ldx, int pR, const int* __restrict__ idx,
+                                 const int* count, int cap, double* __restrict__ Xc) {
+  const int c = gated_count(count, cap);
+  for (int64_t col = blockIdx.x; col < (int64_t)c * pR; col += gridDim.x) {
+    const int64_t k = col / pR, a = col - k * pR;
+    const double2* src = (const double2*)(X + ((int64_t)idx[k] * pR + a) * ldx);
+    double2* dst = (double2*)(Xc + col * ldx);
+    for (int64_t r = threadIdx.x; r < ldx / 2; r += blockDim.x) dst[r] = src[r];
+  }
+}
+__global__ void fb_scatter_kernel(const double* __restrict__ bc, const int32_t* __restrict__ sc,
+                                  const int* __restrict__ idx, const int* count, int cap, int p,
+                                  double* __restrict__ b, int32_t* __restrict__ st) {
+  const int c = gated_count(count, cap);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)c * p;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = t / p, j = t - k * p;
+    b[(int64_t)idx[k] * p + j] = bc[t];
+    if (j == 0 && st) st[idx[k]] = sc[k];
+  }
+}
+void fb_compact(cudaStream_t s, const int* pflag, int64_t groups, const int* ccount, int nchunks, int cap, int* idx,
+                int* count, const double* X, int64_t ldx, int pR, double* Xc, int num_sms, int64_t* lc) {
+  fb_index_kernel<<<1, 1024, 0, s>>>(pflag, groups, ccount, nchunks, cap, idx, count);
+  fb_gather_kernel<<<(unsigned)(2 * num_sms), 256, 0, s>>>(X, ldx, pR, idx, count, cap, Xc);
+  if (lc) *lc += 2;
+}
+void fb_scatter(cudaStream_t s, const double* bc, const int32_t* sc, const int* idx, const int* count, int cap,
+                int p, double* b, int32_t* st, int num_sms, int64_t* lc) {
+  fb_scatter_kernel<<<(unsigned)num_sms, 256, 0, s>>>(bc, sc, idx, count, cap, p, b, st);
+  if (lc) ++*lc;
+}
+
 cudaError_t launch_fused_trsm_gls(cudaStream_t s, const SolveArgs& a, int num_sms, std::string* msg,
                                   int64_t* lc, const int* gate, unsigned long long* ran) {
   PFN_encodeTiled enc = get_encode();
@@ -575,6 +673,9 @@ cudaError_t launch_fused_trsm_gls(cudaStream_t s, const SolveArgs& a, int num_sm
   kp.status_out = a.status_out;
   kp.gate = gate;
   kp.pflag = a.pflag;
+  kp.m_dev = a.m_dev;
+  kp.gate_lo = a.gate_lo;
+  kp.gate_hi = a.gate_hi;
   kp.ran = ran;
   kp.m_blk = a.m_blk;
   kp.num_panels = (a.m_blk + pg.gpp - 1) / pg.gpp;

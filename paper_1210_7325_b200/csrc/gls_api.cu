@@ -85,6 +85,13 @@ struct gls_ctx {
   int64_t cflags_cap = 0;
   int* pflags = nullptr;                 // per problem of a block: 1 = holds a value int8 cannot take
   int64_t pflags_cap = 0;
+  // compacted FP64 fallback of a chunk's few flagged problems (fb_compact): indices, gathered columns
+  // (leading dimension fb_ldx), their records and statuses; fb_cap problems
+  int* fb_idx = nullptr;
+  double* fb_X = nullptr;
+  double* fb_b = nullptr;
+  int32_t* fb_s = nullptr;
+  int64_t fb_cap = 0, fb_ldx = 0;
   unsigned long long* ran = nullptr;     // [0] int8 kernel launches that ran, [1] FP64 ones
   cudaEvent_t ev_oz[2] = {}, ev_fb[2] = {};
   cudaStream_t fb = nullptr;  // gated FP64 fallback launches (off the int8 kernel's stream)
@@ -715,7 +722,8 @@ cudaEvent_t srep_mark(gls_ctx* c, cudaStream_t s) {
 }
 
 int run_fp64(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt,
-             const int* gate, cudaStream_t strm = nullptr, const int* pflag = nullptr) {
+             const int* gate, cudaStream_t strm = nullptr, const int* pflag = nullptr, const int* m_dev = nullptr,
+             int gate_lo = 0, int gate_hi = INT_MAX) {
   if (!strm) strm = c->stream;
   LaunchTimer lt(c, strm, 1);
   SolveArgs a;
@@ -732,6 +740,9 @@ int run_fp64(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b
   a.b_out = b;
   a.status_out = stt;
   a.pflag = pflag;
+  a.m_dev = m_dev;
+  a.gate_lo = gate_lo;
+  a.gate_hi = gate_hi;
   std::string msg;
   cudaError_t e = launch_fused_trsm_gls(strm, a, c->num_sms, &msg, &c->launches, gate, c->ran + 1);
   if (e != cudaSuccess) {
@@ -848,9 +859,10 @@ int run_kernel_int8_only(gls_ctx* c, const double* X, int64_t ldx, int64_t group
 // workspaces.  The path is chosen per problem: a problem whose pR columns hold a value that is not an
 // integer in [-128, 127] is flagged (pflags[g] = 1, counted in cflags[j]) and solved by the FP64 kernel,
 // every other problem by the int8 kernel -- so a problem's bits depend on its own values only, not on
-// its neighbours or the block partition.  For each chunk both kernels are launched, gated on the device
-// by the chunk's count (int8: skipped when every problem is flagged; FP64: when none is; it also skips
-// panels without a flagged problem), each storing only its own problems, and the host never waits.
+// its neighbours or the block partition.  Each chunk's int8 launch is gated on the device by the chunk's
+// count (skipped when every problem is flagged) and stores no flagged problem; after the last chunk the
+// FP64 kernel solves the block's flagged problems (compacted into a dense block when they fit, else in
+// place on the panels holding one), also gated on the device, and the host never waits.
 int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double* b, int32_t* stt) {
   if (!c->fp64_ok) return run_kernel_int8_only(c, X, ldx, groups, b, stt);
   if (c->path == GLS_PATH_FP64 || !c->oz_ok) return run_fp64(c, X, ldx, groups, b, stt, nullptr);
@@ -895,8 +907,27 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
     c->pflags_cap = cap;
   }
   int* const pf = c->pflags;
-  // the flags of the previous block were last read by its FP64 launches, which the compute stream
-  // waited for at the end of that block
+  // the FP64 fallback of the block's flagged problems runs after its int8 launches: up to fcap of them
+  // gathered into a dense block (kFbCompactBytes of columns), more in place on the panels holding one
+  constexpr size_t kFbCompactBytes = (size_t)512 << 20;
+  const int64_t gpp = panel_geom(pR).gpp;
+  int64_t fcap = std::min<int64_t>(groups, (int64_t)(kFbCompactBytes / ((size_t)pR * ldx * sizeof(double))));
+  fcap = std::max<int64_t>(fcap / gpp * gpp, gpp);
+  if (c->fb_cap < fcap || c->fb_ldx != ldx) {
+    if (c->fb_X) CK(c, cudaDeviceSynchronize());
+    dfree(c, c->fb_idx);
+    dfree(c, c->fb_X);
+    dfree(c, c->fb_b);
+    dfree(c, c->fb_s);
+    c->fb_cap = 0;
+    CK(c, walloc(c, &c->fb_idx, (size_t)(fcap + 1) * sizeof(int)));  // + the block's flagged count
+    CK(c, walloc(c, &c->fb_X, (size_t)fcap * pR * ldx * sizeof(double)));
+    CK(c, walloc(c, &c->fb_b, (size_t)fcap * p * sizeof(double)));
+    CK(c, walloc(c, &c->fb_s, (size_t)fcap * sizeof(int32_t)));
+    c->fb_cap = fcap;
+    c->fb_ldx = ldx;
+  }
+  // the flags of the previous block were last read by its FP64 launches on this stream
   CK(c, cudaMemsetAsync(c->cflags, 0, (size_t)nchunks * sizeof(int), c->stream));
   CK(c, cudaMemsetAsync(pf, 0, (size_t)groups * sizeof(int), c->stream));
   unsigned long long* work = (unsigned long long*)(c->flags + 2);
@@ -918,8 +949,6 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
       CK(c, cudaGetLastError());
     }
     // cflags[j] is final here (written by chunk j-1's kernel or a standalone pass)
-    CK(c, cudaEventRecord(c->ev_oz[buf], c->stream));
-    CK(c, cudaStreamWaitEvent(c->fb, c->ev_oz[buf], 0));
     double* bj = b + (size_t)g0 * p;
     int32_t* sj = stt ? stt + g0 : nullptr;
     if (ahead && j + 1 < nchunks)
@@ -928,15 +957,18 @@ int run_kernel(gls_ctx* c, const double* X, int64_t ldx, int64_t groups, double*
     else
       rc = run_int8(c, c->x8[buf], c->ld8, gc, bj, sj, c->cflags + j, nullptr, 0, 0, nullptr, nullptr, pf + g0);
     if (rc) return rc;
-    // the gated FP64 kernel runs on its own stream, so when it has nothing to do its launch never
-    // holds back the next int8 kernel
-    rc = run_fp64(c, X + (size_t)g0 * pR * ldx, ldx, gc, bj, sj, c->cflags + j, c->fb, pf + g0);
-    if (rc) return rc;
   }
-  // the block is complete on the compute stream only when its fallback launches are
-  CK(c, cudaEventRecord(c->ev_fb[0], c->fb));
-  CK(c, cudaStreamWaitEvent(c->stream, c->ev_fb[0], 0));
-  return GLS_OK;
+  // FP64 for the block's flagged problems, after every int8 launch (an FP64 panel is a long one-CTA
+  // trsm: beside a persistent int8 kernel it would hold back that kernel's last CTA pair), each launch
+  // gated on the device by the flagged count (all of them return at once for genotype blocks)
+  int* const fcount = c->fb_idx + fcap;
+  fb_compact(c->stream, pf, groups, c->cflags, (int)nchunks, (int)fcap, c->fb_idx, fcount, X, ldx, pR, c->fb_X,
+             c->num_sms, &c->launches);
+  rc = run_fp64(c, c->fb_X, ldx, fcap, c->fb_b, c->fb_s, fcount, c->stream, nullptr, fcount, 0, (int)fcap);
+  if (rc) return rc;
+  fb_scatter(c->stream, c->fb_b, c->fb_s, c->fb_idx, fcount, (int)fcap, p, b, stt, c->num_sms, &c->launches);
+  CK(c, cudaGetLastError());
+  return run_fp64(c, X, ldx, groups, b, stt, fcount, c->stream, pf, nullptr, (int)fcap, INT_MAX);
 }
 
 // Alg. 8 with host DRAM -> HBM in place of disk -> RAM: chunk j+1 is copied
@@ -1492,6 +1524,10 @@ void gls_destroy(gls_ctx* c) {
   dfree(c, c->flags);
   dfree(c, c->cflags);
   dfree(c, c->pflags);
+  dfree(c, c->fb_idx);
+  dfree(c, c->fb_X);
+  dfree(c, c->fb_b);
+  dfree(c, c->fb_s);
   dfree(c, c->ran);
   for (int k = 0; k < 2; ++k) {
     dfree(c, c->stage8[k]);

@@ -117,7 +117,19 @@ struct SolveArgs {
   // nullable per-problem path flags (int8 conversion): when set, only problems g with pflag[g] != 0 are
   // solved and stored (the int8 kernel stores the others), and panels without one are skipped
   const int* pflag = nullptr;
+  // nullable: only the first min(m_blk, *m_dev) problems exist (a compacted block, fb_compact)
+  const int* m_dev = nullptr;
+  // with a gate: run only if gate_lo < *gate <= gate_hi (default: *gate != 0 for counts)
+  int gate_lo = 0, gate_hi = 0x7fffffff;
 };
+// Compacted FP64 fallback (reading A16): fb_compact writes the block's flagged count (the sum of the
+// chunks' counts ccount[0, nchunks)) to *count and, when 0 < *count <= cap, the flagged problems'
+// indices (ascending) to idx and their columns gathered into Xc (leading dimension ldx); after the FP64
+// kernel has solved Xc (m_dev = count), fb_scatter writes its records / statuses back to b / st.
+void fb_compact(cudaStream_t s, const int* pflag, int64_t groups, const int* ccount, int nchunks, int cap, int* idx,
+                int* count, const double* X, int64_t ldx, int pR, double* Xc, int num_sms, int64_t* lc);
+void fb_scatter(cudaStream_t s, const double* bc, const int32_t* sc, const int* idx, const int* count, int cap,
+                int p, double* b, int32_t* st, int num_sms, int64_t* lc);
 // Returns cudaSuccess or the launch error; msg receives a description on failure.
 // gate (nullable, device): when non-null the kernel returns at once unless *gate != 0 (it is the
 // fallback for blocks the int8 path rejected).
