@@ -90,6 +90,9 @@ int gls_create_async(int64_t n, int32_t pL, int32_t pR, const double* M, const d
  *   b_out : m_blk x p, record i at b_out + i*p (host or device).  A RankDeficient problem
  *           (a pivot of its p x p Cholesky <= 1e-10 * S_jj, reading A4) gets a quiet-NaN record;
  *           the other problems are unaffected.
+ * Path (GLS_PATH_AUTO): per problem, on the device -- see gls_set_path.  Workspaces (kept by the
+ * context, from its stream-ordered pool): two int8 copies of up to 8 waves of X_R columns, one int per
+ * problem of the block, and up to 512 MB for the FP64 fallback's gathered columns.
  * Synchronous: returns after b_out is written. */
 int gls_solve_block(gls_ctx* ctx, const double* X_R, int64_t m_blk, double* b_out);
 
