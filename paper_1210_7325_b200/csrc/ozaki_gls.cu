@@ -803,41 +803,67 @@ __global__ void oz_rowscale_kernel(const double* __restrict__ rowmax, int64_t ro
 // 32i..32i+31, K columns 128c..128c+127; B row s*32 + rr holds digit s of row 32i + rr (plain
 // 128-byte rows; the TMA load applies the 128-byte swizzle).  Tiles of chunks owned by other ranks
 // are not written (the distributed create sums the ranks' zero-initialised T8 buffers).
-__global__ void oz_pack_kernel(const double* __restrict__ T, int64_t ld, int64_t n, ColOwn own,
-                               const int* __restrict__ escale, int NBR, int8_t* __restrict__ T8) {
+// T is column-major and the digit rows run along K, so the 32 x 128 block goes through shared memory:
+// read with a warp on 32 consecutive rows of one column (256 contiguous bytes), then thread (rr, kq)
+// converts K 16kq..16kq+15 of row rr and stores 16 bytes per digit -- the 8 threads of a row write its
+// 128 contiguous bytes.  Rows are padded to kPackLd doubles (even: 16-byte LDS; 2 extra doubles per
+// 16-K group, so a quarter-warp's LDS.128 of 8 groups hit distinct banks).
+constexpr int kPackGrp = 18;                 // 16 K + 2 pad doubles per group
+constexpr int kPackLd = 8 * kPackGrp + 2;    // 146 doubles per row
+__global__ void __launch_bounds__(256) oz_pack_kernel(const double* __restrict__ T, int64_t ld, int64_t n,
+                                                      ColOwn own, const int* __restrict__ escale, int NBR,
+                                                      int8_t* __restrict__ T8) {
+  __shared__ __align__(16) double sT[kR * kPackLd];
   const int64_t tile = blockIdx.x;
   int i = (int)sqrt(2.0 * (double)tile);  // invert oz_tile_offset
   while (i > 0 && oz_tile_offset(i) > tile) --i;
   while (i + 1 <= NBR && oz_tile_offset(i + 1) <= tile) ++i;
   const int c = (int)(tile - oz_tile_offset(i));
   if (!own.owned((int64_t)c * kKC)) return;  // a chunk lies inside one column block (nb % 128 == 0)
-  int8_t* dst = T8 + tile * (int64_t)kOzTileBytes;
-  // thread = (row rr of the block, 16 consecutive K): reads T column-major (a warp covers 32 rows of
-  // one column: coalesced), writes one 16-byte vector per digit
-  for (int u = threadIdx.x; u < kR * (kKC / 16); u += blockDim.x) {
-    const int rr = u & 31, kq = u >> 5;
+  {
+    const int rr = threadIdx.x & 31;
     const int64_t r = (int64_t)i * kR + rr;
-    const int e = (r < n) ? escale[r] : 0;
-    uint32_t d[kNSL][4];
+    double v[kR * kKC / 256];
 #pragma unroll
-    for (int s = 0; s < kNSL; ++s) d[s][0] = d[s][1] = d[s][2] = d[s][3] = 0;
+    for (int q = 0; q < kR * kKC / 256; ++q) {  // element (rr, k), k = warp + 8 q
+      const int k = (threadIdx.x >> 5) + 8 * q;
+      const int64_t j = (int64_t)c * kKC + k;
+      v[q] = (r < n && j <= r) ? T[r + own.local(j) * ld] : 0.0;
+    }
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      const int64_t j = (int64_t)c * kKC + kq * 16 + kk;
-      long long V = 0;
-      if (r < n && j <= r) V = llrint(ldexp(T[r + own.local(j) * ld], e + 48));
+    for (int q = 0; q < kR * kKC / 256; ++q) {
+      const int k = (threadIdx.x >> 5) + 8 * q;
+      sT[rr * kPackLd + (k >> 4) * kPackGrp + (k & 15)] = v[q];
+    }
+  }
+  __syncthreads();
+  const int rr = threadIdx.x >> 3, kq = threadIdx.x & 7;
+  const int64_t r = (int64_t)i * kR + rr;
+  const int e = (r < n) ? escale[r] : 0;
+  const double* src = sT + rr * kPackLd + kq * kPackGrp;
+  uint32_t d[kNSL][4];
+#pragma unroll
+  for (int s = 0; s < kNSL; ++s) d[s][0] = d[s][1] = d[s][2] = d[s][3] = 0;
+#pragma unroll
+  for (int kk = 0; kk < 16; kk += 2) {
+    const double2 x2 = *(const double2*)(src + kk);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      long long V = llrint(ldexp(h ? x2.y : x2.x, e + 48));
+      const int k = kk + h;
 #pragma unroll
       for (int s = kNSL - 1; s > 0; --s) {  // signed base-256 digits, least significant first
         const int8_t lo = (int8_t)(V & 0xff);
-        d[s][kk >> 2] |= (uint32_t)(uint8_t)lo << (8 * (kk & 3));
+        d[s][k >> 2] |= (uint32_t)(uint8_t)lo << (8 * (k & 3));
         V = (V - lo) >> 8;
       }
-      d[0][kk >> 2] |= (uint32_t)(uint8_t)(int8_t)V << (8 * (kk & 3));  // |top| <= 127
+      d[0][k >> 2] |= (uint32_t)(uint8_t)(int8_t)V << (8 * (k & 3));  // |top| <= 127
     }
-#pragma unroll
-    for (int s = 0; s < kNSL; ++s)
-      *(uint4*)(dst + (s * kR + rr) * kKC + kq * 16) = make_uint4(d[s][0], d[s][1], d[s][2], d[s][3]);
   }
+  int8_t* dst = T8 + tile * (int64_t)kOzTileBytes;
+#pragma unroll
+  for (int s = 0; s < kNSL; ++s)
+    *(uint4*)(dst + (s * kR + rr) * kKC + kq * 16) = make_uint4(d[s][0], d[s][1], d[s][2], d[s][3]);
 }
 
 // Column maxima of V = M^{-1} [X_L | y] (n x pl1) over the rows of owned chunks.  One CTA per column.
