@@ -46,3 +46,26 @@ def test_reference_arm_under_torchrun_prints_once():
     assert len(lines) == 1, lines
     d = _check_line(lines[0], 2)
     assert d["scaling"] == "strong"
+
+
+@pytest.mark.gpu
+def test_our_arm_json_line():
+    """The default arm on a small config: the base contract's keys plus roofline (with its measured
+    peak), cpu_baseline (the oracle), e2e (through the C ABI from host buffers, copies declared),
+    gpu_launches and the clocks sampled during the timed region."""
+    r = subprocess.run([sys.executable, "bench.py", "--config", "1", "--steps", "3", "--warmup", "3", "--no-sub"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, lines
+    d = json.loads(lines[0])
+    assert (KEYS - {"impl"}) | {"roofline", "gpu_launches", "clocks"} <= set(d)
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
+    rf = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(rf) and 0 < rf["frac"] < 1.2
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
